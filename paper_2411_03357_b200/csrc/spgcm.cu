@@ -1,0 +1,834 @@
+// libspgcm: AES-256-GCM seal/open for B200 (sm_100a) behind the C-ABI of
+// include/spgcm.h.  See DESIGN.md §3 for the layout and the roofline.
+//
+// Reference seam replaced: specpipe.channel.encrypt_at / decrypt_at
+// (/root/reference/pkg/src/specpipe/channel.py:85-115).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "spgcm.h"
+#include "spgcm_kernels.cuh"
+
+using namespace spgcm;
+
+// =============================================================================
+// Device: the batched seal/open kernel
+// =============================================================================
+
+__device__ __forceinline__ void fill_tables(uint8_t *sm, const KParams &p) {
+    // AES: 2 regions x 256 entries x 2 tables x 8 uint4 (4 copies each)
+    for (uint32_t f = threadIdx.x; f < 2u * 256u * 2u * 8u; f += blockDim.x) {
+        const uint32_t c4 = f & 7u, t = (f >> 3) & 1u, v = (f >> 4) & 255u, pr = f >> 12;
+        const uint32_t val = __ldg(p.ttab + (2u * pr + t) * 256u + v);
+        *reinterpret_cast<uint4 *>(sm + pr * 65536u + v * 256u + t * 128u + c4 * 16u) =
+            make_uint4(val, val, val, val);
+    }
+    // GHASH: 256 entries x (8 M copies + 8 uint4 of R8 copies)
+    for (uint32_t f = threadIdx.x; f < 256u * 16u; f += blockDim.x) {
+        const uint32_t s = f & 15u, v = f >> 4;
+        uint4 val;
+        if (s < 8u) {
+            val = __ldg(p.mg + v);
+        } else {
+            const uint32_t r = __ldg(p.ttab + 4u * 256u + v);
+            val = make_uint4(r, r, r, r);
+        }
+        *reinterpret_cast<uint4 *>(sm + kSmGh + v * 256u + s * 16u) = val;
+    }
+}
+
+__device__ __forceinline__ uint4 len_block(uint64_t len) {
+    const uint64_t bits = len * 8u;
+    return make_uint4(0u, 0u, bswap32((uint32_t)(bits >> 32)), bswap32((uint32_t)bits));
+}
+
+// Tag finalisation for one message; S = GHASH without E_K(J0).  Warp-uniform.
+__device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams &p, const MsgDev &md,
+                                               uint4 S, uint32_t x0, uint32_t x1, uint32_t x2,
+                                               uint32_t lct, int lane) {
+    const uint4 ek = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
+    const uint4 tag = xor4(S, ek);
+    if (!p.open) {
+        if (lane == 0) {
+            if ((reinterpret_cast<uintptr_t>(md.tag) & 15u) == 0)
+                *reinterpret_cast<uint4 *>(md.tag) = tag;
+            else
+                store_bytes(md.tag, tag, 16);
+        }
+        return;
+    }
+    uint32_t bad = 0;
+    if (lane == 0) {
+        const uint4 want = load_bytes(md.tag, 16);
+        bad = (want.x ^ tag.x) | (want.y ^ tag.y) | (want.z ^ tag.z) | (want.w ^ tag.w);
+        if (md.status) *md.status = bad ? 1 : 0;
+    }
+    bad = __shfl_sync(0xffffffffu, bad, 0);
+    if (bad) {
+        // unverified plaintext never leaves: zero the whole output
+        for (uint64_t k = (uint64_t)lane; k < md.len; k += 32) md.dst[k] = 0;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParams p) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    fill_tables(sm, p);
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint32_t lct = (uint32_t)lane * 4u;                  // T tables
+    const uint32_t lcm = (uint32_t)(lane & 7) * 16u;           // M_G copies
+    const uint32_t lcr = 128u + (uint32_t)lane * 4u;           // R8 copies
+
+    // contiguous, balanced row range for this warp
+    const uint64_t total = p.row_end - p.row_begin;
+    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+    uint64_t g = p.row_begin + (total * gw) / nw;
+    const uint64_t g_end = p.row_begin + (total * (gw + 1)) / nw;
+    if (g >= g_end) return;
+
+    // first message containing row g (binary search on row_begin)
+    uint32_t lo = 0, hi = p.nmsgs - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (p.msgs[mid].row_begin <= g) lo = mid; else hi = mid - 1;
+    }
+    uint32_t m = lo;
+
+    while (g < g_end) {
+        const MsgDev md = p.msgs[m];
+        const uint64_t t_a = g - md.row_begin;
+        const uint64_t t_b = min((uint64_t)md.rows, g_end - md.row_begin);
+        const int64_t nblk = (int64_t)((md.len + 15u) >> 4);
+        const int tail = (int)(md.len & 15u);
+        const bool vec = ((reinterpret_cast<uintptr_t>(md.src) | reinterpret_cast<uintptr_t>(md.dst)) & 15u) == 0;
+        const uint32_t x0 = bswap32(md.dir) ^ p.rk[0];
+        const uint32_t x1 = bswap32((uint32_t)(md.iv >> 32)) ^ p.rk[1];
+        const uint32_t x2 = bswap32((uint32_t)md.iv) ^ p.rk[2];
+        const int64_t base_i = nblk - 32 * (int64_t)md.rows + lane;  // block of this lane in local row 0
+
+        auto load_row = [&](uint64_t t) -> uint4 {
+            const int64_t i = base_i + 32 * (int64_t)t;
+            if (i < 0) return make_uint4(0, 0, 0, 0);
+            const int nb = (i == nblk - 1 && tail) ? tail : 16;
+            const uint8_t *ptr = md.src + 16 * i;
+            if (vec && nb == 16) return __ldcs(reinterpret_cast<const uint4 *>(ptr));
+            return load_bytes(ptr, nb);
+        };
+
+        uint4 y = make_uint4(0, 0, 0, 0);
+        uint4 cur = load_row(t_a);
+        for (uint64_t t = t_a; t < t_b; ++t) {
+            const uint4 nxt = (t + 1 < t_b) ? load_row(t + 1) : make_uint4(0, 0, 0, 0);
+            const int64_t i = base_i + 32 * (int64_t)t;
+            const uint32_t ctr = (uint32_t)(i + 2);
+            const uint4 ks = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(ctr) ^ p.rk[3]);
+            uint4 out = xor4(cur, ks);
+            uint4 gin = cur;
+            if (i >= 0) {
+                const int nb = (i == nblk - 1 && tail) ? tail : 16;
+                if (nb != 16) out = mask_bytes(out, nb);
+                uint8_t *dptr = md.dst + 16 * i;
+                if (vec && nb == 16) __stcs(reinterpret_cast<uint4 *>(dptr), out);
+                else store_bytes(dptr, out, nb);
+                if (!p.open) gin = out;
+            } else {
+                gin = make_uint4(0, 0, 0, 0);
+            }
+            y = (t == t_a) ? gin : xor4(gmul_g(sm, y, lcm, lcr), gin);
+            cur = nxt;
+        }
+
+        // combine lanes: W = sum_l Y_l * H^(32 - l)
+        uint4 w = warp_xor(nt_mul_lane(p.nt + (size_t)(kNtLane + 31 - lane) * kNtEntries, y));
+        // scale by H^(32*r_end + 1), r_end = rows after this run
+        const uint32_t r_end = md.rows - (uint32_t)t_b;
+        w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
+        if (r_end & 15u) w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+
+        const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);
+        if (t_a == 0 && t_b == md.rows) {
+            const uint4 S = xor4(w, warp_xor(lh_part));
+            finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
+        } else {
+            uint32_t *acc = p.acc + (size_t)m * 8u;
+            if (lane < 4) atomicXor(acc + lane, word_of(w, lane));
+            __threadfence();
+            __syncwarp();
+            uint32_t old = 0;
+            if (lane == 0) old = atomicAdd(acc + 4, (uint32_t)(t_b - t_a));
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old + (uint32_t)(t_b - t_a) == md.rows) {
+                __threadfence();
+                uint32_t v = 0;
+                if (lane < 4) v = atomicExch(acc + lane, 0u);
+                if (lane == 0) atomicExch(acc + 4, 0u);
+                uint4 a;
+                a.x = __shfl_sync(0xffffffffu, v, 0);
+                a.y = __shfl_sync(0xffffffffu, v, 1);
+                a.z = __shfl_sync(0xffffffffu, v, 2);
+                a.w = __shfl_sync(0xffffffffu, v, 3);
+                const uint4 S = xor4(a, warp_xor(lh_part));
+                finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
+            }
+        }
+        g = md.row_begin + t_b;
+        ++m;
+    }
+}
+
+// =============================================================================
+// Device: context setup (H, powers of H, tables) — runs once per key
+// =============================================================================
+
+struct G128 {
+    uint64_t hi, lo;  // big-endian halves of the 16-byte GCM string
+};
+
+__host__ __device__ inline G128 g_mulx(G128 v) {
+    const uint64_t lsb = v.lo & 1u;
+    v.lo = (v.lo >> 1) | (v.hi << 63);
+    v.hi >>= 1;
+    if (lsb) v.hi ^= 0xe100000000000000ull;
+    return v;
+}
+
+__host__ __device__ inline G128 g_mul(G128 x, G128 y) {
+    G128 z = {0, 0};
+    G128 v = y;
+    for (int i = 0; i < 128; ++i) {
+        const uint64_t bit = i < 64 ? (x.hi >> (63 - i)) & 1u : (x.lo >> (127 - i)) & 1u;
+        if (bit) { z.hi ^= v.hi; z.lo ^= v.lo; }
+        v = g_mulx(v);
+    }
+    return z;
+}
+
+__host__ __device__ inline uint32_t bs32(uint32_t x) {
+    return (x >> 24) | ((x >> 8) & 0xff00u) | ((x << 8) & 0xff0000u) | (x << 24);
+}
+
+__host__ __device__ inline uint4 g_to_words(G128 v) {
+    return make_uint4(bs32((uint32_t)(v.hi >> 32)), bs32((uint32_t)v.hi), bs32((uint32_t)(v.lo >> 32)),
+                      bs32((uint32_t)v.lo));
+}
+
+__host__ __device__ inline G128 g_from_words(uint4 w) {
+    G128 v;
+    v.hi = ((uint64_t)bs32(w.x) << 32) | bs32(w.y);
+    v.lo = ((uint64_t)bs32(w.z) << 32) | bs32(w.w);
+    return v;
+}
+
+__host__ __device__ inline G128 g_pow(G128 h, uint64_t e) {
+    G128 r = {0x8000000000000000ull, 0};  // 1 = x^0
+    G128 b = h;
+    while (e) {
+        if (e & 1u) r = g_mul(r, b);
+        b = g_mul(b, b);
+        e >>= 1;
+    }
+    return r;
+}
+
+// H = E_K(0^128): plain byte-wise AES in one thread.
+__global__ void k_setup_h(KParams p, const uint8_t *sbox, uint4 *out_h) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint8_t s[16];
+    const uint8_t *rk = reinterpret_cast<const uint8_t *>(p.rk);
+    for (int i = 0; i < 16; ++i) s[i] = rk[i];
+    auto xt = [](uint8_t a) -> uint8_t { return (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1b : 0)); };
+    for (int r = 1; r <= 14; ++r) {
+        uint8_t t[16];
+        for (int c = 0; c < 4; ++c)
+            for (int q = 0; q < 4; ++q) t[q + 4 * c] = sbox[s[q + 4 * ((c + q) & 3)]];
+        if (r != 14) {
+            for (int c = 0; c < 4; ++c) {
+                const uint8_t a0 = t[4 * c], a1 = t[4 * c + 1], a2 = t[4 * c + 2], a3 = t[4 * c + 3];
+                s[4 * c + 0] = xt(a0) ^ (xt(a1) ^ a1) ^ a2 ^ a3;
+                s[4 * c + 1] = a0 ^ xt(a1) ^ (xt(a2) ^ a2) ^ a3;
+                s[4 * c + 2] = a0 ^ a1 ^ xt(a2) ^ (xt(a3) ^ a3);
+                s[4 * c + 3] = (xt(a0) ^ a0) ^ a1 ^ a2 ^ xt(a3);
+            }
+        } else {
+            for (int i = 0; i < 16; ++i) s[i] = t[i];
+        }
+        for (int i = 0; i < 16; ++i) s[i] ^= rk[16 * r + i];
+    }
+    uint32_t w[4];
+    for (int k = 0; k < 4; ++k)
+        w[k] = (uint32_t)s[4 * k] | ((uint32_t)s[4 * k + 1] << 8) | ((uint32_t)s[4 * k + 2] << 16) |
+               ((uint32_t)s[4 * k + 3] << 24);
+    *out_h = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// powers[idx] for every nibble table, plus G = H^32 at powers[kNumNt]
+__global__ void k_setup_powers(const uint4 *hptr, uint4 *powers) {
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx > kNumNt) return;
+    const G128 h = g_from_words(*hptr);
+    uint64_t e;
+    if (idx < kNtF) e = idx + 1;                                   // H^1..H^32
+    else if (idx < kNtP32) e = 512ull * (idx - kNtF) + 1;          // F_a
+    else if (idx < kNumNt) e = 32ull * (idx - kNtP32 + 1);         // H^(32b)
+    else e = 32;                                                    // G
+    powers[idx] = g_to_words(g_pow(h, e));
+}
+
+// nibble tables: nt[t][q][v] = (nibble v at position q) * powers[t]
+__global__ void k_setup_nt(const uint4 *powers, uint4 *nt) {
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint64_t)kNumNt * kNtEntries) return;
+    const uint32_t t = (uint32_t)(idx / kNtEntries), q = (uint32_t)(idx % kNtEntries) / 16u, v = (uint32_t)idx & 15u;
+    // element with nibble v at nibble position q (MSB of the nibble = lowest degree)
+    const uint32_t shift_in_string = 124u - 4u * q;  // bit position from the right in a 128-bit BE int
+    G128 x = {0, 0};
+    if (shift_in_string >= 64) x.hi = (uint64_t)v << (shift_in_string - 64);
+    else x.lo = (uint64_t)v << shift_in_string;
+    nt[idx] = g_to_words(g_mul(x, g_from_words(powers[t])));
+}
+
+// M_G[v] = (byte v at position 0) * G
+__global__ void k_setup_mg(const uint4 *powers, uint4 *mg) {
+    const uint32_t v = threadIdx.x;
+    G128 x = {(uint64_t)v << 56, 0};
+    mg[v] = g_to_words(g_mul(x, g_from_words(powers[kNumNt])));
+}
+
+// =============================================================================
+// Host
+// =============================================================================
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    return fail(e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver || e == cudaErrorNoKernelImageForDevice
+                    ? SP_ENODEV
+                    : SP_ECUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define SP_CUDA(call, where)                          \
+    do {                                              \
+        cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+// FIPS-197 constants derived, not tabulated: S-box from GF(2^8) inverse + affine.
+struct Consts {
+    uint8_t sbox[256];
+    uint32_t t[4][256];
+    uint32_t r8[256];
+    Consts() {
+        auto mul = [](uint8_t a, uint8_t b) {
+            uint8_t r = 0;
+            for (int i = 0; i < 8; ++i) {
+                if (b & 1) r ^= a;
+                const uint8_t h = a & 0x80;
+                a <<= 1;
+                if (h) a ^= 0x1b;
+                b >>= 1;
+            }
+            return r;
+        };
+        for (int x = 0; x < 256; ++x) {
+            uint8_t inv = 0;
+            for (int y = 1; x && y < 256; ++y)
+                if (mul((uint8_t)x, (uint8_t)y) == 1) { inv = (uint8_t)y; break; }
+            uint8_t s = inv, r = inv;
+            for (int k = 0; k < 4; ++k) { r = (uint8_t)((r << 1) | (r >> 7)); s ^= r; }
+            sbox[x] = s ^ 0x63;
+        }
+        for (int x = 0; x < 256; ++x) {
+            const uint32_t s = sbox[x], s2 = mul(sbox[x], 2), s3 = mul(sbox[x], 3);
+            t[0][x] = s2 | (s << 8) | (s << 16) | (s3 << 24);
+            t[1][x] = s3 | (s2 << 8) | (s << 16) | (s << 24);
+            t[2][x] = s | (s3 << 8) | (s2 << 16) | (s << 24);
+            t[3][x] = s | (s << 8) | (s3 << 16) | (s2 << 24);
+        }
+        for (int v = 0; v < 256; ++v) {
+            // byte 15 = v, multiplied by x^8: result lives in bytes 0,1
+            G128 e = {0, (uint64_t)v};
+            for (int k = 0; k < 8; ++k) e = g_mulx(e);
+            const uint4 w = g_to_words(e);
+            r8[v] = w.x;
+        }
+    }
+};
+
+const Consts &consts() {
+    static Consts c;
+    return c;
+}
+
+void key_expand(const uint8_t key[32], uint32_t rk[60]) {
+    const Consts &c = consts();
+    uint8_t w[240];
+    memcpy(w, key, 32);
+    uint8_t rcon = 1;
+    for (int i = 8; i < 60; ++i) {
+        uint8_t t[4];
+        memcpy(t, w + 4 * (i - 1), 4);
+        if (i % 8 == 0) {
+            const uint8_t t0 = t[0];
+            t[0] = c.sbox[t[1]] ^ rcon;
+            t[1] = c.sbox[t[2]];
+            t[2] = c.sbox[t[3]];
+            t[3] = c.sbox[t0];
+            rcon = (uint8_t)((rcon << 1) ^ ((rcon & 0x80) ? 0x1b : 0));
+        } else if (i % 8 == 4) {
+            for (int k = 0; k < 4; ++k) t[k] = c.sbox[t[k]];
+        }
+        for (int k = 0; k < 4; ++k) w[4 * i + k] = w[4 * (i - 8) + k] ^ t[k];
+    }
+    memcpy(rk, w, 240);  // little-endian words == AES state column words
+}
+
+struct Workspace {
+    MsgDev *d_msgs = nullptr;
+    size_t cap_msgs = 0;
+    uint32_t *d_acc = nullptr;
+    size_t cap_acc = 0;
+    std::vector<MsgDev> h_msgs;
+};
+
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace *> g_ws;
+
+}  // namespace
+
+struct sp_ctx {
+    int device = 0;
+    int num_sms = 148;
+    uint32_t rk[60];
+    uint32_t *d_ttab = nullptr;  // T[4][256] + R8[256]
+    uint4 *d_mg = nullptr;
+    uint4 *d_nt = nullptr;
+    uint4 *d_pow = nullptr;      // kNumNt + 1 powers
+    uint8_t *d_sbox = nullptr;
+    uint4 *d_h = nullptr;
+};
+
+namespace {
+
+Workspace *workspace_for(int device, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto &w = g_ws[{device, s}];
+    if (!w) w = new Workspace();
+    return w;
+}
+
+KParams base_params(const sp_ctx *ctx) {
+    KParams p;
+    memset(&p, 0, sizeof(p));
+    memcpy(p.rk, ctx->rk, sizeof(p.rk));
+    p.ttab = ctx->d_ttab;
+    p.mg = ctx->d_mg;
+    p.nt = ctx->d_nt;
+    return p;
+}
+
+int check_desc(const sp_desc &d) {
+    if (d.len < 1 || d.len > SP_MAX_MESSAGE_BYTES) return fail(SP_EINVAL, "message length must be in 1..32 MiB");
+    if (d.dir > 1u) return fail(SP_EINVAL, "direction must be 0 (H2D) or 1 (D2H)");
+    if (!d.src || !d.dst || !d.tag) return fail(SP_EINVAL, "null buffer");
+    return SP_OK;
+}
+
+uint32_t rows_of(uint64_t len) { return (uint32_t)((((len + 15u) >> 4) + 31u) >> 5); }
+
+int grid_for(const sp_ctx *ctx, uint64_t rows) {
+    // >= 4 rows per warp before adding CTAs; at most one CTA per SM
+    const uint64_t want = (rows + (uint64_t)kWarpsPerCta * 4u - 1u) / ((uint64_t)kWarpsPerCta * 4u);
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->num_sms));
+}
+
+int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
+    if (ws->cap_msgs < nmsgs) {
+        if (ws->d_msgs) SP_CUDA(cudaFree(ws->d_msgs), "cudaFree");
+        size_t cap = std::max<size_t>(nmsgs, 256);
+        SP_CUDA(cudaMalloc(&ws->d_msgs, cap * sizeof(MsgDev)), "cudaMalloc(msgs)");
+        ws->cap_msgs = cap;
+    }
+    if (ws->cap_acc < nmsgs) {
+        if (ws->d_acc) SP_CUDA(cudaFree(ws->d_acc), "cudaFree");
+        size_t cap = std::max<size_t>(nmsgs, 256);
+        SP_CUDA(cudaMalloc(&ws->d_acc, cap * 8 * sizeof(uint32_t)), "cudaMalloc(acc)");
+        SP_CUDA(cudaMemsetAsync(ws->d_acc, 0, cap * 8 * sizeof(uint32_t), s), "cudaMemsetAsync(acc)");
+        ws->cap_acc = cap;
+    }
+    return SP_OK;
+}
+
+int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_end, cudaStream_t s) {
+    if (row_end <= row_begin) return SP_OK;
+    p.row_begin = row_begin;
+    p.row_end = row_end;
+    const int grid = grid_for(ctx, row_end - row_begin);
+    k_gcm<<<grid, kThreads, kSmemBytes, s>>>(p);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    SP_CUDA(cudaGetLastError(), "k_gcm launch");
+    return SP_OK;
+}
+
+// Build device message table for a batch; returns total rows.
+int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Workspace *ws, KParams &p,
+                uint64_t &rows, bool open) {
+    ws->h_msgs.resize((size_t)n);
+    rows = 0;
+    for (int i = 0; i < n; ++i) {
+        int rc = check_desc(d[i]);
+        if (rc) return rc;
+        if (open && !d[i].status) return fail(SP_EINVAL, "open needs a status pointer");
+        MsgDev &m = ws->h_msgs[(size_t)i];
+        m.src = static_cast<const uint8_t *>(d[i].src);
+        m.dst = static_cast<uint8_t *>(d[i].dst);
+        m.tag = static_cast<uint8_t *>(d[i].tag);
+        m.status = d[i].status;
+        m.len = d[i].len;
+        m.iv = d[i].iv;
+        m.dir = d[i].dir;
+        m.rows = rows_of(d[i].len);
+        m.row_begin = rows;
+        rows += m.rows;
+    }
+    int rc = ensure_ws(ws, (size_t)n, s);
+    if (rc) return rc;
+    SP_CUDA(cudaMemcpyAsync(ws->d_msgs, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev), cudaMemcpyHostToDevice, s),
+            "cudaMemcpyAsync(msgs)");
+    p = base_params(ctx);
+    p.msgs = ws->d_msgs;
+    p.acc = ws->d_acc;
+    p.nmsgs = (uint32_t)n;
+    p.open = open ? 1u : 0u;
+    return SP_OK;
+}
+
+int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, bool open) {
+    if (!ctx) return fail(SP_EINVAL, "null context");
+    if (n <= 0) return n == 0 ? SP_OK : fail(SP_EINVAL, "negative batch size");
+    if (!d) return fail(SP_EINVAL, "null descriptors");
+    SP_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    Workspace *ws = workspace_for(ctx->device, s);
+    KParams p;
+    uint64_t rows = 0;
+    int rc = stage_batch(ctx, d, n, s, ws, p, rows, open);
+    if (rc) return rc;
+    return launch_rows(ctx, p, 0, rows, s);
+}
+
+// ---- host-buffer pipeline ----------------------------------------------------
+// Pieces of ~kPieceBytes (whole rows) flow H2D (stream a) -> kernel (stream b)
+// -> D2H (stream c); each stage waits on the previous stage's event.
+constexpr uint64_t kPieceRows = (8ull << 20) / 512u;  // 8 MiB of payload per piece
+
+struct HostPipe {
+    int device = -1;
+    cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+    uint8_t *d_in = nullptr, *d_out = nullptr, *d_tags = nullptr;
+    int32_t *d_status = nullptr;
+    size_t cap_bytes = 0, cap_msgs = 0;
+    std::vector<cudaEvent_t> ev_in, ev_k;
+    std::mutex mu;
+};
+
+std::mutex g_pipes_mu;
+std::map<int, HostPipe *> g_pipes;
+
+HostPipe *pipe_for(int device) {
+    std::lock_guard<std::mutex> lk(g_pipes_mu);
+    auto &p = g_pipes[device];
+    if (!p) p = new HostPipe();
+    return p;
+}
+
+int ensure_pipe(HostPipe *hp, int device, size_t bytes, size_t nmsgs, size_t npieces) {
+    if (!hp->s_in) {
+        SP_CUDA(cudaStreamCreateWithFlags(&hp->s_in, cudaStreamNonBlocking), "stream");
+        SP_CUDA(cudaStreamCreateWithFlags(&hp->s_k, cudaStreamNonBlocking), "stream");
+        SP_CUDA(cudaStreamCreateWithFlags(&hp->s_out, cudaStreamNonBlocking), "stream");
+        hp->device = device;
+    }
+    if (hp->cap_bytes < bytes) {
+        if (hp->d_in) { cudaFree(hp->d_in); cudaFree(hp->d_out); }
+        size_t cap = std::max<size_t>(bytes, 1u << 20);
+        SP_CUDA(cudaMalloc(&hp->d_in, cap), "cudaMalloc(pipe in)");
+        SP_CUDA(cudaMalloc(&hp->d_out, cap), "cudaMalloc(pipe out)");
+        hp->cap_bytes = cap;
+    }
+    if (hp->cap_msgs < nmsgs) {
+        if (hp->d_tags) { cudaFree(hp->d_tags); cudaFree(hp->d_status); }
+        size_t cap = std::max<size_t>(nmsgs, 64);
+        SP_CUDA(cudaMalloc(&hp->d_tags, cap * 16), "cudaMalloc(pipe tags)");
+        SP_CUDA(cudaMalloc(&hp->d_status, cap * sizeof(int32_t)), "cudaMalloc(pipe status)");
+        hp->cap_msgs = cap;
+    }
+    while (hp->ev_in.size() < npieces) {
+        cudaEvent_t a, b;
+        SP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+        SP_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+        hp->ev_in.push_back(a);
+        hp->ev_k.push_back(b);
+    }
+    return SP_OK;
+}
+
+// byte range [lo, hi) of local rows [t0, t1) of a message of `len` bytes
+inline void rows_to_bytes(uint64_t len, uint32_t rows, uint64_t t0, uint64_t t1, uint64_t &lo, uint64_t &hi) {
+    const int64_t nblk = (int64_t)((len + 15u) >> 4);
+    const int64_t b0 = nblk - 32 * (int64_t)(rows - t0);
+    const int64_t b1 = nblk - 32 * (int64_t)(rows - t1);
+    lo = (uint64_t)std::max<int64_t>(0, b0) * 16u;
+    hi = std::min<uint64_t>(len, (uint64_t)std::max<int64_t>(0, b1) * 16u);
+}
+
+int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
+    if (!ctx) return fail(SP_EINVAL, "null context");
+    if (n <= 0) return n == 0 ? SP_OK : fail(SP_EINVAL, "negative batch size");
+    if (!d) return fail(SP_EINVAL, "null descriptors");
+    for (int i = 0; i < n; ++i) {
+        int rc = check_desc(d[i]);
+        if (rc) return rc;
+    }
+    SP_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    HostPipe *hp = pipe_for(ctx->device);
+    std::lock_guard<std::mutex> lk(hp->mu);
+
+    // device staging layout: messages packed at 256-byte aligned offsets
+    std::vector<uint64_t> off((size_t)n);
+    uint64_t total = 0, rows = 0;
+    for (int i = 0; i < n; ++i) {
+        off[(size_t)i] = total;
+        total += (d[i].len + 255u) & ~255ull;
+        rows += rows_of(d[i].len);
+    }
+    const size_t npieces = (size_t)((rows + kPieceRows - 1) / kPieceRows);
+    int rc = ensure_pipe(hp, ctx->device, total, (size_t)n, npieces);
+    if (rc) return rc;
+
+    std::vector<sp_desc> dd((size_t)n);
+    for (int i = 0; i < n; ++i) {
+        dd[(size_t)i] = d[i];
+        dd[(size_t)i].src = hp->d_in + off[(size_t)i];
+        dd[(size_t)i].dst = hp->d_out + off[(size_t)i];
+        dd[(size_t)i].tag = hp->d_tags + 16u * (size_t)i;
+        dd[(size_t)i].status = hp->d_status + i;
+    }
+    if (open) {
+        for (int i = 0; i < n; ++i)
+            SP_CUDA(cudaMemcpyAsync(hp->d_tags + 16u * (size_t)i, d[i].tag, 16, cudaMemcpyHostToDevice, hp->s_in),
+                    "cudaMemcpyAsync(tag)");
+    }
+    Workspace *ws = workspace_for(ctx->device, hp->s_k);
+    KParams p;
+    uint64_t rows_chk = 0;
+    rc = stage_batch(ctx, dd.data(), n, hp->s_k, ws, p, rows_chk, open);
+    if (rc) return rc;
+
+    // walk pieces of whole rows across the flattened batch
+    int mi = 0;
+    uint64_t g = 0;
+    size_t k = 0;
+    const std::vector<MsgDev> &msgs = ws->h_msgs;
+    while (g < rows) {
+        const uint64_t g_end = std::min(rows, g + kPieceRows);
+        // H2D for every message slice in [g, g_end)
+        int mj = mi;
+        uint64_t gg = g;
+        while (gg < g_end) {
+            const MsgDev &m = msgs[(size_t)mj];
+            const uint64_t t0 = gg - m.row_begin, t1 = std::min<uint64_t>(m.rows, g_end - m.row_begin);
+            uint64_t lo, hi;
+            rows_to_bytes(m.len, m.rows, t0, t1, lo, hi);
+            if (hi > lo)
+                SP_CUDA(cudaMemcpyAsync(hp->d_in + off[(size_t)mj] + lo, static_cast<const uint8_t *>(d[mj].src) + lo,
+                                        hi - lo, cudaMemcpyHostToDevice, hp->s_in),
+                        "cudaMemcpyAsync(H2D)");
+            gg = m.row_begin + t1;
+            if (t1 == m.rows) ++mj;
+        }
+        SP_CUDA(cudaEventRecord(hp->ev_in[k], hp->s_in), "event record");
+        SP_CUDA(cudaStreamWaitEvent(hp->s_k, hp->ev_in[k], 0), "wait");
+        rc = launch_rows(ctx, p, g, g_end, hp->s_k);
+        if (rc) return rc;
+        SP_CUDA(cudaEventRecord(hp->ev_k[k], hp->s_k), "event record");
+        SP_CUDA(cudaStreamWaitEvent(hp->s_out, hp->ev_k[k], 0), "wait");
+        // D2H of the same slices
+        gg = g;
+        while (gg < g_end) {
+            const MsgDev &m = msgs[(size_t)mi];
+            const uint64_t t0 = gg - m.row_begin, t1 = std::min<uint64_t>(m.rows, g_end - m.row_begin);
+            uint64_t lo, hi;
+            rows_to_bytes(m.len, m.rows, t0, t1, lo, hi);
+            if (hi > lo)
+                SP_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(d[mi].dst) + lo, hp->d_out + off[(size_t)mi] + lo,
+                                        hi - lo, cudaMemcpyDeviceToHost, hp->s_out),
+                        "cudaMemcpyAsync(D2H)");
+            gg = m.row_begin + t1;
+            if (t1 == m.rows) ++mi;
+        }
+        g = g_end;
+        ++k;
+    }
+    if (!open) {
+        for (int i = 0; i < n; ++i)
+            SP_CUDA(cudaMemcpyAsync(d[i].tag, hp->d_tags + 16u * (size_t)i, 16, cudaMemcpyDeviceToHost, hp->s_out),
+                    "cudaMemcpyAsync(tag D2H)");
+    }
+    std::vector<int32_t> st;
+    if (open) {
+        st.resize((size_t)n);
+        SP_CUDA(cudaMemcpyAsync(st.data(), hp->d_status, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                hp->s_out),
+                "cudaMemcpyAsync(status)");
+    }
+    SP_CUDA(cudaStreamSynchronize(hp->s_out), "cudaStreamSynchronize");
+    if (open) {
+        int bad = 0;
+        for (int i = 0; i < n; ++i) {
+            if (d[i].status) *d[i].status = st[(size_t)i];
+            if (st[(size_t)i]) {
+                // the device zeroed its copy, but the D2H of early pieces may
+                // have raced ahead of the verdict: scrub the host copy too
+                memset(d[i].dst, 0, d[i].len);
+                bad = 1;
+            }
+        }
+        if (bad) return fail(SP_EAUTH, "authentication failed");
+    }
+    return SP_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+
+extern "C" {
+
+const char *sp_last_error(void) { return g_err.c_str(); }
+const char *sp_version(void) { return "spgcm 0.1.0 sm_100a"; }
+uint64_t sp_launch_count(void) { return g_launches.load(); }
+
+int sp_ctx_create(const uint8_t key[SP_KEY_BYTES], sp_ctx **out) {
+    if (!key || !out) return fail(SP_EINVAL, "null argument");
+    *out = nullptr;
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaDeviceProp prop;
+    SP_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    if (prop.major != 10) return fail(SP_ENODEV, "libspgcm is built for sm_100a (B200) only");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+            "cudaFuncSetAttribute(k_gcm)");
+    sp_ctx *c = new sp_ctx();
+    c->device = dev;
+    c->num_sms = prop.multiProcessorCount;
+    key_expand(key, c->rk);
+    const Consts &k = consts();
+    auto bail = [&](int rc) {
+        sp_ctx_destroy(c);
+        return rc;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->d_ttab, 5 * 256 * sizeof(uint32_t))) ||
+        (e = cudaMalloc(&c->d_mg, 256 * sizeof(uint4))) ||
+        (e = cudaMalloc(&c->d_nt, (size_t)kNumNt * kNtEntries * sizeof(uint4))) ||
+        (e = cudaMalloc(&c->d_pow, (size_t)(kNumNt + 1) * sizeof(uint4))) ||
+        (e = cudaMalloc(&c->d_sbox, 256)) || (e = cudaMalloc(&c->d_h, sizeof(uint4))))
+        return bail(cuda_fail(e, "cudaMalloc(ctx)"));
+    if ((e = cudaMemcpy(c->d_ttab, k.t, sizeof(k.t), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(c->d_ttab + 4 * 256, k.r8, sizeof(k.r8), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(c->d_sbox, k.sbox, 256, cudaMemcpyHostToDevice)))
+        return bail(cuda_fail(e, "cudaMemcpy(ctx)"));
+    KParams p = base_params(c);
+    k_setup_h<<<1, 1>>>(p, c->d_sbox, c->d_h);
+    k_setup_powers<<<(kNumNt + 1 + 127) / 128, 128>>>(c->d_h, c->d_pow);
+    k_setup_nt<<<(unsigned)(((uint64_t)kNumNt * kNtEntries + 255) / 256), 256>>>(c->d_pow, c->d_nt);
+    k_setup_mg<<<1, 256>>>(c->d_pow, c->d_mg);
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    if ((e = cudaGetLastError()) || (e = cudaDeviceSynchronize())) return bail(cuda_fail(e, "ctx setup kernels"));
+    *out = c;
+    return SP_OK;
+}
+
+void sp_ctx_destroy(sp_ctx *c) {
+    if (!c) return;
+    cudaFree(c->d_ttab);
+    cudaFree(c->d_mg);
+    cudaFree(c->d_nt);
+    cudaFree(c->d_pow);
+    cudaFree(c->d_sbox);
+    cudaFree(c->d_h);
+    delete c;
+}
+
+int sp_ctx_round_keys(const sp_ctx *c, uint8_t out[240]) {
+    if (!c || !out) return fail(SP_EINVAL, "null argument");
+    memcpy(out, c->rk, 240);
+    return SP_OK;
+}
+
+int sp_ctx_hash_key(const sp_ctx *c, uint8_t out[16]) {
+    if (!c || !out) return fail(SP_EINVAL, "null argument");
+    SP_CUDA(cudaMemcpy(out, c->d_h, 16, cudaMemcpyDeviceToHost), "cudaMemcpy(H)");
+    return SP_OK;
+}
+
+int sp_seal_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
+    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), false);
+}
+
+int sp_open_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
+    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), true);
+}
+
+int sp_seal(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len, void *dst, void *tag16,
+            sp_stream_t stream) {
+    sp_desc d{dir, 0, iv, len, src, dst, tag16, nullptr};
+    return sp_seal_batch(ctx, &d, 1, stream);
+}
+
+int sp_open(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len, const void *tag16, void *dst,
+            int32_t *status_dev, sp_stream_t stream) {
+    sp_desc d{dir, 0, iv, len, src, dst, const_cast<void *>(tag16), status_dev};
+    return sp_open_batch(ctx, &d, 1, stream);
+}
+
+int sp_seal_host_batch(sp_ctx *ctx, const sp_desc *d, int n) { return run_host_batch(ctx, d, n, false); }
+
+int sp_open_host_batch(sp_ctx *ctx, const sp_desc *d, int n) { return run_host_batch(ctx, d, n, true); }
+
+int sp_seal_host(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len, void *dst,
+                 uint8_t tag16[SP_TAG_BYTES]) {
+    sp_desc d{dir, 0, iv, len, src, dst, tag16, nullptr};
+    return run_host_batch(ctx, &d, 1, false);
+}
+
+int sp_open_host(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len,
+                 const uint8_t tag16[SP_TAG_BYTES], void *dst) {
+    int32_t status = 0;
+    sp_desc d{dir, 0, iv, len, src, dst, const_cast<uint8_t *>(tag16), &status};
+    return run_host_batch(ctx, &d, 1, true);
+}
+
+}  // extern "C"

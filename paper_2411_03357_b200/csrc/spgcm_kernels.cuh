@@ -1,0 +1,206 @@
+// sm_100a device code for the AES-256-GCM seal/open path.
+//
+// Replaces the arithmetic the reference reaches through
+// `AESGCM(key).encrypt/decrypt` (channel.py:96 and channel.py:111-113).
+//
+// Design:
+//  * One persistent CTA per SM (512 threads, 192 KB of shared tables):
+//      [0,   64K)  AES T0/T1, entry v at v*256, T0 copy c at +4c, T1 at +128+4c
+//      [64K,128K)  AES T2/T3, same layout
+//      [128K,192K) GHASH: entry v at v*256, M_G[v] copy c (c<8) at +16c,
+//                  R8[v] copy c (c<32) at +128+4c
+//    Every lane reads its own copy, so the random-index lookups are
+//    bank-conflict free (LDS.32: bank = lane; LDS.128: bank group = lane&7).
+//    The 256-byte entry stride lets one PRMT build the full lookup offset
+//    (byte << 8 | lane constant).
+//  * Work unit = a "row" of 32 consecutive 16-byte GCM blocks, rows aligned
+//    to the END of each message.  Each warp takes a contiguous range of rows
+//    (whole batch flattened), so loads/stores are 512-byte coalesced and the
+//    GHASH Horner chain per lane runs with stride multiplier G = H^32.
+//  * A run of rows of one message ends with: lane multiply by H^(32-lane)
+//    (nibble tables in HBM), warp XOR-reduce, multiply by H^(32*r_end+1) =
+//    F[r_end/16] * H^(32*(r_end%16)) (lane-parallel nibble lookups), then
+//    either the final tag (run covers the message) or an atomic XOR into a
+//    per-message accumulator with a rows-done counter (last finisher tags).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spgcm {
+
+constexpr int kThreads = 512;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr uint64_t kMaxMsg = 32ull << 20;
+constexpr uint32_t kMaxRows = (uint32_t)((kMaxMsg / 16 + 31) / 32);  // 65536
+constexpr uint32_t kNumF = (kMaxRows + 15) / 16;                     // 4096
+// nibble-table index layout (each table: 32 positions x 16 values x uint4)
+constexpr uint32_t kNtLane = 0;          // H^e, e = 1..32  -> index e-1
+constexpr uint32_t kNtF = 32;            // F_a = H^(512a+1), a < kNumF
+constexpr uint32_t kNtP32 = 32 + kNumF;  // H^(32b), b = 1..15 -> kNtP32 + b - 1
+constexpr uint32_t kNumNt = kNtP32 + 15;
+constexpr uint32_t kNtEntries = 32 * 16;
+
+constexpr uint32_t kSmAes0 = 0;
+constexpr uint32_t kSmAes1 = 65536;
+constexpr uint32_t kSmGh = 131072;
+constexpr uint32_t kSmemBytes = 196608;
+
+struct MsgDev {
+    const uint8_t *src;
+    uint8_t *dst;
+    uint8_t *tag;
+    int32_t *status;
+    uint64_t len;
+    uint64_t iv;
+    uint64_t row_begin;  // global row index of this message's first row
+    uint32_t rows;
+    uint32_t dir;
+};
+
+struct KParams {
+    uint32_t rk[60];
+    const uint32_t *ttab;  // T0..T3 [4][256] then R8[256]
+    const uint4 *mg;       // M_G[256], G = H^32
+    const uint4 *nt;       // nibble tables [kNumNt][32][16]
+    const MsgDev *msgs;
+    uint32_t *acc;         // per message: 4 words XOR accumulator + rows done (stride 8)
+    uint64_t row_begin;    // rows [row_begin, row_end) of the flattened batch
+    uint64_t row_end;
+    uint32_t nmsgs;
+    uint32_t open;
+};
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ uint32_t word_of(const uint4 &v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+
+// ---- AES-256 on lane-replicated T-tables ------------------------------------
+// PRMT selector building (w.byte_k << 8) | lane*4: out b0 = lc.b0, b1 = w.bk,
+// b2 = b3 = lc.b1 (= 0).
+#define SP_SEL(k) (0x5504u | ((uint32_t)(k) << 4))
+
+__device__ __forceinline__ uint32_t tl(const uint8_t *sm, uint32_t off, uint32_t w, uint32_t sel,
+                                       uint32_t lc) {
+    return *reinterpret_cast<const uint32_t *>(sm + off + __byte_perm(w, lc, sel));
+}
+
+// s0..s3: counter block words already XORed with round key 0.
+__device__ __forceinline__ uint4 aes256_rounds(const uint8_t *sm, const uint32_t *rk, uint32_t lc,
+                                               uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+#pragma unroll
+    for (int r = 1; r < 14; ++r) {
+        const uint32_t t0 = tl(sm, kSmAes0, s0, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s1, SP_SEL(1), lc) ^
+                            tl(sm, kSmAes1, s2, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s3, SP_SEL(3), lc) ^
+                            rk[4 * r + 0];
+        const uint32_t t1 = tl(sm, kSmAes0, s1, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s2, SP_SEL(1), lc) ^
+                            tl(sm, kSmAes1, s3, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s0, SP_SEL(3), lc) ^
+                            rk[4 * r + 1];
+        const uint32_t t2 = tl(sm, kSmAes0, s2, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s3, SP_SEL(1), lc) ^
+                            tl(sm, kSmAes1, s0, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s1, SP_SEL(3), lc) ^
+                            rk[4 * r + 2];
+        const uint32_t t3 = tl(sm, kSmAes0, s3, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s0, SP_SEL(1), lc) ^
+                            tl(sm, kSmAes1, s1, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s2, SP_SEL(3), lc) ^
+                            rk[4 * r + 3];
+        s0 = t0; s1 = t1; s2 = t2; s3 = t3;
+    }
+    // Final round: S-box bytes come out of the T-tables: T2 has S at byte 0,
+    // T3 at byte 1, T0 at byte 2, T1 at byte 3.
+    uint4 o;
+#define SP_LAST(ca, cb, cc, cd, k)                                                        \
+    ((tl(sm, kSmAes1, ca, SP_SEL(0), lc) & 0x000000ffu) |                                 \
+     (tl(sm, kSmAes1 + 128, cb, SP_SEL(1), lc) & 0x0000ff00u) |                           \
+     (tl(sm, kSmAes0, cc, SP_SEL(2), lc) & 0x00ff0000u) |                                 \
+     (tl(sm, kSmAes0 + 128, cd, SP_SEL(3), lc) & 0xff000000u)) ^ rk[56 + k]
+    o.x = SP_LAST(s0, s1, s2, s3, 0);
+    o.y = SP_LAST(s1, s2, s3, s0, 1);
+    o.z = SP_LAST(s2, s3, s0, s1, 2);
+    o.w = SP_LAST(s3, s0, s1, s2, 3);
+#undef SP_LAST
+    return o;
+}
+
+// ---- GHASH: Y * G with an 8-bit Shoup table in shared memory ----------------
+// Element layout: little-endian 32-bit words of the 16-byte GCM string
+// (byte 0 holds coefficients x^0..x^7, MSB first).  Multiplying by x^8 moves
+// every byte one position up; byte 15 falls off and is folded back with R8.
+__device__ __forceinline__ uint4 gmul_g(const uint8_t *sm, uint4 y, uint32_t lcm, uint32_t lcr) {
+    const uint8_t *gh = sm + kSmGh;
+    uint4 z = *reinterpret_cast<const uint4 *>(gh + __byte_perm(y.w, lcm, SP_SEL(3)));
+#pragma unroll
+    for (int b = 14; b >= 0; --b) {
+        const uint32_t raddr = __byte_perm(z.w, lcr, SP_SEL(3));
+        z.w = __funnelshift_l(z.z, z.w, 8);
+        z.z = __funnelshift_l(z.y, z.z, 8);
+        z.y = __funnelshift_l(z.x, z.y, 8);
+        z.x = z.x << 8;
+        const uint32_t r = *reinterpret_cast<const uint32_t *>(gh + raddr);
+        const uint4 m = *reinterpret_cast<const uint4 *>(gh + __byte_perm(word_of(y, b >> 2), lcm, SP_SEL(b & 3)));
+        z.x ^= r ^ m.x;
+        z.y ^= m.y;
+        z.z ^= m.z;
+        z.w ^= m.w;
+    }
+    return z;
+}
+
+// ---- nibble-table multiplies (HBM/L2 resident tables) ----------------------
+__device__ __forceinline__ uint32_t nibble_of(const uint4 &v, int q) {
+    const uint32_t byte = (word_of(v, q >> 3) >> (8 * ((q >> 1) & 3))) & 0xffu;
+    return (q & 1) ? (byte & 15u) : (byte >> 4);
+}
+
+// Full multiply by the table's element, done by one lane (32 lookups).
+__device__ __forceinline__ uint4 nt_mul_lane(const uint4 *tab, uint4 v) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc = xor4(acc, __ldg(tab + q * 16 + nibble_of(v, q)));
+    return acc;
+}
+
+__device__ __forceinline__ uint4 warp_xor(uint4 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v.x ^= __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y ^= __shfl_xor_sync(0xffffffffu, v.y, o);
+        v.z ^= __shfl_xor_sync(0xffffffffu, v.z, o);
+        v.w ^= __shfl_xor_sync(0xffffffffu, v.w, o);
+    }
+    return v;
+}
+
+// Lane-parallel partial product: lane q looks up nibble q (v warp-uniform).
+__device__ __forceinline__ uint4 nt_part(const uint4 *tab, uint4 v, int lane) {
+    return __ldg(tab + lane * 16 + nibble_of(v, lane));
+}
+
+// ---- block load / store ------------------------------------------------------
+__device__ __forceinline__ uint4 load_bytes(const uint8_t *p, int n) {
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int k = 0; k < n; ++k) w[k >> 2] |= (uint32_t)p[k] << (8 * (k & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void store_bytes(uint8_t *p, uint4 v, int n) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int k = 0; k < n; ++k) p[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+}
+
+__device__ __forceinline__ uint4 mask_bytes(uint4 v, int n) {
+    // keep bytes [0, n), zero the rest (n in 1..15)
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int keep = n - 4 * k;
+        w[k] = keep >= 4 ? w[k] : (keep <= 0 ? 0u : (w[k] & ((1u << (8 * keep)) - 1u)));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+}  // namespace spgcm

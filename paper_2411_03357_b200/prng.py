@@ -1,0 +1,71 @@
+"""Bit-exact, fast `prng_fill` (memory.py:106-110) and the seeded payload
+sources of the reference (`simulator.py:185-190`: small-I/O and app-write
+payloads; `engine.py:214,401`: the engine's own small-I/O RNG).
+
+The reference produces payloads with `random.Random(seed).randbytes(n)`, i.e.
+`getrandbits(8n).to_bytes(n, "little")` over CPython's MT19937.  Here the
+initial MT state comes from CPython itself (`Random(seed).getstate()`, so int
+and str seeding are exact), and the bulk stream is drawn from numpy's MT19937
+with that state injected — same generator, ~50x faster than the reference's
+0.18 GB/s, which matters for 600 MB OPT layers.
+"""
+from __future__ import annotations
+
+import random
+from typing import Callable
+
+import numpy as np
+
+_CHUNK_WORDS = 1 << 22
+
+
+def _bitgen_for(seed) -> np.random.MT19937:
+    st = random.Random(seed).getstate()[1]
+    bg = np.random.MT19937()
+    bg.state = {
+        "bit_generator": "MT19937",
+        "state": {"key": np.asarray(st[:624], dtype=np.uint32), "pos": int(st[624])},
+    }
+    return bg
+
+
+def random_bytes(seed, n: int, out: np.ndarray | None = None) -> np.ndarray:
+    """`random.Random(seed).randbytes(n)` as a uint8 numpy array."""
+    if n < 0:
+        raise ValueError("negative length")
+    res = out if out is not None else np.empty(n, dtype=np.uint8)
+    if n == 0:
+        return res
+    bg = _bitgen_for(seed)
+    full, rem = divmod(n, 4)
+    pos = 0
+    words_left = full
+    while words_left:
+        k = min(words_left, _CHUNK_WORDS)
+        w = bg.random_raw(k).astype("<u4")
+        res[pos:pos + 4 * k] = w.view(np.uint8)
+        pos += 4 * k
+        words_left -= k
+    if rem:
+        last = int(bg.random_raw(1)[0]) >> (32 - 8 * rem)
+        res[pos:pos + rem] = np.frombuffer(last.to_bytes(4, "little")[:rem], dtype=np.uint8)
+    return res
+
+
+def prng_fill(seed: int) -> Callable[[int], bytes]:
+    """Drop-in for specpipe.memory.prng_fill (memory.py:106-110)."""
+
+    def fill(n: int) -> bytes:
+        return random_bytes(seed, n).tobytes()
+
+    return fill
+
+
+def small_io_payload(seed: int, index: int, size: int) -> bytes:
+    """simulator.py:185-186."""
+    return random_bytes(f"smallio:{seed}:{index}", size).tobytes()
+
+
+def app_write_payload(data_seed: int, size: int) -> bytes:
+    """simulator.py:189-190."""
+    return random_bytes(f"appwrite:{data_seed}", size).tobytes()

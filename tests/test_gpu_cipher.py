@@ -1,0 +1,256 @@
+"""GPU parity of the sm_100a AES-256-GCM kernels against the golden vectors
+produced by the reference itself (tests/golden/cipher_vectors.json) and against
+the CPU oracles (oracle.gcm plain-C restatement, oracle.port = cryptography,
+the reference's own dependency).  Bit-exact: ciphertext, tags and plaintext.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from oracle import gcm as oracle_gcm
+from oracle import port as oracle_port
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cipher_vectors.json")))
+MIB = 1 << 20
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    torch.cuda.set_device(0)
+    return torch
+
+
+@pytest.fixture(scope="module")
+def ctx_for(torch_cuda):
+    from paper_2411_03357_b200.gcm import GcmContext
+
+    cache = {}
+
+    def get(key: bytes):
+        if key not in cache:
+            cache[key] = GcmContext(key)
+        return cache[key]
+
+    return get
+
+
+def _payload(v):
+    from paper_2411_03357_b200 import prng
+
+    if "p_hex" in v:
+        return bytes.fromhex(v["p_hex"])
+    return prng.random_bytes(v["payload_seed"], v["len"]).tobytes()
+
+
+def _dev(torch, b: bytes):
+    return torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+
+
+def _host(t) -> bytes:
+    return t.cpu().numpy().tobytes()
+
+
+def _check_vec(v, c: bytes, tag: bytes):
+    assert tag.hex() == v["tag"], (v["len"], v["iv"], v["dir"])
+    if "c_hex" in v:
+        assert c.hex() == v["c_hex"]
+    assert hashlib.sha256(c).hexdigest() == v["sha256_c"]
+
+
+def test_tc14_and_hash_key(ctx_for, torch_cuda):
+    torch = torch_cuda
+    ctx = ctx_for(bytes(32))
+    assert ctx.round_keys() == oracle_gcm.key_expand(bytes(32))
+    assert ctx.hash_key() == oracle_gcm.aes_block(bytes(32), bytes(16))
+    src = _dev(torch, bytes(16))
+    dst = torch.empty_like(src)
+    tag = torch.empty(16, dtype=torch.uint8, device="cuda")
+    ctx.seal_device(0, 0, src, dst, tag)
+    torch.cuda.synchronize()
+    assert _host(dst).hex() == "cea7403d4d606b6e074ec5d3baf39d18"
+    assert _host(tag).hex() == "d0d1c8a799996bf0265b98b5d48ab919"
+
+
+def test_golden_vectors_one_by_one(ctx_for, torch_cuda):
+    """Every reference-generated vector, each in its own launch; open round trip."""
+    torch = torch_cuda
+    for v in GOLD["vectors"]:
+        key = bytes.fromhex(v["key"])
+        ctx = ctx_for(key)
+        p = _payload(v)
+        assert hashlib.sha256(p).hexdigest() == v["sha256_p"]
+        src = _dev(torch, p)
+        dst = torch.empty_like(src)
+        tag = torch.empty(16, dtype=torch.uint8, device="cuda")
+        iv = int(v["iv"])
+        ctx.seal_device(v["dir"], iv, src, dst, tag)
+        back = torch.empty_like(src)
+        st = torch.full((1,), 7, dtype=torch.int32, device="cuda")
+        ctx.open_device(v["dir"], iv, dst, back, tag, st)
+        torch.cuda.synchronize()
+        _check_vec(v, _host(dst), _host(tag))
+        assert int(st.item()) == 0
+        assert torch.equal(back, src)
+
+
+def test_golden_vectors_single_batch(ctx_for, torch_cuda):
+    """All vectors of one key in ONE launch (K3 descriptor batch)."""
+    torch = torch_cuda
+    by_key = {}
+    for v in GOLD["vectors"]:
+        by_key.setdefault(v["key"], []).append(v)
+    for khex, vs in by_key.items():
+        ctx = ctx_for(bytes.fromhex(khex))
+        srcs = [_dev(torch, _payload(v)) for v in vs]
+        dsts = [torch.empty_like(s) for s in srcs]
+        tags = torch.empty((len(vs), 16), dtype=torch.uint8, device="cuda")
+        items = [(v["dir"], int(v["iv"]), s, d, tags[i]) for i, (v, s, d) in enumerate(zip(vs, srcs, dsts))]
+        ctx.seal_batch(items)
+        backs = [torch.empty_like(s) for s in srcs]
+        st = torch.full((len(vs),), 7, dtype=torch.int32, device="cuda")
+        ctx.open_batch([(v["dir"], int(v["iv"]), d, b, tags[i]) for i, (v, d, b) in
+                        enumerate(zip(vs, dsts, backs))], st)
+        torch.cuda.synchronize()
+        for i, v in enumerate(vs):
+            _check_vec(v, _host(dsts[i]), _host(tags[i]))
+            assert torch.equal(backs[i], srcs[i])
+        assert int(st.abs().sum().item()) == 0
+
+
+def test_random_sizes_vs_oracles(ctx_for, torch_cuda):
+    torch = torch_cuda
+    rng = random.Random(1234)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    sizes = [rng.randrange(1, 70000) for _ in range(60)] + [rng.randrange(1, 3 * MIB) for _ in range(12)]
+    items, refs, srcs = [], [], []
+    tags = torch.empty((len(sizes), 16), dtype=torch.uint8, device="cuda")
+    for i, n in enumerate(sizes):
+        p = rng.randbytes(n)
+        iv = rng.choice([0, 1, rng.randrange(1 << 64), (1 << 64) - 1, (1 << 32) - 1])
+        d = rng.randrange(2)
+        src = _dev(torch, p)
+        dst = torch.empty_like(src)
+        srcs.append(src)
+        items.append((d, iv, src, dst, tags[i]))
+        refs.append(oracle_port.seal(key, d, iv, p) if n > 4096 else oracle_gcm.seal(key, d, iv, p))
+    ctx.seal_batch(items)
+    torch.cuda.synchronize()
+    for i, (c, t) in enumerate(refs):
+        assert _host(items[i][3]) == c, sizes[i]
+        assert _host(tags[i]) == t, sizes[i]
+
+
+def test_unaligned_and_inplace(ctx_for, torch_cuda):
+    torch = torch_cuda
+    key = bytes(range(100, 132))
+    ctx = ctx_for(key)
+    rng = random.Random(5)
+    big = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    for so, do, n in [(1, 3, 1000), (15, 0, 4097), (0, 7, 65536 + 9), (5, 5, 33), (8, 12, 300000)]:
+        p = rng.randbytes(n)
+        big[so:so + n] = torch.frombuffer(bytearray(p), dtype=torch.uint8).cuda()
+        out = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+        tag = torch.empty(17, dtype=torch.uint8, device="cuda")
+        ctx.seal_batch([(1, 99, big[so:so + n], out[do:do + n], tag[1:17])])
+        torch.cuda.synchronize()
+        c, t = oracle_port.seal(key, 1, 99, p)
+        assert _host(out[do:do + n]) == c
+        assert _host(tag[1:17]) == t
+        assert int(out[:do].abs().sum()) == 0 and int(out[do + n:].abs().sum()) == 0
+    # in place
+    p = rng.randbytes(100003)
+    buf = _dev(torch, p)
+    tag = torch.empty(16, dtype=torch.uint8, device="cuda")
+    ctx.seal_device(0, 5, buf, buf, tag)
+    torch.cuda.synchronize()
+    c, t = oracle_port.seal(key, 0, 5, p)
+    assert _host(buf) == c and _host(tag) == t
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.open_device(0, 5, buf, buf, tag, st)
+    torch.cuda.synchronize()
+    assert _host(buf) == p and int(st.item()) == 0
+
+
+def test_tamper_rejected_and_zeroed(ctx_for, torch_cuda):
+    """Bit flips in payload or tag, wrong IV, wrong direction -> status 1 and
+    no plaintext released (channel.py:110-115 AuthError semantics)."""
+    torch = torch_cuda
+    key = bytes(range(32, 64))
+    ctx = ctx_for(key)
+    rng = random.Random(9)
+    for n in (1, 16, 17, 5000, 2 * MIB + 3):
+        p = rng.randbytes(n)
+        src = _dev(torch, p)
+        ct = torch.empty_like(src)
+        tag = torch.empty(16, dtype=torch.uint8, device="cuda")
+        ctx.seal_device(0, 77, src, ct, tag)
+        cases = []
+        c2 = ct.clone(); c2[rng.randrange(n)] ^= 1 << rng.randrange(8); cases.append((0, 77, c2, tag))
+        t2 = tag.clone(); t2[rng.randrange(16)] ^= 0x80; cases.append((0, 77, ct, t2))
+        cases.append((0, 78, ct, tag))
+        cases.append((1, 77, ct, tag))
+        for d, iv, c, t in cases:
+            out = torch.full_like(src, 0x5A)
+            st = torch.zeros(1, dtype=torch.int32, device="cuda")
+            ctx.open_device(d, iv, c, out, t, st)
+            torch.cuda.synchronize()
+            assert int(st.item()) == 1
+            assert int(out.abs().sum().item()) == 0
+
+
+def test_host_bytes_api(ctx_for, torch_cuda):
+    from paper_2411_03357_b200.gcm import GcmAuthError
+
+    key = bytes(range(7, 39))
+    ctx = ctx_for(key)
+    rng = random.Random(3)
+    for n in (1, 2048, 229376, 8 * MIB + 1, 32 * MIB):
+        p = rng.randbytes(n)
+        iv = rng.randrange(1 << 64)
+        c, t = ctx.seal_bytes(1, iv, p)
+        assert (c, t) == oracle_port.seal(key, 1, iv, p)
+        assert ctx.open_bytes(1, iv, c, t) == p
+        bad = bytearray(c); bad[-1] ^= 1
+        with pytest.raises(GcmAuthError):
+            ctx.open_bytes(1, iv, bytes(bad), t)
+
+
+def test_full_size_batch_round_trip(ctx_for, torch_cuda):
+    """BASELINE config sizes: an OPT-13B layer (18 x 32 MiB + 25,298,944 B) in one
+    launch; size-independent property = open(seal(P)) == P with all tags valid,
+    plus spot checks of first/last chunk against the reference arithmetic."""
+    torch = torch_cuda
+    key = bytes(range(200, 232))
+    ctx = ctx_for(key)
+    sizes = [32 * MIB] * 18 + [25_298_944]
+    total = sum(sizes)
+    buf = torch.randint(0, 256, (total,), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(buf)
+    back = torch.empty_like(buf)
+    tags = torch.empty((len(sizes), 16), dtype=torch.uint8, device="cuda")
+    items, off = [], 0
+    for i, n in enumerate(sizes):
+        items.append((0, 1000 + i, buf[off:off + n], out[off:off + n], tags[i]))
+        off += n
+    ctx.seal_batch(items)
+    st = torch.full((len(sizes),), 7, dtype=torch.int32, device="cuda")
+    ctx.open_batch([(0, 1000 + i, it[3], back[o:o + it[2].numel()], tags[i])
+                    for i, (it, o) in enumerate(zip(items, np.cumsum([0] + sizes[:-1])))], st)
+    torch.cuda.synchronize()
+    assert int(st.abs().sum().item()) == 0
+    assert torch.equal(back, buf)
+    for i in (0, len(sizes) - 1):
+        p = _host(items[i][2])
+        c, t = oracle_port.seal(key, 0, 1000 + i, p)
+        assert _host(items[i][3]) == c and _host(tags[i]) == t
