@@ -1,0 +1,310 @@
+"""B200 data plane of the speculative pipeline: where the engine's seals,
+opens and PCIe copies actually run.
+
+Mapping of the reference's in-process model onto one GPU:
+
+* host blocks (`memory.HostMemory`) are page-locked host arrays;
+  `engine.device_mem` holds real HBM buffers;
+* every seal/open of BOTH channel endpoints runs in the libspgcm kernels on
+  the compute stream, batched per engine step (chunk runs, NOP pads and
+  drains are one launch each);
+* swap-in data (spec encrypt-ahead and on-the-fly) crosses PCIe on the H2D
+  copy stream into an HBM staging slot and is sealed in place at its counter;
+  swap-out plaintext returns on the D2H copy stream once the host endpoint's
+  (deferred) open lands.  Cross-stream order uses CUDA events only: the host
+  thread never waits except where the reference's semantics expose bytes to
+  the host (digests, `app_read`, `finish`).
+
+`DryPlane` runs the same engine with no bytes at all (sizes and counters
+only) — the schedule the reference's simulator prices, usable without a GPU.
+"""
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass, field
+from typing import Any
+
+from . import gcm as _gcm
+from .channel import DeviceCiphertext
+
+TAG = 16
+
+
+def open_message_sync(key: bytes, direction: int, iv: int, msg: DeviceCiphertext):
+    """Blocking open of one device message (channel.decrypt_at on device data)."""
+    import torch
+
+    ctx = _gcm.context_for(key)
+    out = torch.empty(msg.declared_len, dtype=torch.uint8, device=msg.payload.device)
+    st = torch.zeros(1, dtype=torch.int32, device=msg.payload.device)
+    ctx.open_batch([(direction, iv, msg.payload, out, msg.auth_tag, msg.declared_len)], st)
+    if int(st.item()) != 0:
+        raise _gcm.GcmAuthError(f"tag mismatch at counter {iv}")
+    return out
+
+
+@dataclass
+class _Pending:
+    """A sealed chunk whose device payload is the wire message."""
+
+    msg: DeviceCiphertext
+    iv: int
+
+
+class GpuPlane:
+    """Streams, staging and batched launches for one engine on one GPU."""
+
+    kind = "gpu"
+
+    def __init__(self, key: bytes, device: int | None = None) -> None:
+        import torch
+
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        with torch.cuda.device(self.device):
+            self.ctx = _gcm.context_for(key)
+            self.s_comp = torch.cuda.Stream(self.device)
+            self.s_h2d = torch.cuda.Stream(self.device)
+            self.s_d2h = torch.cuda.Stream(self.device)
+        self._host_ready: dict[int, Any] = {}  # block id -> event after last D2H into it
+        self._h2d_done: dict[int, Any] = {}    # block id -> event after last H2D from it
+        self._status = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
+        self._status_used = 0
+        self.bytes_h2d = 0
+        self.bytes_d2h = 0
+        self.launches = 0
+
+    # -- helpers -------------------------------------------------------------------
+    def _empty(self, n: int):
+        with self.torch.cuda.stream(self.s_comp):
+            return self.torch.empty(n, dtype=self.torch.uint8, device=self.device)
+
+    def _status_slots(self, n: int):
+        if self._status_used + n > self._status.numel():
+            self.check_auth()
+        s = self._status[self._status_used:self._status_used + n]
+        self._status_used += n
+        return s
+
+    def check_auth(self) -> None:
+        """Raise GcmAuthError if any open since the last check failed."""
+        if self._status_used:
+            self.s_comp.synchronize()
+            bad = int(self._status[:self._status_used].abs().sum().item())
+            self._status[:self._status_used].zero_()
+            self._status_used = 0
+            if bad:
+                raise _gcm.GcmAuthError("authentication failed on the device")
+
+    # -- seals ---------------------------------------------------------------------
+    def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int) -> list:
+        """H2D the plaintext of `block` [inner + off, +n) for each span and
+        seal chunk i at iv0 + i in place (one copy + one launch)."""
+        torch = self.torch
+        total = sum(n for _, n in spans)
+        first = spans[0][0]
+        buf = self._empty(total + TAG * len(spans))
+        ev = self._host_ready.get(block.id)
+        if ev is not None:
+            self.s_h2d.wait_event(ev)
+        src = torch.from_numpy(block.data[inner + first: inner + first + total])
+        with torch.cuda.stream(self.s_h2d):
+            buf[:total].copy_(src if block.pinned is not None else src.pin_memory(), non_blocking=True)
+            buf.record_stream(self.s_h2d)
+            done = torch.cuda.Event()
+            done.record(self.s_h2d)
+        self._h2d_done[block.id] = done
+        self.bytes_h2d += total
+        self.s_comp.wait_stream(self.s_h2d)
+        items, msgs = [], []
+        for i, (off, n) in enumerate(spans):
+            view = buf[off - first: off - first + n]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            items.append((direction, iv0 + i, view, view, tag, n))
+            msgs.append(DeviceCiphertext(view, tag, n))
+        self.ctx.seal_batch(items, self.s_comp)
+        self.launches += 1
+        return msgs
+
+    def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
+        """Seal device plaintext `src` chunk-wise into a fresh staging buffer."""
+        total = sum(n for _, n in spans)
+        first = spans[0][0]
+        buf = self._empty(total + TAG * len(spans))
+        items, msgs = [], []
+        for i, (off, n) in enumerate(spans):
+            view = buf[off - first: off - first + n]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            items.append((direction, iv0 + i, src[off:off + n], view, tag, n))
+            msgs.append(DeviceCiphertext(view, tag, n))
+        self.ctx.seal_batch(items, self.s_comp)
+        self.launches += 1
+        return msgs
+
+    def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
+        """Seal small host payloads (NOP pads, token I/O) in one launch."""
+        torch = self.torch
+        total = sum(len(p) for p in payloads)
+        staged = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        staged.numpy()[:] = memoryview(b"".join(payloads)).cast("B")
+        buf = self._empty(total + TAG * len(payloads))
+        with torch.cuda.stream(self.s_comp):
+            buf[:total].copy_(staged, non_blocking=True)
+        items, msgs, off = [], [], 0
+        for i, p in enumerate(payloads):
+            view = buf[off:off + len(p)]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            items.append((direction, iv0 + i, view, view, tag, len(p)))
+            msgs.append(DeviceCiphertext(view, tag, len(p), nop=nop))
+            off += len(p)
+        self.ctx.seal_batch(items, self.s_comp)
+        self.launches += 1
+        return msgs
+
+    # -- opens ---------------------------------------------------------------------
+    def open_into(self, jobs: list, direction: int) -> None:
+        """jobs: (msg, iv, dst view or None).  One launch; NOPs open into
+        scratch so their tags are still verified."""
+        if not jobs:
+            return
+        items = []
+        for msg, iv, dst in jobs:
+            if dst is None:
+                dst = self._empty(msg.declared_len)
+            items.append((direction, iv, msg.payload, dst, msg.auth_tag, msg.declared_len))
+        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_comp)
+        self.launches += 1
+
+    def land_on_host(self, block, jobs: list, direction: int) -> None:
+        """Host endpoint open of D2H messages, then the plaintext lands in
+        `block` (jobs: (msg, iv, offset_in_block))."""
+        torch = self.torch
+        total = sum(m.declared_len for m, _, _ in jobs)
+        buf = self._empty(total)
+        items, off = [], 0
+        places = []
+        for msg, iv, boff in jobs:
+            view = buf[off:off + msg.declared_len]
+            items.append((direction, iv, msg.payload, view, msg.auth_tag, msg.declared_len))
+            places.append((view, boff, msg.declared_len))
+            off += msg.declared_len
+        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_comp)
+        self.launches += 1
+        self.s_d2h.wait_stream(self.s_comp)
+        pend = self._h2d_done.get(block.id)
+        if pend is not None:
+            self.s_d2h.wait_event(pend)
+        with torch.cuda.stream(self.s_d2h):
+            for view, boff, n in places:
+                dst = torch.from_numpy(block.data[boff:boff + n])
+                dst.copy_(view, non_blocking=True)
+            buf.record_stream(self.s_d2h)
+            ev = torch.cuda.Event()
+            ev.record(self.s_d2h)
+        self.bytes_d2h += total
+        self._host_ready[block.id] = ev
+
+    def host_sync(self, block_id: int | None = None) -> None:
+        """Wait until D2H landings are visible to the host."""
+        if block_id is None:
+            self.s_d2h.synchronize()
+            return
+        ev = self._host_ready.get(block_id)
+        if ev is not None:
+            ev.synchronize()
+
+    def before_host_write(self, block_id: int) -> None:
+        """The host is about to mutate `block_id`: in-flight copies that
+        read or write it must be finished first."""
+        for table in (self._h2d_done, self._host_ready):
+            ev = table.get(block_id)
+            if ev is not None:
+                ev.synchronize()
+
+    def new_device_buffer(self, n: int):
+        return self._empty(n)
+
+    def device_from_host(self, data: bytes):
+        t = self.torch.frombuffer(bytearray(data), dtype=self.torch.uint8)
+        with self.torch.cuda.stream(self.s_comp):
+            return t.to(self.device, non_blocking=False)
+
+    def to_host_bytes(self, view) -> bytes:
+        self.s_comp.synchronize()
+        return view.cpu().numpy().tobytes()
+
+    def digests(self, views: list) -> list:
+        self.s_comp.synchronize()
+        return [hashlib.sha256(v.cpu().numpy().tobytes()).hexdigest() for v in views]
+
+    def finish(self) -> None:
+        self.s_comp.synchronize()
+        self.s_h2d.synchronize()
+        self.s_d2h.synchronize()
+        self.check_auth()
+
+
+@dataclass(eq=False)
+class _DryPayload:
+    n: int
+
+    def numel(self) -> int:
+        return self.n
+
+    def __getitem__(self, sl: slice) -> "_DryPayload":
+        return _DryPayload(len(range(*sl.indices(self.n))))
+
+
+class DryPlane:
+    """No bytes, no GPU: messages carry only their sizes.  Used for schedule
+    planning and for control-plane tests in CPU-only environments."""
+
+    kind = "dry"
+
+    def __init__(self, key: bytes | None = None) -> None:
+        self.bytes_h2d = 0
+        self.bytes_d2h = 0
+        self.launches = 0
+
+    def _msgs(self, sizes, nop=False):
+        return [DeviceCiphertext(_DryPayload(n), None, n, nop=nop) for n in sizes]
+
+    def seal_host_chunks(self, block, inner, spans, direction, iv0):
+        self.bytes_h2d += sum(n for _, n in spans)
+        return self._msgs([n for _, n in spans])
+
+    def seal_device_chunks(self, src, spans, direction, iv0):
+        return self._msgs([n for _, n in spans])
+
+    def seal_bytes_device(self, payloads, direction, iv0, nop=False):
+        return self._msgs([len(p) for p in payloads], nop=nop)
+
+    def open_into(self, jobs, direction):
+        pass
+
+    def land_on_host(self, block, jobs, direction):
+        self.bytes_d2h += sum(m.declared_len for m, _, _ in jobs)
+
+    def host_sync(self, block_id=None):
+        pass
+
+    def before_host_write(self, block_id):
+        pass
+
+    def check_auth(self):
+        pass
+
+    def new_device_buffer(self, n):
+        return _DryPayload(n)
+
+    def device_from_host(self, data):
+        return _DryPayload(len(data))
+
+    def to_host_bytes(self, view):
+        raise RuntimeError("the dry plane holds no bytes")
+
+    def digests(self, views):
+        return [None] * len(views)
+
+    def finish(self):
+        pass

@@ -52,13 +52,25 @@ def random_bytes(seed, n: int, out: np.ndarray | None = None) -> np.ndarray:
     return res
 
 
+class PrngFill:
+    """Callable payload source `n -> bytes`; `fill_into` writes straight into
+    a (pinned) host array without the intermediate bytes object."""
+
+    __slots__ = ("seed",)
+
+    def __init__(self, seed) -> None:
+        self.seed = seed
+
+    def __call__(self, n: int) -> bytes:
+        return random_bytes(self.seed, n).tobytes()
+
+    def fill_into(self, out: np.ndarray) -> None:
+        random_bytes(self.seed, out.shape[0], out=out)
+
+
 def prng_fill(seed: int) -> Callable[[int], bytes]:
     """Drop-in for specpipe.memory.prng_fill (memory.py:106-110)."""
-
-    def fill(n: int) -> bytes:
-        return random_bytes(seed, n).tobytes()
-
-    return fill
+    return PrngFill(seed)
 
 
 def small_io_payload(seed: int, index: int, size: int) -> bytes:

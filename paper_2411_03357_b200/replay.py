@@ -1,0 +1,170 @@
+"""Trace replay through the B200 engine — the driver half of the reference's
+simulator (`_Replay._build_engine` simulator.py:253-284 and
+`_dispatch_engine` simulator.py:404-426) without its CPU cost model: here the
+time is real (CUDA events / wall clock on the GPU box).
+
+Systems (simulator.py SystemKind):
+  specpipe — speculation on, deferred swap decrypts (the product path);
+  synccc   — every transfer sealed/opened on the fly, synchronous decrypts;
+  nocc     — no crypto at all: plain pinned-memory cudaMemcpyAsync swaps on
+             the same streams (the "unencrypted swap" the north star compares
+             against).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+from .channel import new_channel
+from .engine import CopyRequest, Engine, EngineConfig
+from .memory import HostMemory, KvCache, ModelLayer
+from .predictor import Predictor, PredictorConfig, classify
+from .prng import app_write_payload, prng_fill, random_bytes, small_io_payload
+from .workload import AppWriteEvent, ComputeEvent, SmallIoEvent, SwapInRequest, SwapOut, SyncEvent, Trace
+
+
+@dataclass(frozen=True)
+class ReplayConfig:
+    system: str = "specpipe"
+    workers: int = 2
+    window: int = 64
+    leeway: int = 8
+    depth: int = 1
+    seed: int = 0
+    record_stream: bool = False
+    plane: str = "gpu"
+    chunk_bytes: int = 32 * 1024 * 1024
+    predictor_chunk_bytes: int | None = None  # default: PredictorConfig() as the reference driver
+
+
+@dataclass
+class ReplayResult:
+    engine: Engine | None
+    wall_s: float
+    swap_bytes: int
+    payload_bytes: int
+    error: str | None = None
+
+    @property
+    def swap_gbs(self) -> float:
+        return self.swap_bytes / self.wall_s / 1e9 if self.wall_s > 0 else 0.0
+
+
+def build_engine(trace: Trace, config: ReplayConfig):
+    """Engine + block table exactly as simulator.py:253-284 builds them."""
+    header = trace.header
+    memory = HostMemory()
+    cpu, gpu = new_channel(seed=config.seed)
+    pconf = PredictorConfig() if config.predictor_chunk_bytes is None else \
+        PredictorConfig(chunk_bytes=config.predictor_chunk_bytes)
+    predictor = Predictor(header.profile, pconf)
+    spec_on = config.system == "specpipe"
+    engine = Engine(memory, cpu, gpu, predictor, EngineConfig(
+        window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
+        chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
+        record_stream=config.record_stream, plane=config.plane))
+    blocks = {}
+    for spec in header.blocks:
+        if spec.resident == "cpu":
+            block = memory.alloc(spec.kind, spec.nbytes, prng_fill(spec.content_seed))
+            if isinstance(spec.kind, (ModelLayer, KvCache)):
+                predictor.observe_swap_out(block.id)
+        else:
+            block = memory.alloc(spec.kind, spec.nbytes)
+            if config.plane == "gpu":
+                import torch
+
+                host = torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes))
+                dev = engine.plane.new_device_buffer(spec.nbytes)
+                dev.copy_(host)
+                engine.seed_device(block.id, dev)
+            else:
+                engine.seed_device(block.id, engine.plane.new_device_buffer(spec.nbytes))
+        blocks[spec.id] = (block, classify(spec.nbytes, header.profile, pconf))
+    return engine, blocks
+
+
+def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool = False) -> ReplayResult:
+    """Replay `trace`; with `catch`, an engine exception (e.g. the reference's
+    defect C2 EngineError) is returned in `error` with the engine state at
+    the point of failure, as the parity harness needs."""
+    engine, blocks = build_engine(trace, config)
+    if config.plane == "gpu":
+        engine.plane.finish()
+    t0 = time.perf_counter()
+    try:
+        _dispatch_all(engine, blocks, trace, config)
+    except Exception as exc:
+        if not catch:
+            raise
+        return ReplayResult(engine, time.perf_counter() - t0, trace.swap_bytes(), trace.payload_bytes(),
+                            f"{type(exc).__name__}: {exc}")
+    wall = time.perf_counter() - t0
+    return ReplayResult(engine, wall, trace.swap_bytes(), trace.payload_bytes())
+
+
+def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig) -> None:
+    io_index = 0
+    for ev in trace.events:
+        if isinstance(ev, SwapInRequest):
+            block, cls = blocks[ev.block]
+            engine.copy_h2d(CopyRequest("h2d", block.base, block.len, cls, block_id=block.id, submit_time=ev.t))
+        elif isinstance(ev, SwapOut):
+            block, cls = blocks[ev.block]
+            engine.copy_d2h(CopyRequest("d2h", block.base, block.len, cls, block_id=block.id, submit_time=ev.t))
+        elif isinstance(ev, SmallIoEvent):
+            engine.small_io(ev.direction, ev.size, small_io_payload(config.seed, io_index, ev.size))
+            io_index += 1
+        elif isinstance(ev, SyncEvent):
+            engine.sync()
+        elif isinstance(ev, AppWriteEvent):
+            block, _ = blocks[ev.block]
+            engine.app_write(block.id, ev.offset, app_write_payload(ev.data_seed, ev.size))
+        elif isinstance(ev, ComputeEvent):
+            pass
+    engine.finish()
+
+
+def run_plain(trace: Trace, seed: int = 0) -> ReplayResult:
+    """NoCc on the GPU: the same swaps as plain pinned copies, no crypto."""
+    import torch
+
+    memory = HostMemory()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    blocks, device_mem = {}, {}
+    for spec in trace.header.blocks:
+        if spec.resident == "cpu":
+            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes, prng_fill(spec.content_seed))
+        else:
+            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes)
+            device_mem[spec.id] = torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)).to(dev)
+    torch.cuda.synchronize()
+    pending_in: list = []
+    t0 = time.perf_counter()
+    for ev in trace.events:
+        if isinstance(ev, SwapInRequest):
+            b = blocks[ev.block]
+            with torch.cuda.stream(s_h2d):
+                d = torch.empty(b.len, dtype=torch.uint8, device=dev)
+                d.copy_(b.pinned if b.pinned is not None else torch.from_numpy(b.data), non_blocking=True)
+            device_mem[ev.block] = d
+            pending_in.append(d)
+        elif isinstance(ev, SwapOut):
+            b = blocks[ev.block]
+            d = device_mem.pop(ev.block)
+            s_d2h.wait_stream(s_h2d)
+            with torch.cuda.stream(s_d2h):
+                (b.pinned if b.pinned is not None else torch.from_numpy(b.data)).copy_(d, non_blocking=True)
+                d.record_stream(s_d2h)
+        elif isinstance(ev, SyncEvent):
+            s_h2d.synchronize()
+            pending_in.clear()
+        elif isinstance(ev, SmallIoEvent):
+            payload = torch.frombuffer(bytearray(ev.size), dtype=torch.uint8)
+            with torch.cuda.stream(s_h2d if ev.direction == "h2d" else s_d2h):
+                if ev.direction == "h2d":
+                    payload.to(dev, non_blocking=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return ReplayResult(None, wall, trace.swap_bytes(), trace.payload_bytes())
