@@ -1,0 +1,453 @@
+#!/usr/bin/env python
+"""Benchmark of the encrypted-swap hot path (BASELINE.json metric:
+"AES-GCM GB/s per GPU (1/2/4/8 B200); OPT-66B offload tokens/s vs no-crypto").
+
+Workload (BASELINE.json configs[1]): one OPT-13B layer, 629,278,720 B =
+18 x 32 MiB + 25,298,944 B messages at consecutive H2D counters, synthetic
+bytes.  One step = seal the layer + open it again (every tag verified), in
+one batched launch each.  `value` counts payload bytes through AES-GCM (seal
+and open each count) per second, inputs resident in HBM; the layer is 5x the
+126 MB L2, so nothing is cached between steps.  `e2e` is the same metric
+through the C-ABI host-buffer entry points (sp_seal_host_batch /
+sp_open_host_batch: pinned host in -> pinned host out, PCIe copies inside).
+
+Multi-GPU (torchrun): each rank runs its own independent channel (key seed =
+rank) on its own layer — the path shards with no data-path collective, so
+scaling is weak; NCCL is used only for the barrier and the max-over-ranks
+timing reduction.
+
+`--impl reference` times the reference's own CPU arithmetic for the path
+(oracle/port.py: `cryptography` AESGCM as channel.py:96,111 call it,
+including the payload/tag split and concat of encrypt_at/decrypt_at) over the
+same layer, one process per host core; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+OPT13B_LAYER = 629_278_720
+CHUNK = 32 * MIB
+METRIC = "AES-GCM GB/s per GPU (1/2/4/8 B200); OPT-66B offload tokens/s vs no-crypto"
+
+
+def layer_sizes(layer: int = OPT13B_LAYER, chunk: int = CHUNK) -> list[int]:
+    return [chunk] * (layer // chunk) + ([layer % chunk] if layer % chunk else [])
+
+
+# -- distributed plumbing --------------------------------------------------------
+def dist_env() -> tuple[int, int, int]:
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def init_dist(world: int, backend: str):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend=backend)
+    return dist
+
+
+def reduce_max(dist, value: float, device=None) -> float:
+    """Max over ranks (the contract's multi-GPU timing rule)."""
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist, device=None) -> None:
+    if dist is not None:
+        if device is not None and device.type == "cuda":
+            dist.barrier(device_ids=[device.index])
+        else:
+            dist.barrier()
+
+
+# -- clocks -----------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int) -> None:
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(prefix="clk", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for ln in open(self.path):
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# -- peaks / profiles -----------------------------------------------------------------
+def measured_peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def ncu_traffic_per_launch() -> float | None:
+    """dram bytes read+write of one k_gcm launch over this workload, from the
+    committed `ncu --set full` capture summary (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "kgcm_ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        s = json.load(open(p))
+        return float(s["dram_bytes_read"] + s["dram_bytes_write"])
+    except (KeyError, ValueError, TypeError):
+        return None
+
+
+# -- CPU baseline (oracle port = the reference's cryptography arithmetic) ----------------
+_BARRIER = None
+
+
+def _cpu_init(barrier) -> None:
+    global _BARRIER
+    _BARRIER = barrier
+
+
+def _cpu_worker(args):
+    """Generate this worker's messages, line up with the others, then time
+    only the seal+open work (oracle.port = the reference's arithmetic)."""
+    seed, sizes, reps = args
+    import numpy as np
+
+    from oracle import port
+
+    key = bytes(range(32))
+    rng = np.random.default_rng(seed)
+    bufs = [rng.integers(0, 256, n, dtype=np.uint8).tobytes() for n in sizes]
+    if _BARRIER is not None:
+        _BARRIER.wait()
+    t0 = time.perf_counter()
+    total = 0
+    for _ in range(reps):
+        for i, p in enumerate(bufs):
+            c, t = port.seal(key, 0, i, p)            # encrypt_at: encrypt + payload/tag split
+            q = port.open_(key, 0, i, c, t)           # decrypt_at: payload+tag concat + decrypt
+            total += 2 * len(p)
+            assert len(q) == len(p)
+    return total, time.perf_counter() - t0
+
+
+def cpu_sample(cores: int, sizes: list[int], reps: int = 1) -> tuple[float, float]:
+    """Seal+open `sizes` spread over `cores` processes; returns (GB/s of
+    AES-GCM payload, seconds) where seconds = the slowest worker's crypto
+    time after a common start barrier (payload generation excluded)."""
+    if cores <= 1:
+        total, wall = _cpu_worker((0, sizes, reps))
+        return total / wall / 1e9, wall
+    import multiprocessing as mp
+
+    shards = [s for s in (sizes[i::cores] for i in range(cores)) if s]
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(len(shards))
+    with ctx.Pool(len(shards), initializer=_cpu_init, initargs=(barrier,)) as pool:
+        res = pool.map(_cpu_worker, [(i, s, reps) for i, s in enumerate(shards)], chunksize=1)
+    wall = max(r[1] for r in res)
+    return sum(r[0] for r in res) / wall / 1e9, wall
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# -- reference arm --------------------------------------------------------------------------
+def run_reference(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = host_cores()
+    sizes = layer_sizes()
+    # one step = the whole layer sealed + opened, messages spread over processes
+    # (the reference itself is single-threaded; this is its arithmetic on every core)
+    procs = min(cores, len(sizes))
+    for _ in range(args.warmup):
+        cpu_sample(procs, sizes)
+    gbs_steps, walls = [], []
+    for _ in range(args.steps):
+        g, w = cpu_sample(procs, sizes)
+        gbs_steps.append(g)
+        walls.append(w)
+    ms = 1000.0 * sum(walls) / len(walls)
+    value = 2 * sum(sizes) / (ms / 1000.0) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "opt-13b layer seal+open (18 x 32 MiB + 25,298,944 B), AES-256-GCM",
+                   "layer_bytes": sum(sizes), "messages": len(sizes), "parallelism": "independent channels"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": f"full layer per step, {procs} processes (of {cores} host cores), "
+                                   "oracle/port.py = cryptography AESGCM with encrypt_at/decrypt_at framing"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -- our arm ------------------------------------------------------------------------------------
+def run_gpu(args) -> None:
+    import torch
+
+    from paper_2411_03357_b200 import _native
+    from paper_2411_03357_b200.gcm import GcmContext
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(world, "nccl")
+    sizes = layer_sizes()
+    total = sum(sizes)
+    n = len(sizes)
+    ctx = GcmContext(bytes((rank * 37 + i) & 0xFF for i in range(32)))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    plain = torch.randint(0, 256, (total,), dtype=torch.uint8, device=dev, generator=gen)
+    ct = torch.empty_like(plain)
+    back = torch.empty_like(plain)
+    tags = torch.empty((n, 16), dtype=torch.uint8, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    offs = [sum(sizes[:i]) for i in range(n)]
+    seal_items = [(0, 1000 + i, plain[o:o + s], ct[o:o + s], tags[i]) for i, (o, s) in enumerate(zip(offs, sizes))]
+    open_items = [(0, 1000 + i, ct[o:o + s], back[o:o + s], tags[i]) for i, (o, s) in enumerate(zip(offs, sizes))]
+    stream = torch.cuda.Stream(dev)
+
+    def step():
+        ctx.seal_batch(seal_items, stream)
+        ctx.open_batch(open_items, status, stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    stream.synchronize()
+    assert torch.equal(back, plain) and int(status.abs().sum()) == 0, "round trip failed"
+
+    # ---- device-resident timed region (per-launch events on the launching stream)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    barrier(dist, dev)
+    torch.cuda.synchronize()
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(K):
+            ev[k][0].record(stream)
+            ctx.seal_batch(seal_items, stream)
+            ev[k][1].record(stream)
+            ctx.open_batch(open_items, status, stream)
+            ev[k][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    gpu_launches = _native.launch_count() - launches0
+    barrier(dist, dev)
+    ms_local = t_start.elapsed_time(t_end) / K
+    ms = reduce_max(dist, ms_local, dev)
+    seal_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    open_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    value = 2 * total / (ms / 1000.0) / 1e9 * world  # whole job
+    assert int(status.abs().sum()) == 0
+
+    # ---- e2e through the C-ABI host-buffer entry points (pinned host buffers)
+    h_plain = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    h_plain.copy_(plain)
+    h_ct = torch.empty_like(h_plain, pin_memory=True)
+    h_back = torch.empty_like(h_plain, pin_memory=True)
+    h_tags = torch.empty((n, 16), dtype=torch.uint8, pin_memory=True)
+    hs_items = [(0, 5000 + i, h_plain[o:o + s], h_ct[o:o + s], h_tags[i]) for i, (o, s) in enumerate(zip(offs, sizes))]
+    ho_items = [(0, 5000 + i, h_ct[o:o + s], h_back[o:o + s], h_tags[i]) for i, (o, s) in enumerate(zip(offs, sizes))]
+
+    def e2e_step():
+        ctx.seal_host_batch(hs_items)
+        ctx.open_host_batch(ho_items)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        e2e_step()
+    assert torch.equal(h_back, h_plain)
+    KE = max(1, min(K, 5))
+    barrier(dist, dev)
+    t0 = time.perf_counter()
+    for _ in range(KE):
+        e2e_step()
+    e2e_ms_local = (time.perf_counter() - t0) * 1000.0 / KE
+    barrier(dist, dev)
+    e2e_ms = reduce_max(dist, e2e_ms_local, dev)
+    e2e_value = 2 * total / (e2e_ms / 1000.0) / 1e9 * world
+    h2d_bytes = 2 * total + 16 * n
+    d2h_bytes = 2 * total + 16 * n + 4 * n
+
+    # ---- plain PCIe copies of the same bytes, H2D and D2H overlapped on two
+    # streams (the ceiling the e2e pipeline is compared against)
+    dcopy = torch.empty_like(plain)
+    s_a, s_b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(KE):
+        for _r in range(2):
+            with torch.cuda.stream(s_a):
+                dcopy.copy_(h_plain, non_blocking=True)
+            with torch.cuda.stream(s_b):
+                h_back.copy_(ct, non_blocking=True)
+        torch.cuda.synchronize()
+    pcie_ms = (time.perf_counter() - t0) * 1000.0 / KE
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peaks, peaks_kind = measured_peaks()
+    clocks = clk.summary()
+    bytes_per_launch = 2 * total + 16 * n  # algorithmic: read + write every payload byte, tags
+    achieved = bytes_per_launch / ((seal_ms + open_ms) / 2 / 1000.0) / 1e9
+    f_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    # integer-pipe bounds with SURVEY §8d's canonical counts per payload byte:
+    # 16 LSU lookups/B on 32 lanes/SM/clk; 36 ALU ops/B on 64 lanes/SM/clk
+    lsu_bound = 32 * sms * f_mhz * 1e6 / 16 / 1e9
+    alu_bound = 64 * sms * f_mhz * 1e6 / 36 / 1e9
+    per_gpu_payload = 2 * total / (ms / 1000.0) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "opt-13b layer seal+open per GPU (18 x 32 MiB + 25,298,944 B messages, "
+                               "consecutive H2D counters), AES-256-GCM, one batched launch each",
+                   "layer_bytes": total, "messages": n, "parallelism": f"independent channels x{world}",
+                   "l2": "inputs (629 MB) > 126 MB L2; no flush needed"},
+        "seal_gbs": round(total / seal_ms / 1e6, 2), "open_gbs": round(total / open_ms / 1e6, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks.get("hbm_gbs"),
+                     "unit": "GB/s", "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 4),
+                     "traffic": ncu_traffic_per_launch(), "peak_kind": peaks_kind,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "note": "k_gcm is bound by the shared-memory LSU pipe, not HBM: see int_roofline"},
+        "int_roofline": {"bound": "lsu (T-table + GHASH lookups)", "payload_gbs": round(per_gpu_payload, 2),
+                         "lsu_bound_gbs": round(lsu_bound, 1), "alu_bound_gbs": round(alu_bound, 1),
+                         "frac_of_lsu_bound": round(per_gpu_payload / lsu_bound, 4),
+                         "sm_mhz": f_mhz, "sms": sms,
+                         "counts": "SURVEY 8d: 16 lookups/B (32 lanes/SM/clk), 36 ALU ops/B (64 lanes/SM/clk)"},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": d2h_bytes, "ms_per_step": round(e2e_ms, 3), "steps": KE,
+                "path": "sp_seal_host_batch + sp_open_host_batch, pinned host buffers",
+                "plain_duplex_copy_ms_same_bytes": round(pcie_ms, 3),
+                "ratio_vs_plain_copies": round(pcie_ms / e2e_ms, 4)},
+        "gpu_launches": int(gpu_launches),
+        "clocks": clocks,
+    }
+
+    if not args.no_cpu_baseline:
+        sample_sizes = layer_sizes()[:8]
+        g1, w1 = cpu_sample(1, sample_sizes)
+        line["cpu_baseline"] = {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "port",
+                                "sample": f"8 x 32 MiB seal+open on 1 core via oracle/port.py "
+                                          f"(cryptography AESGCM, encrypt_at/decrypt_at framing), {w1:.1f} s"}
+    if args.offload:
+        line["offload"] = offload_bench(args)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def offload_bench(args) -> dict:
+    """OPT-66B-shaped FlexGen weight offload through the B200 engine vs the
+    same swaps as plain copies (the north star's 'within 10% of unencrypted
+    swap throughput')."""
+    import torch
+
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import ReplayConfig, run_engine, run_plain
+
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=args.offload_iters)
+    res_plain = run_plain(tr)
+    res_enc = run_engine(tr, ReplayConfig(system="specpipe", plane="gpu", record_stream=False))
+    rep = res_enc.engine.report()
+    torch.cuda.synchronize()
+    return {"model": "opt-66b", "layers_offloaded": 2, "iterations": args.offload_iters,
+            "layer_bytes": workload.opt_layer_bytes("opt-66b"), "swap_bytes": tr.swap_bytes(),
+            "encrypted_gbs": round(res_enc.swap_gbs, 2), "plain_gbs": round(res_plain.swap_gbs, 2),
+            "throughput_ratio": round(res_enc.swap_gbs / res_plain.swap_gbs, 4),
+            "note": "tokens/s ratio == swap throughput ratio (same trace, same batch)",
+            "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "nops": rep["nops"],
+            "sequence_hit_rate": rep["sequence_hit_rate"]}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--offload", action="store_true", help="also run the OPT-66B engine offload comparison")
+    ap.add_argument("--offload-iters", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

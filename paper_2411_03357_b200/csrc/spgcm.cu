@@ -82,6 +82,7 @@ __device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams 
 
 __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParams p) {
     extern __shared__ __align__(16) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
     fill_tables(sm, p);
     __syncthreads();
 
@@ -127,13 +128,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             return load_bytes(ptr, nb);
         };
 
+        const CtrConst cc = ctr_const(p.rk, lct, x0, x1, x2);
+        CtrCache ck;
+        ck.gid = 0xffffffffu;
+        ck.d0 = ck.d1 = ck.d2 = ck.d3 = 0;
         uint4 y = make_uint4(0, 0, 0, 0);
         uint4 cur = load_row(t_a);
         for (uint64_t t = t_a; t < t_b; ++t) {
             const uint4 nxt = (t + 1 < t_b) ? load_row(t + 1) : make_uint4(0, 0, 0, 0);
             const int64_t i = base_i + 32 * (int64_t)t;
             const uint32_t ctr = (uint32_t)(i + 2);
-            const uint4 ks = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(ctr) ^ p.rk[3]);
+            const uint4 ks = aes256_ctr(p.rk, lct, cc, ck, ctr);
             uint4 out = xor4(cur, ks);
             uint4 gin = cur;
             if (i >= 0) {
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             } else {
                 gin = make_uint4(0, 0, 0, 0);
             }
-            y = (t == t_a) ? gin : xor4(gmul_g(sm, y, lcm, lcr), gin);
+            y = (t == t_a) ? gin : xor4(gmul_g(y, lcm, lcr), gin);
             cur = nxt;
         }
 

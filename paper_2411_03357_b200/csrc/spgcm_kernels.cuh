@@ -86,38 +86,61 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 // b2 = b3 = lc.b1 (= 0).
 #define SP_SEL(k) (0x5504u | ((uint32_t)(k) << 4))
 
-__device__ __forceinline__ uint32_t tl(const uint8_t *sm, uint32_t off, uint32_t w, uint32_t sel,
-                                       uint32_t lc) {
-    return *reinterpret_cast<const uint32_t *>(sm + off + __byte_perm(w, lc, sel));
+// The dynamic shared window of a non-cluster launch starts at shared address
+// kSmBase (checked at kernel entry).  Lookups use absolute addresses so one
+// PRMT + one LDS [reg+imm] is the whole lookup (no base add per access).
+constexpr uint32_t kSmBase = 0x400;
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr, uint32_t off_unused = 0) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 
-// s0..s3: counter block words already XORed with round key 0.
-__device__ __forceinline__ uint4 aes256_rounds(const uint8_t *sm, const uint32_t *rk, uint32_t lc,
-                                               uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+template <uint32_t OFF>
+__device__ __forceinline__ uint32_t lds32_at(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF + kSmBase));
+    return v;
+}
+
+template <uint32_t OFF>
+__device__ __forceinline__ uint4 lds128_at(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+%5];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr), "n"(OFF + kSmBase));
+    return v;
+}
+
+template <uint32_t OFF>
+__device__ __forceinline__ uint32_t tl(uint32_t w, uint32_t sel, uint32_t lc) {
+    return lds32_at<OFF>(__byte_perm(w, lc, sel));
+}
+
+#define T0L(w, b) tl<kSmAes0>(w, SP_SEL(b), lc)
+#define T1L(w, b) tl<kSmAes0 + 128>(w, SP_SEL(b), lc)
+#define T2L(w, b) tl<kSmAes1>(w, SP_SEL(b), lc)
+#define T3L(w, b) tl<kSmAes1 + 128>(w, SP_SEL(b), lc)
+
+// Rounds r0..13 (full T-table rounds) on state s0..s3, then the final round.
+__device__ __forceinline__ uint4 aes256_from_round(int r0, const uint32_t *rk, uint32_t lc, uint32_t s0,
+                                                   uint32_t s1, uint32_t s2, uint32_t s3) {
 #pragma unroll
     for (int r = 1; r < 14; ++r) {
-        const uint32_t t0 = tl(sm, kSmAes0, s0, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s1, SP_SEL(1), lc) ^
-                            tl(sm, kSmAes1, s2, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s3, SP_SEL(3), lc) ^
-                            rk[4 * r + 0];
-        const uint32_t t1 = tl(sm, kSmAes0, s1, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s2, SP_SEL(1), lc) ^
-                            tl(sm, kSmAes1, s3, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s0, SP_SEL(3), lc) ^
-                            rk[4 * r + 1];
-        const uint32_t t2 = tl(sm, kSmAes0, s2, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s3, SP_SEL(1), lc) ^
-                            tl(sm, kSmAes1, s0, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s1, SP_SEL(3), lc) ^
-                            rk[4 * r + 2];
-        const uint32_t t3 = tl(sm, kSmAes0, s3, SP_SEL(0), lc) ^ tl(sm, kSmAes0 + 128, s0, SP_SEL(1), lc) ^
-                            tl(sm, kSmAes1, s1, SP_SEL(2), lc) ^ tl(sm, kSmAes1 + 128, s2, SP_SEL(3), lc) ^
-                            rk[4 * r + 3];
+        if (r < r0) continue;
+        const uint32_t t0 = T0L(s0, 0) ^ T1L(s1, 1) ^ T2L(s2, 2) ^ T3L(s3, 3) ^ rk[4 * r + 0];
+        const uint32_t t1 = T0L(s1, 0) ^ T1L(s2, 1) ^ T2L(s3, 2) ^ T3L(s0, 3) ^ rk[4 * r + 1];
+        const uint32_t t2 = T0L(s2, 0) ^ T1L(s3, 1) ^ T2L(s0, 2) ^ T3L(s1, 3) ^ rk[4 * r + 2];
+        const uint32_t t3 = T0L(s3, 0) ^ T1L(s0, 1) ^ T2L(s1, 2) ^ T3L(s2, 3) ^ rk[4 * r + 3];
         s0 = t0; s1 = t1; s2 = t2; s3 = t3;
     }
     // Final round: S-box bytes come out of the T-tables: T2 has S at byte 0,
     // T3 at byte 1, T0 at byte 2, T1 at byte 3.
     uint4 o;
-#define SP_LAST(ca, cb, cc, cd, k)                                                        \
-    ((tl(sm, kSmAes1, ca, SP_SEL(0), lc) & 0x000000ffu) |                                 \
-     (tl(sm, kSmAes1 + 128, cb, SP_SEL(1), lc) & 0x0000ff00u) |                           \
-     (tl(sm, kSmAes0, cc, SP_SEL(2), lc) & 0x00ff0000u) |                                 \
-     (tl(sm, kSmAes0 + 128, cd, SP_SEL(3), lc) & 0xff000000u)) ^ rk[56 + k]
+#define SP_LAST(ca, cb, cc, cd, k)                                                       \
+    ((T2L(ca, 0) & 0x000000ffu) | (T3L(cb, 1) & 0x0000ff00u) | (T0L(cc, 2) & 0x00ff0000u) | \
+     (T1L(cd, 3) & 0xff000000u)) ^ rk[56 + k]
     o.x = SP_LAST(s0, s1, s2, s3, 0);
     o.y = SP_LAST(s1, s2, s3, s0, 1);
     o.z = SP_LAST(s2, s3, s0, s1, 2);
@@ -126,13 +149,68 @@ __device__ __forceinline__ uint4 aes256_rounds(const uint8_t *sm, const uint32_t
     return o;
 }
 
+// s0..s3: counter block words already XORed with round key 0.
+__device__ __forceinline__ uint4 aes256_rounds(const uint8_t *, const uint32_t *rk, uint32_t lc, uint32_t s0,
+                                               uint32_t s1, uint32_t s2, uint32_t s3) {
+    return aes256_from_round(1, rk, lc, s0, s1, s2, s3);
+}
+
+// ---- counter-mode caching ----------------------------------------------------
+// After round 0 only column 3 (the 32-bit counter) varies.  With counters
+// < 2^24 (messages <= 32 MiB), round-1 column 3 is message-constant, columns
+// 1-2 change only when ctr >> 8 changes, and round 2 has one varying input
+// column.  Per block that is 5 lookups for rounds 1-2 instead of 32.
+struct CtrConst {
+    uint32_t c0, c1, c2, t3;  // round-1 partial columns (message constants)
+};
+
+struct CtrCache {
+    uint32_t gid;             // ctr >> 8 the d-values belong to
+    uint32_t d0, d1, d2, d3;  // round-2 partial columns (group constants)
+};
+
+__device__ __forceinline__ CtrConst ctr_const(const uint32_t *rk, uint32_t lc, uint32_t x0, uint32_t x1,
+                                              uint32_t x2) {
+    CtrConst c;
+    const uint32_t s3hi = rk[3];  // byte 0 of (bswap(ctr) ^ rk3) for ctr < 2^24
+    c.c0 = T0L(x0, 0) ^ T1L(x1, 1) ^ T2L(x2, 2) ^ rk[4];
+    c.c1 = T0L(x1, 0) ^ T1L(x2, 1) ^ T3L(x0, 3) ^ rk[5];
+    c.c2 = T0L(x2, 0) ^ T2L(x0, 2) ^ T3L(x1, 3) ^ rk[6];
+    c.t3 = T0L(s3hi, 0) ^ T1L(x0, 1) ^ T2L(x1, 2) ^ T3L(x2, 3) ^ rk[7];
+    return c;
+}
+
+__device__ __forceinline__ void ctr_refresh(CtrCache &k, const CtrConst &c, const uint32_t *rk, uint32_t lc,
+                                            uint32_t s3, uint32_t gid) {
+    const uint32_t t1 = c.c1 ^ T2L(s3, 2);
+    const uint32_t t2 = c.c2 ^ T1L(s3, 1);
+    const uint32_t t3 = c.t3;
+    k.d0 = T1L(t1, 1) ^ T2L(t2, 2) ^ T3L(t3, 3) ^ rk[8];
+    k.d1 = T0L(t1, 0) ^ T1L(t2, 1) ^ T2L(t3, 2) ^ rk[9];
+    k.d2 = T0L(t2, 0) ^ T1L(t3, 1) ^ T3L(t1, 3) ^ rk[10];
+    k.d3 = T0L(t3, 0) ^ T2L(t1, 2) ^ T3L(t2, 3) ^ rk[11];
+    k.gid = gid;
+}
+
+__device__ __forceinline__ uint4 aes256_ctr(const uint32_t *rk, uint32_t lc, const CtrConst &c, CtrCache &k,
+                                            uint32_t ctr) {
+    const uint32_t s3 = bswap32(ctr) ^ rk[3];
+    const uint32_t gid = ctr >> 8;
+    if (gid != k.gid) ctr_refresh(k, c, rk, lc, s3, gid);
+    const uint32_t t0 = c.c0 ^ T3L(s3, 3);
+    const uint32_t u0 = T0L(t0, 0) ^ k.d0;
+    const uint32_t u1 = T3L(t0, 3) ^ k.d1;
+    const uint32_t u2 = T2L(t0, 2) ^ k.d2;
+    const uint32_t u3 = T1L(t0, 1) ^ k.d3;
+    return aes256_from_round(3, rk, lc, u0, u1, u2, u3);
+}
+
 // ---- GHASH: Y * G with an 8-bit Shoup table in shared memory ----------------
 // Element layout: little-endian 32-bit words of the 16-byte GCM string
 // (byte 0 holds coefficients x^0..x^7, MSB first).  Multiplying by x^8 moves
 // every byte one position up; byte 15 falls off and is folded back with R8.
-__device__ __forceinline__ uint4 gmul_g(const uint8_t *sm, uint4 y, uint32_t lcm, uint32_t lcr) {
-    const uint8_t *gh = sm + kSmGh;
-    uint4 z = *reinterpret_cast<const uint4 *>(gh + __byte_perm(y.w, lcm, SP_SEL(3)));
+__device__ __forceinline__ uint4 gmul_g(uint4 y, uint32_t lcm, uint32_t lcr) {
+    uint4 z = lds128_at<kSmGh>(__byte_perm(y.w, lcm, SP_SEL(3)));
 #pragma unroll
     for (int b = 14; b >= 0; --b) {
         const uint32_t raddr = __byte_perm(z.w, lcr, SP_SEL(3));
@@ -140,8 +218,8 @@ __device__ __forceinline__ uint4 gmul_g(const uint8_t *sm, uint4 y, uint32_t lcm
         z.z = __funnelshift_l(z.y, z.z, 8);
         z.y = __funnelshift_l(z.x, z.y, 8);
         z.x = z.x << 8;
-        const uint32_t r = *reinterpret_cast<const uint32_t *>(gh + raddr);
-        const uint4 m = *reinterpret_cast<const uint4 *>(gh + __byte_perm(word_of(y, b >> 2), lcm, SP_SEL(b & 3)));
+        const uint32_t r = lds32_at<kSmGh>(raddr);
+        const uint4 m = lds128_at<kSmGh>(__byte_perm(word_of(y, b >> 2), lcm, SP_SEL(b & 3)));
         z.x ^= r ^ m.x;
         z.y ^= m.y;
         z.z ^= m.z;

@@ -64,6 +64,7 @@ class GpuPlane:
         with torch.cuda.device(self.device):
             self.ctx = _gcm.context_for(key)
             self.s_comp = torch.cuda.Stream(self.device)
+            self.s_spec = torch.cuda.Stream(self.device)
             self.s_h2d = torch.cuda.Stream(self.device)
             self.s_d2h = torch.cuda.Stream(self.device)
         self._host_ready: dict[int, Any] = {}  # block id -> event after last D2H into it
@@ -97,34 +98,49 @@ class GpuPlane:
                 raise _gcm.GcmAuthError("authentication failed on the device")
 
     # -- seals ---------------------------------------------------------------------
-    def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int) -> list:
+    def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int,
+                         speculative: bool = False) -> list:
         """H2D the plaintext of `block` [inner + off, +n) for each span and
-        seal chunk i at iv0 + i in place (one copy + one launch)."""
+        seal chunk i at iv0 + i in place (one copy + one launch).
+
+        Speculative (encrypt-ahead) seals run on their own stream and carry a
+        `ready` event that the committing open waits on; on-the-fly seals run
+        on the compute stream in issue order."""
         torch = self.torch
         total = sum(n for _, n in spans)
         first = spans[0][0]
-        buf = self._empty(total + TAG * len(spans))
         ev = self._host_ready.get(block.id)
         if ev is not None:
             self.s_h2d.wait_event(ev)
         src = torch.from_numpy(block.data[inner + first: inner + first + total])
+        s_seal = self.s_spec if speculative else self.s_comp
         with torch.cuda.stream(self.s_h2d):
+            # staging is allocated on the stream that first writes it (the
+            # copy engine) and marked as used by every stream that reads it,
+            # so the caching allocator never hands it out early
+            buf = torch.empty(total + TAG * len(spans), dtype=torch.uint8, device=self.device)
             buf[:total].copy_(src if block.pinned is not None else src.pin_memory(), non_blocking=True)
-            buf.record_stream(self.s_h2d)
+            buf.record_stream(self.s_comp)
+            if speculative:
+                buf.record_stream(self.s_spec)
             done = torch.cuda.Event()
             done.record(self.s_h2d)
         self._h2d_done[block.id] = done
         self.bytes_h2d += total
-        self.s_comp.wait_stream(self.s_h2d)
-        items, msgs = [], []
+        s_seal.wait_event(done)
+        items, views = [], []
         for i, (off, n) in enumerate(spans):
             view = buf[off - first: off - first + n]
             tag = buf[total + TAG * i: total + TAG * (i + 1)]
             items.append((direction, iv0 + i, view, view, tag, n))
-            msgs.append(DeviceCiphertext(view, tag, n))
-        self.ctx.seal_batch(items, self.s_comp)
+            views.append((view, tag, n))
+        self.ctx.seal_batch(items, s_seal)
         self.launches += 1
-        return msgs
+        ready = None
+        if speculative:
+            ready = torch.cuda.Event()
+            ready.record(self.s_spec)
+        return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
 
     def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
         """Seal device plaintext `src` chunk-wise into a fresh staging buffer."""
@@ -168,7 +184,11 @@ class GpuPlane:
         if not jobs:
             return
         items = []
+        waited = set()
         for msg, iv, dst in jobs:
+            if msg.ready is not None and id(msg.ready) not in waited:
+                self.s_comp.wait_event(msg.ready)
+                waited.add(id(msg.ready))
             if dst is None:
                 dst = self._empty(msg.declared_len)
             items.append((direction, iv, msg.payload, dst, msg.auth_tag, msg.declared_len))
@@ -239,6 +259,7 @@ class GpuPlane:
 
     def finish(self) -> None:
         self.s_comp.synchronize()
+        self.s_spec.synchronize()
         self.s_h2d.synchronize()
         self.s_d2h.synchronize()
         self.check_auth()
@@ -269,7 +290,7 @@ class DryPlane:
     def _msgs(self, sizes, nop=False):
         return [DeviceCiphertext(_DryPayload(n), None, n, nop=nop) for n in sizes]
 
-    def seal_host_chunks(self, block, inner, spans, direction, iv0):
+    def seal_host_chunks(self, block, inner, spans, direction, iv0, speculative=False):
         self.bytes_h2d += sum(n for _, n in spans)
         return self._msgs([n for _, n in spans])
 
