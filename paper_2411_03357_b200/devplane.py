@@ -91,6 +91,7 @@ class GpuPlane:
         """Raise GcmAuthError if any open since the last check failed."""
         if self._status_used:
             self.s_comp.synchronize()
+            self.s_d2h.synchronize()
             bad = int(self._status[:self._status_used].abs().sum().item())
             self._status[:self._status_used].zero_()
             self._status_used = 0
@@ -143,19 +144,24 @@ class GpuPlane:
         return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
 
     def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
-        """Seal device plaintext `src` chunk-wise into a fresh staging buffer."""
+        """Seal device plaintext `src` chunk-wise into a fresh staging buffer
+        (compute stream); messages carry a `ready` event for other streams."""
+        torch = self.torch
         total = sum(n for _, n in spans)
         first = spans[0][0]
         buf = self._empty(total + TAG * len(spans))
-        items, msgs = [], []
+        items, views = [], []
         for i, (off, n) in enumerate(spans):
             view = buf[off - first: off - first + n]
             tag = buf[total + TAG * i: total + TAG * (i + 1)]
             items.append((direction, iv0 + i, src[off:off + n], view, tag, n))
-            msgs.append(DeviceCiphertext(view, tag, n))
+            views.append((view, tag, n))
         self.ctx.seal_batch(items, self.s_comp)
         self.launches += 1
-        return msgs
+        ready = torch.cuda.Event()
+        ready.record(self.s_comp)
+        buf.record_stream(self.s_d2h)
+        return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
 
     def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
         """Seal small host payloads (NOP pads, token I/O) in one launch."""
@@ -197,28 +203,32 @@ class GpuPlane:
 
     def land_on_host(self, block, jobs: list, direction: int) -> None:
         """Host endpoint open of D2H messages, then the plaintext lands in
-        `block` (jobs: (msg, iv, offset_in_block))."""
+        `block` (jobs: (msg, iv, offset_in_block)).  Both the open and the
+        copy run on the D2H stream, so landings overlap H2D traffic and the
+        compute stream's commits."""
         torch = self.torch
         total = sum(m.declared_len for m, _, _ in jobs)
-        buf = self._empty(total)
-        items, off = [], 0
-        places = []
+        waited = set()
+        for m, _, _ in jobs:
+            if m.ready is not None and id(m.ready) not in waited:
+                self.s_d2h.wait_event(m.ready)
+                waited.add(id(m.ready))
+        pend = self._h2d_done.get(block.id)
+        if pend is not None:
+            self.s_d2h.wait_event(pend)
+        with torch.cuda.stream(self.s_d2h):
+            buf = torch.empty(total, dtype=torch.uint8, device=self.device)
+        items, places, off = [], [], 0
         for msg, iv, boff in jobs:
             view = buf[off:off + msg.declared_len]
             items.append((direction, iv, msg.payload, view, msg.auth_tag, msg.declared_len))
             places.append((view, boff, msg.declared_len))
             off += msg.declared_len
-        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_comp)
+        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_d2h)
         self.launches += 1
-        self.s_d2h.wait_stream(self.s_comp)
-        pend = self._h2d_done.get(block.id)
-        if pend is not None:
-            self.s_d2h.wait_event(pend)
         with torch.cuda.stream(self.s_d2h):
             for view, boff, n in places:
-                dst = torch.from_numpy(block.data[boff:boff + n])
-                dst.copy_(view, non_blocking=True)
-            buf.record_stream(self.s_d2h)
+                torch.from_numpy(block.data[boff:boff + n]).copy_(view, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self.s_d2h)
         self.bytes_d2h += total
