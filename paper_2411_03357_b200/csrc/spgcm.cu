@@ -99,16 +99,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
     const uint64_t g_end = p.row_begin + (total * (gw + 1)) / nw;
     if (g >= g_end) return;
 
+    const MsgDev *msgs = p.nmsgs <= kInline ? p.inl : p.msgs;
     // first message containing row g (binary search on row_begin)
     uint32_t lo = 0, hi = p.nmsgs - 1;
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (p.msgs[mid].row_begin <= g) lo = mid; else hi = mid - 1;
+        if (msgs[mid].row_begin <= g) lo = mid; else hi = mid - 1;
     }
     uint32_t m = lo;
 
     while (g < g_end) {
-        const MsgDev md = p.msgs[m];
+        const MsgDev md = msgs[m];
         const uint64_t t_a = g - md.row_begin;
         const uint64_t t_b = min((uint64_t)md.rows, g_end - md.row_begin);
         const int64_t nblk = (int64_t)((md.len + 15u) >> 4);
@@ -408,12 +409,20 @@ void key_expand(const uint8_t key[32], uint32_t rk[60]) {
     memcpy(rk, w, 240);  // little-endian words == AES state column words
 }
 
+constexpr int kPinSlots = 4;
+
 struct Workspace {
     MsgDev *d_msgs = nullptr;
     size_t cap_msgs = 0;
     uint32_t *d_acc = nullptr;
     size_t cap_acc = 0;
     std::vector<MsgDev> h_msgs;
+    // pinned staging ring for descriptor arrays larger than kInline
+    MsgDev *h_pin[kPinSlots] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_pin[kPinSlots] = {nullptr, nullptr, nullptr, nullptr};
+    bool ev_live[kPinSlots] = {false, false, false, false};
+    size_t cap_pin = 0;
+    int slot = 0;
 };
 
 std::mutex g_ws_mu;
@@ -518,9 +527,36 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
     }
     int rc = ensure_ws(ws, (size_t)n, s);
     if (rc) return rc;
-    SP_CUDA(cudaMemcpyAsync(ws->d_msgs, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev), cudaMemcpyHostToDevice, s),
-            "cudaMemcpyAsync(msgs)");
     p = base_params(ctx);
+    if ((uint32_t)n <= kInline) {
+        memcpy(p.inl, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev));
+    } else {
+        // pinned ring slot: wait only for the copy that last used this slot
+        const int k = ws->slot;
+        ws->slot = (k + 1) % kPinSlots;
+        if (ws->cap_pin < (size_t)n) {
+            for (int j = 0; j < kPinSlots; ++j) {
+                if (ws->ev_live[j]) SP_CUDA(cudaEventSynchronize(ws->ev_pin[j]), "cudaEventSynchronize");
+                if (ws->h_pin[j]) cudaFreeHost(ws->h_pin[j]);
+                ws->h_pin[j] = nullptr;
+                ws->ev_live[j] = false;
+            }
+            const size_t cap = std::max<size_t>((size_t)n, 1024);
+            for (int j = 0; j < kPinSlots; ++j) {
+                SP_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&ws->h_pin[j]), cap * sizeof(MsgDev),
+                                      cudaHostAllocDefault), "cudaHostAlloc(msgs)");
+                if (!ws->ev_pin[j])
+                    SP_CUDA(cudaEventCreateWithFlags(&ws->ev_pin[j], cudaEventDisableTiming), "event");
+            }
+            ws->cap_pin = cap;
+        }
+        if (ws->ev_live[k]) SP_CUDA(cudaEventSynchronize(ws->ev_pin[k]), "cudaEventSynchronize");
+        memcpy(ws->h_pin[k], ws->h_msgs.data(), (size_t)n * sizeof(MsgDev));
+        SP_CUDA(cudaMemcpyAsync(ws->d_msgs, ws->h_pin[k], (size_t)n * sizeof(MsgDev), cudaMemcpyHostToDevice, s),
+                "cudaMemcpyAsync(msgs)");
+        SP_CUDA(cudaEventRecord(ws->ev_pin[k], s), "cudaEventRecord");
+        ws->ev_live[k] = true;
+    }
     p.msgs = ws->d_msgs;
     p.acc = ws->d_acc;
     p.nmsgs = (uint32_t)n;

@@ -58,7 +58,13 @@ struct MsgDev {
     uint32_t dir;
 };
 
+// Batches of up to kInline messages travel inside the kernel parameters (no
+// descriptor copy, no host staging on the launch path); larger batches use a
+// device array filled from a pinned staging ring.
+constexpr uint32_t kInline = 32;
+
 struct KParams {
+    MsgDev inl[kInline];
     uint32_t rk[60];
     const uint32_t *ttab;  // T0..T3 [4][256] then R8[256]
     const uint4 *mg;       // M_G[256], G = H^32
