@@ -401,7 +401,7 @@ def run_gpu(args) -> None:
         line["cpu_baseline"] = {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"8 x 32 MiB seal+open on 1 core via oracle/port.py "
                                           f"(cryptography AESGCM, encrypt_at/decrypt_at framing), {w1:.1f} s"}
-    if args.offload:
+    if not args.no_offload and world == 1:
         line["offload"] = offload_bench(args)
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -409,24 +409,32 @@ def run_gpu(args) -> None:
 
 
 def offload_bench(args) -> dict:
-    """OPT-66B-shaped FlexGen weight offload through the B200 engine vs the
-    same swaps as plain copies (the north star's 'within 10% of unencrypted
-    swap throughput')."""
+    """OPT-66B-shaped FlexGen weight offload (2 offloaded layers, 61 x 32 MiB
+    blocks each) through the B200 engine vs the same swaps as plain copies —
+    the north star's 'within 10% of unencrypted swap throughput'.  Runs
+    alternate plain / encrypted; best of `reps` each (host-side variance of
+    pinned-memory copies is large on a shared box)."""
     import torch
 
     from paper_2411_03357_b200 import workload
     from paper_2411_03357_b200.replay import ReplayConfig, run_engine, run_plain
 
     tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=args.offload_iters)
-    res_plain = run_plain(tr)
-    res_enc = run_engine(tr, ReplayConfig(system="specpipe", plane="gpu", record_stream=False))
-    rep = res_enc.engine.report()
-    torch.cuda.synchronize()
+    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast")
+    plain, enc, rep = [], [], None
+    for _ in range(args.offload_reps):
+        plain.append(run_plain(tr, fill="fast").swap_gbs)
+        r = run_engine(tr, cfg)
+        enc.append(r.swap_gbs)
+        rep = r.engine.report()
+        del r
+        torch.cuda.empty_cache()
     return {"model": "opt-66b", "layers_offloaded": 2, "iterations": args.offload_iters,
             "layer_bytes": workload.opt_layer_bytes("opt-66b"), "swap_bytes": tr.swap_bytes(),
-            "encrypted_gbs": round(res_enc.swap_gbs, 2), "plain_gbs": round(res_plain.swap_gbs, 2),
-            "throughput_ratio": round(res_enc.swap_gbs / res_plain.swap_gbs, 4),
-            "note": "tokens/s ratio == swap throughput ratio (same trace, same batch)",
+            "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
+            "encrypted_runs": [round(x, 2) for x in enc], "plain_runs": [round(x, 2) for x in plain],
+            "throughput_ratio": round(max(enc) / max(plain), 4),
+            "note": "tokens/s ratio == swap throughput ratio (same trace, same batch); random payload",
             "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "nops": rep["nops"],
             "sequence_hit_rate": rep["sequence_hit_rate"]}
 
@@ -438,8 +446,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--offload", action="store_true", help="also run the OPT-66B engine offload comparison")
+    ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=2)
+    ap.add_argument("--offload-reps", type=int, default=2)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -580,7 +581,38 @@ int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, bool open) {
 // ---- host-buffer pipeline ----------------------------------------------------
 // Pieces of ~kPieceBytes (whole rows) flow H2D (stream a) -> kernel (stream b)
 // -> D2H (stream c); each stage waits on the previous stage's event.
-constexpr uint64_t kPieceRows = (8ull << 20) / 512u;  // 8 MiB of payload per piece
+// Piece schedule of the host pipeline: pieces double from kPieceMinRows up to
+// max_piece_rows() and halve again over the tail, so the H2D of the first
+// piece and the D2H of the last one (the only un-overlapped transfers) are
+// small while the steady state runs on large copies.
+constexpr uint64_t kPieceMinRows = (1ull << 20) / 512u;  // 1 MiB
+
+uint64_t max_piece_rows() {
+    // 32 MiB by default; SPGCM_PIECE_MIB overrides (tuning)
+    static const uint64_t rows = [] {
+        const char *e = getenv("SPGCM_PIECE_MIB");
+        const long mib = e ? atol(e) : 32;
+        return (uint64_t)std::max(1L, mib) * (1ull << 20) / 512u;
+    }();
+    return rows;
+}
+
+std::vector<uint64_t> piece_schedule(uint64_t rows) {
+    std::vector<uint64_t> out;
+    const uint64_t cap = max_piece_rows();
+    uint64_t done = 0, cur = std::min(kPieceMinRows, cap);
+    while (done < rows) {
+        const uint64_t left = rows - done;
+        uint64_t take = std::min(cur, left);
+        if (left > take && left < 2 * take) take = std::max<uint64_t>(kPieceMinRows, left / 2);  // taper
+        take = std::min(take, left);
+        out.push_back(take);
+        done += take;
+        cur = std::min(cap, cur * 2);
+        if (rows - done < 2 * cur) cur = std::max<uint64_t>(kPieceMinRows, (rows - done) / 2);
+    }
+    return out;
+}
 
 struct HostPipe {
     int device = -1;
@@ -662,7 +694,8 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
         total += (d[i].len + 255u) & ~255ull;
         rows += rows_of(d[i].len);
     }
-    const size_t npieces = (size_t)((rows + kPieceRows - 1) / kPieceRows);
+    const std::vector<uint64_t> sched = piece_schedule(rows);
+    const size_t npieces = sched.size();
     int rc = ensure_pipe(hp, ctx->device, total, (size_t)n, npieces);
     if (rc) return rc;
 
@@ -691,7 +724,7 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
     size_t k = 0;
     const std::vector<MsgDev> &msgs = ws->h_msgs;
     while (g < rows) {
-        const uint64_t g_end = std::min(rows, g + kPieceRows);
+        const uint64_t g_end = std::min(rows, g + sched[k]);
         // H2D for every message slice in [g, g_end)
         int mj = mi;
         uint64_t gg = g;

@@ -67,6 +67,7 @@ class GpuPlane:
             self.s_spec = torch.cuda.Stream(self.device)
             self.s_h2d = torch.cuda.Stream(self.device)
             self.s_d2h = torch.cuda.Stream(self.device)
+            self.s_land = torch.cuda.Stream(self.device)
         self._host_ready: dict[int, Any] = {}  # block id -> event after last D2H into it
         self._h2d_done: dict[int, Any] = {}    # block id -> event after last H2D from it
         self._status = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
@@ -91,6 +92,7 @@ class GpuPlane:
         """Raise GcmAuthError if any open since the last check failed."""
         if self._status_used:
             self.s_comp.synchronize()
+            self.s_land.synchronize()
             self.s_d2h.synchronize()
             bad = int(self._status[:self._status_used].abs().sum().item())
             self._status[:self._status_used].zero_()
@@ -160,7 +162,7 @@ class GpuPlane:
         self.launches += 1
         ready = torch.cuda.Event()
         ready.record(self.s_comp)
-        buf.record_stream(self.s_d2h)
+        buf.record_stream(self.s_land)
         return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
 
     def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
@@ -202,21 +204,19 @@ class GpuPlane:
         self.launches += 1
 
     def land_on_host(self, block, jobs: list, direction: int) -> None:
-        """Host endpoint open of D2H messages, then the plaintext lands in
-        `block` (jobs: (msg, iv, offset_in_block)).  Both the open and the
-        copy run on the D2H stream, so landings overlap H2D traffic and the
-        compute stream's commits."""
+        """Host endpoint open of D2H messages (landing stream), then the
+        plaintext lands in `block` on the D2H copy stream (jobs: (msg, iv,
+        offset_in_block)).  Neither waits on the compute stream's commits, so
+        landings overlap the swap-ins; the copy engine is never held up by an
+        open kernel of a later landing."""
         torch = self.torch
         total = sum(m.declared_len for m, _, _ in jobs)
         waited = set()
         for m, _, _ in jobs:
             if m.ready is not None and id(m.ready) not in waited:
-                self.s_d2h.wait_event(m.ready)
+                self.s_land.wait_event(m.ready)
                 waited.add(id(m.ready))
-        pend = self._h2d_done.get(block.id)
-        if pend is not None:
-            self.s_d2h.wait_event(pend)
-        with torch.cuda.stream(self.s_d2h):
+        with torch.cuda.stream(self.s_land):
             buf = torch.empty(total, dtype=torch.uint8, device=self.device)
         items, places, off = [], [], 0
         for msg, iv, boff in jobs:
@@ -224,11 +224,20 @@ class GpuPlane:
             items.append((direction, iv, msg.payload, view, msg.auth_tag, msg.declared_len))
             places.append((view, boff, msg.declared_len))
             off += msg.declared_len
-        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_d2h)
+            if hasattr(msg.payload, "record_stream"):
+                msg.payload.record_stream(self.s_land)
+        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_land)
         self.launches += 1
+        opened = torch.cuda.Event()
+        opened.record(self.s_land)
+        self.s_d2h.wait_event(opened)
+        pend = self._h2d_done.get(block.id)
+        if pend is not None:
+            self.s_d2h.wait_event(pend)
         with torch.cuda.stream(self.s_d2h):
             for view, boff, n in places:
                 torch.from_numpy(block.data[boff:boff + n]).copy_(view, non_blocking=True)
+            buf.record_stream(self.s_d2h)
             ev = torch.cuda.Event()
             ev.record(self.s_d2h)
         self.bytes_d2h += total
@@ -270,6 +279,7 @@ class GpuPlane:
     def finish(self) -> None:
         self.s_comp.synchronize()
         self.s_spec.synchronize()
+        self.s_land.synchronize()
         self.s_h2d.synchronize()
         self.s_d2h.synchronize()
         self.check_auth()

@@ -35,6 +35,11 @@ class ReplayConfig:
     plane: str = "gpu"
     chunk_bytes: int = 32 * 1024 * 1024
     predictor_chunk_bytes: int | None = None  # default: PredictorConfig() as the reference driver
+    # "seeded": block payloads = prng_fill(content_seed), bit-exact with the
+    # reference (parity runs); "fast": device-generated random bytes copied to
+    # the pinned blocks (benchmarks: AES-CTR cost is data-independent, and
+    # seeding 4 GB at CPU speed would dominate setup time)
+    fill: str = "seeded"
 
 
 @dataclass
@@ -66,22 +71,53 @@ def build_engine(trace: Trace, config: ReplayConfig):
     blocks = {}
     for spec in header.blocks:
         if spec.resident == "cpu":
-            block = memory.alloc(spec.kind, spec.nbytes, prng_fill(spec.content_seed))
+            block = memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, config))
             if isinstance(spec.kind, (ModelLayer, KvCache)):
                 predictor.observe_swap_out(block.id)
         else:
             block = memory.alloc(spec.kind, spec.nbytes)
             if config.plane == "gpu":
-                import torch
-
-                host = torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes))
                 dev = engine.plane.new_device_buffer(spec.nbytes)
-                dev.copy_(host)
+                if config.fill == "fast":
+                    _fast_random(dev, spec.content_seed)
+                else:
+                    import torch
+
+                    dev.copy_(torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)))
                 engine.seed_device(block.id, dev)
             else:
                 engine.seed_device(block.id, engine.plane.new_device_buffer(spec.nbytes))
         blocks[spec.id] = (block, classify(spec.nbytes, header.profile, pconf))
     return engine, blocks
+
+
+def _fast_random(dev_tensor, seed: int) -> None:
+    import torch
+
+    g = torch.Generator(device=dev_tensor.device)
+    g.manual_seed(seed)
+    dev_tensor.copy_(torch.randint(0, 256, dev_tensor.shape, dtype=torch.uint8, device=dev_tensor.device,
+                                   generator=g))
+
+
+class _FastFill:
+    """Host block filler: random bytes made on the GPU, copied to pinned memory."""
+
+    def __init__(self, seed: int) -> None:
+        self.seed = seed
+
+    def fill_into(self, out) -> None:
+        import torch
+
+        dev = torch.empty(out.shape[0], dtype=torch.uint8, device="cuda")
+        _fast_random(dev, self.seed)
+        torch.from_numpy(out).copy_(dev)
+
+
+def _fill_for(spec, config: ReplayConfig):
+    if config.fill == "fast":
+        return _FastFill(spec.content_seed)
+    return prng_fill(spec.content_seed)
 
 
 def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool = False) -> ReplayResult:
@@ -125,7 +161,7 @@ def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConf
     engine.finish()
 
 
-def run_plain(trace: Trace, seed: int = 0) -> ReplayResult:
+def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded") -> ReplayResult:
     """NoCc on the GPU: the same swaps as plain pinned copies, no crypto."""
     import torch
 
@@ -133,12 +169,18 @@ def run_plain(trace: Trace, seed: int = 0) -> ReplayResult:
     dev = torch.device("cuda", torch.cuda.current_device())
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     blocks, device_mem = {}, {}
+    cfg = ReplayConfig(fill=fill)
     for spec in trace.header.blocks:
         if spec.resident == "cpu":
-            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes, prng_fill(spec.content_seed))
+            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, cfg))
         else:
             blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes)
-            device_mem[spec.id] = torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)).to(dev)
+            d = torch.empty(spec.nbytes, dtype=torch.uint8, device=dev)
+            if fill == "fast":
+                _fast_random(d, spec.content_seed)
+            else:
+                d.copy_(torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)))
+            device_mem[spec.id] = d
     torch.cuda.synchronize()
     pending_in: list = []
     t0 = time.perf_counter()
