@@ -419,18 +419,23 @@ def offload_bench(args) -> dict:
     from paper_2411_03357_b200 import workload
     from paper_2411_03357_b200.replay import ReplayConfig, run_engine, run_plain
 
-    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=args.offload_iters)
+    # one warm-up iteration (first touch of every block, allocator growth),
+    # then `offload_iters` timed iterations
+    iters = args.offload_iters + 1
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=iters)
+    start = len(tr.events) // iters
     cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast")
     plain, enc, rep = [], [], None
     for _ in range(args.offload_reps):
-        plain.append(run_plain(tr, fill="fast").swap_gbs)
-        r = run_engine(tr, cfg)
+        plain.append(run_plain(tr, fill="fast", measure_from=start).swap_gbs)
+        r = run_engine(tr, cfg, measure_from=start)
         enc.append(r.swap_gbs)
         rep = r.engine.report()
         del r
         torch.cuda.empty_cache()
     return {"model": "opt-66b", "layers_offloaded": 2, "iterations": args.offload_iters,
-            "layer_bytes": workload.opt_layer_bytes("opt-66b"), "swap_bytes": tr.swap_bytes(),
+            "layer_bytes": workload.opt_layer_bytes("opt-66b"), "swap_bytes_timed": tr.swap_bytes() * args.offload_iters // iters,
+            "warmup_iterations": 1,
             "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
             "encrypted_runs": [round(x, 2) for x in enc], "plain_runs": [round(x, 2) for x in plain],
             "throughput_ratio": round(max(enc) / max(plain), 4),
@@ -448,7 +453,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=2)
-    ap.add_argument("--offload-reps", type=int, default=2)
+    ap.add_argument("--offload-reps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

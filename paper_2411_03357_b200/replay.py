@@ -115,33 +115,52 @@ class _FastFill:
 
 
 def _fill_for(spec, config: ReplayConfig):
+    if config.plane == "dry":
+        return None  # the dry plane never reads payload bytes
     if config.fill == "fast":
         return _FastFill(spec.content_seed)
     return prng_fill(spec.content_seed)
 
 
-def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool = False) -> ReplayResult:
+def _swap_bytes_from(trace: Trace, start: int) -> int:
+    size = {b.id: b.nbytes for b in trace.header.blocks}
+    return sum(size[e.block] for e in trace.events[start:] if isinstance(e, (SwapOut, SwapInRequest)))
+
+
+def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool = False,
+               measure_from: int = 0) -> ReplayResult:
     """Replay `trace`; with `catch`, an engine exception (e.g. the reference's
     defect C2 EngineError) is returned in `error` with the engine state at
-    the point of failure, as the parity harness needs."""
+    the point of failure, as the parity harness needs.  With `measure_from`,
+    the clock starts (after draining the GPU) at that event index and
+    `swap_bytes` counts only the swaps from there on (warm-up excluded)."""
     engine, blocks = build_engine(trace, config)
     if config.plane == "gpu":
         engine.plane.finish()
-    t0 = time.perf_counter()
+    mark = {"t0": time.perf_counter()}
+
+    def at_mark() -> None:
+        if config.plane == "gpu":
+            engine.plane.finish()
+        mark["t0"] = time.perf_counter()
+
     try:
-        _dispatch_all(engine, blocks, trace, config)
+        _dispatch_all(engine, blocks, trace, config, measure_from, at_mark)
     except Exception as exc:
         if not catch:
             raise
-        return ReplayResult(engine, time.perf_counter() - t0, trace.swap_bytes(), trace.payload_bytes(),
+        return ReplayResult(engine, time.perf_counter() - mark["t0"], trace.swap_bytes(), trace.payload_bytes(),
                             f"{type(exc).__name__}: {exc}")
-    wall = time.perf_counter() - t0
-    return ReplayResult(engine, wall, trace.swap_bytes(), trace.payload_bytes())
+    wall = time.perf_counter() - mark["t0"]
+    return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
 
 
-def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig) -> None:
+def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,
+                  at_mark=None) -> None:
     io_index = 0
-    for ev in trace.events:
+    for k, ev in enumerate(trace.events):
+        if k == measure_from and k and at_mark is not None:
+            at_mark()
         if isinstance(ev, SwapInRequest):
             block, cls = blocks[ev.block]
             engine.copy_h2d(CopyRequest("h2d", block.base, block.len, cls, block_id=block.id, submit_time=ev.t))
@@ -161,7 +180,7 @@ def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConf
     engine.finish()
 
 
-def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded") -> ReplayResult:
+def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: int = 0) -> ReplayResult:
     """NoCc on the GPU: the same swaps as plain pinned copies, no crypto."""
     import torch
 
@@ -184,7 +203,10 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded") -> ReplayResult
     torch.cuda.synchronize()
     pending_in: list = []
     t0 = time.perf_counter()
-    for ev in trace.events:
+    for k, ev in enumerate(trace.events):
+        if k == measure_from and k:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
         if isinstance(ev, SwapInRequest):
             b = blocks[ev.block]
             with torch.cuda.stream(s_h2d):
@@ -209,4 +231,4 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded") -> ReplayResult
                     payload.to(dev, non_blocking=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    return ReplayResult(None, wall, trace.swap_bytes(), trace.payload_bytes())
+    return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())

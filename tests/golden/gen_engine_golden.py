@@ -72,6 +72,16 @@ def cases():
             out.append((f"adv_{pol}_{rate}_{s}", {"gen": "adversarial", "policy": pol, "rate": rate, "seed": s,
                                                   "requests": 12, "kv_block_bytes": 28 * KIB, "parallel_size": 4}))
     out.append(("activation_l10", {"gen": "activation", "layers": 10, "act_bytes": 48 * KIB + 3, "steps": 3}))
+    # full-size shapes, replayed on the GPU by the
+    # slow-marked parity test
+    out.append(("full_kv_opt30b_lifo_adv", {"gen": "adversarial", "policy": "lifo", "rate": 0.25, "seed": 8,
+                                            "requests": 12, "kv_block_bytes": 229_376, "parallel_size": 4}))
+    out.append(("full_kv_opt30b_fifo", {"gen": "kvswap", "requests": 12, "policy": "fifo",
+                                        "kv_block_bytes": 229_376, "parallel_size": 4, "small_io_size": 2048,
+                                        "seed": 0}))
+    out.append(("full_act_opt30b", {"gen": "activation", "layers": 4, "act_bytes": 29_360_128, "steps": 2}))
+    out.append(("full_offload_opt13b", {"gen": "opt_offload", "model": "opt-13b", "offload": [21, 22],
+                                        "iterations": 2}))
     return out
 
 
@@ -90,7 +100,50 @@ def make_trace(p: dict) -> Trace:
         return workload.gen_adversarial_trace(base, p["rate"], seed=p["seed"])
     if g == "activation":
         return activation_trace(p["layers"], p["act_bytes"], p["steps"])
+    if g == "opt_offload":
+        return opt_offload_trace(p["model"], p["offload"], p["iterations"])
     raise ValueError(g)
+
+
+OPT = {"opt-13b": (5120, 40), "opt-30b": (7168, 48), "opt-66b": (9216, 64)}
+
+
+def opt_offload_trace(model: str, offload, iterations: int, chunk: int = 32 * 1024 * 1024) -> Trace:
+    """Config 2 shape: each OPT layer (2*(12h^2+13h) bytes) split into 32 MiB
+    blocks + tail so the reference classifies them MODEL_WEIGHTS (defect C3)."""
+    import random
+
+    h, nl = OPT[model]
+    layer = 2 * (12 * h * h + 13 * h)
+    sizes = [chunk] * (layer // chunk) + ([layer % chunk] if layer % chunk else [])
+    rng = random.Random(0)
+    profile = ModelProfile(model, layer, 16 * h * 2)
+    blocks, of, nid = [], {}, 1
+    for l in sorted(offload):
+        of[l] = []
+        for n in sizes:
+            blocks.append(BlockSpec(id=nid, kind=ModelLayer(l), nbytes=n, resident="cpu",
+                                    content_seed=rng.randrange(1 << 30)))
+            of[l].append(nid)
+            nid += 1
+    ev, t = [], 0
+    for _ in range(iterations):
+        for l in range(1, nl + 1):
+            ids = of.get(l)
+            if ids:
+                ev.extend(SwapInRequest(t, b) for b in ids)
+                ev.append(SyncEvent(t))
+                t += 1
+            ev.append(ComputeEvent(t, 200_000))
+            t += 1
+            if ids:
+                ev.extend(SwapOut(t, b) for b in ids)
+                t += 1
+    params = {"generator": "opt_offload", "model": model, "offload": sorted(offload), "iterations": iterations,
+              "chunk_bytes": chunk, "layer_bytes": layer, "compute_per_layer": 200_000, "seed": 0}
+    tr = Trace(TraceHeader(SCHEMA_VERSION, profile, params, tuple(blocks)), ev)
+    workload.validate_trace(tr)
+    return tr
 
 
 def action_tuple(a):
