@@ -27,24 +27,42 @@ using namespace spgcm;
 // =============================================================================
 
 __device__ __forceinline__ void fill_tables(uint8_t *sm, const KParams &p) {
-    // AES: 2 regions x 256 entries x 2 tables x 8 uint4 (4 copies each)
-    for (uint32_t f = threadIdx.x; f < 2u * 256u * 2u * 8u; f += blockDim.x) {
-        const uint32_t c4 = f & 7u, t = (f >> 3) & 1u, v = (f >> 4) & 255u, pr = f >> 12;
-        const uint32_t val = __ldg(p.ttab + (2u * pr + t) * 256u + v);
-        *reinterpret_cast<uint4 *>(sm + pr * 65536u + v * 256u + t * 128u + c4 * 16u) =
-            make_uint4(val, val, val, val);
+    // 8192 AES stores + 4096 GHASH stores of 16 B = 24 per thread.  All global
+    // loads are issued before any store so their latencies overlap (the tables
+    // are usually evicted from L2 by the payload stream: one DRAM round trip
+    // per CTA instead of 24 dependent ones).
+    static_assert((2u * 256u * 2u * 8u) % kThreads == 0 && (256u * 16u) % kThreads == 0, "fill split");
+    constexpr int kA = (2 * 256 * 2 * 8) / kThreads, kG = (256 * 16) / kThreads;
+    uint32_t aval[kA];
+    uint4 gval[kG];
+#pragma unroll
+    for (int j = 0; j < kA; ++j) {
+        const uint32_t f = threadIdx.x + (uint32_t)j * kThreads;
+        const uint32_t t = (f >> 3) & 1u, v = (f >> 4) & 255u, pr = f >> 12;
+        aval[j] = __ldg(p.ttab + (2u * pr + t) * 256u + v);
     }
-    // GHASH: 256 entries x (8 M copies + 8 uint4 of R8 copies)
-    for (uint32_t f = threadIdx.x; f < 256u * 16u; f += blockDim.x) {
-        const uint32_t s = f & 15u, v = f >> 4;
-        uint4 val;
-        if (s < 8u) {
-            val = __ldg(p.mg + v);
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+        const uint32_t f = threadIdx.x + (uint32_t)j * kThreads;
+        const uint32_t sidx = f & 15u, v = f >> 4;
+        if (sidx < 8u) {
+            gval[j] = __ldg(p.mg + v);
         } else {
             const uint32_t r = __ldg(p.ttab + 4u * 256u + v);
-            val = make_uint4(r, r, r, r);
+            gval[j] = make_uint4(r, r, r, r);
         }
-        *reinterpret_cast<uint4 *>(sm + kSmGh + v * 256u + s * 16u) = val;
+    }
+#pragma unroll
+    for (int j = 0; j < kA; ++j) {
+        const uint32_t f = threadIdx.x + (uint32_t)j * kThreads;
+        const uint32_t c4 = f & 7u, t = (f >> 3) & 1u, v = (f >> 4) & 255u, pr = f >> 12;
+        *reinterpret_cast<uint4 *>(sm + pr * 65536u + v * 256u + t * 128u + c4 * 16u) =
+            make_uint4(aval[j], aval[j], aval[j], aval[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+        const uint32_t f = threadIdx.x + (uint32_t)j * kThreads;
+        *reinterpret_cast<uint4 *>(sm + kSmGh + (f >> 4) * 256u + (f & 15u) * 16u) = gval[j];
     }
 }
 

@@ -145,6 +145,9 @@ class GpuPlane:
             ready.record(self.s_spec)
         return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
 
+    def spec_batch(self) -> "SpecBatch":
+        return SpecBatch(self)
+
     def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
         """Seal device plaintext `src` chunk-wise into a fresh staging buffer
         (compute stream); messages carry a `ready` event for other streams."""
@@ -285,6 +288,65 @@ class GpuPlane:
         self.check_auth()
 
 
+class SpecBatch:
+    """Encrypt-ahead work of one engine entry point: one H2D copy per block
+    as tasks are added, ONE sealing launch on the speculation stream at
+    `launch()`.  Every message shares the batch's `ready` event (recorded at
+    launch, before any consumer can wait on it)."""
+
+    def __init__(self, plane: "GpuPlane") -> None:
+        self.plane = plane
+        self.items: list = []
+        self.ready = plane.torch.cuda.Event()
+        self.last_copy = None
+
+    def add(self, block, inner: int, spans: list, direction: int, iv0: int) -> list:
+        p, torch = self.plane, self.plane.torch
+        total = sum(n for _, n in spans)
+        first = spans[0][0]
+        ev = p._host_ready.get(block.id)
+        if ev is not None:
+            p.s_h2d.wait_event(ev)
+        src = torch.from_numpy(block.data[inner + first: inner + first + total])
+        with torch.cuda.stream(p.s_h2d):
+            buf = torch.empty(total + TAG * len(spans), dtype=torch.uint8, device=p.device)
+            buf[:total].copy_(src if block.pinned is not None else src.pin_memory(), non_blocking=True)
+            buf.record_stream(p.s_comp)
+            buf.record_stream(p.s_spec)
+            done = torch.cuda.Event()
+            done.record(p.s_h2d)
+        p._h2d_done[block.id] = done
+        p.bytes_h2d += total
+        self.last_copy = done
+        msgs = []
+        for i, (off, n) in enumerate(spans):
+            view = buf[off - first: off - first + n]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            self.items.append((direction, iv0 + i, view, view, tag, n))
+            msgs.append(DeviceCiphertext(view, tag, n, ready=self.ready))
+        return msgs
+
+    def launch(self) -> None:
+        if not self.items:
+            return
+        p = self.plane
+        p.s_spec.wait_event(self.last_copy)
+        p.ctx.seal_batch(self.items, p.s_spec)
+        p.launches += 1
+        self.ready.record(p.s_spec)
+
+
+class _DrySpecBatch:
+    def __init__(self, plane) -> None:
+        self.plane = plane
+
+    def add(self, block, inner, spans, direction, iv0):
+        return self.plane.seal_host_chunks(block, inner, spans, direction, iv0, speculative=True)
+
+    def launch(self) -> None:
+        pass
+
+
 @dataclass(eq=False)
 class _DryPayload:
     n: int
@@ -313,6 +375,9 @@ class DryPlane:
     def seal_host_chunks(self, block, inner, spans, direction, iv0, speculative=False):
         self.bytes_h2d += sum(n for _, n in spans)
         return self._msgs([n for _, n in spans])
+
+    def spec_batch(self):
+        return _DrySpecBatch(self)
 
     def seal_device_chunks(self, src, spans, direction, iv0):
         return self._msgs([n for _, n in spans])

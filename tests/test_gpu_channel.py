@@ -137,7 +137,11 @@ def test_engine_tamper_detected():
     eng.speculate_tick()
     eng._complete_spec_tasks()
     rec = eng.validator.pending_records()[0]
+    import torch
+
+    torch.cuda.synchronize()  # let the speculative seal finish before tampering
     rec.chunks[0].payload[100] ^= 1
+    torch.cuda.synchronize()
     with pytest.raises(GcmAuthError):
         eng.copy_h2d(CopyRequest("h2d", b.base, b.len, TransferClass.MODEL_WEIGHTS, block_id=b.id))
 
