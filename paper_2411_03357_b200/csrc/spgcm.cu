@@ -112,8 +112,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
 
     // contiguous, balanced row range for this warp
     const uint64_t total = p.row_end - p.row_begin;
-    const uint64_t gw = (uint64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-    const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+    const uint32_t warp = threadIdx.x >> 5;
+    if (warp >= p.warps_used) return;
+    const uint64_t gw = (uint64_t)blockIdx.x * p.warps_used + warp;
+    const uint64_t nw = (uint64_t)gridDim.x * p.warps_used;
     uint64_t g = p.row_begin + (total * gw) / nw;
     const uint64_t g_end = p.row_begin + (total * (gw + 1)) / nw;
     if (g >= g_end) return;
@@ -148,6 +150,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             return load_bytes(ptr, nb);
         };
 
+        // Prefetch into L2 the F / H^(32b) rows this lane's epilogue reads
+        // (2 lines each; cold in HBM otherwise): overlaps two of the
+        // epilogue's dependent DRAM round trips with the row loop.
+        {
+            const uint32_t r_end_pf = md.rows - (uint32_t)t_b;
+            const char *ft = reinterpret_cast<const char *>(p.nt + (size_t)(kNtF + (r_end_pf >> 4)) * kNtEntries + lane * 16);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ft));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ft + 128));
+            if (r_end_pf & 15u) {
+                const char *pt = reinterpret_cast<const char *>(
+                    p.nt + (size_t)(kNtP32 + (r_end_pf & 15u) - 1u) * kNtEntries + lane * 16);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pt));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + 128));
+            }
+        }
+        const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);
         const CtrConst cc = ctr_const(p.rk, lct, x0, x1, x2);
         CtrCache ck;
         ck.gid = 0xffffffffu;
@@ -182,7 +200,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
         w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
         if (r_end & 15u) w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
 
-        const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);
         if (t_a == 0 && t_b == md.rows) {
             const uint4 S = xor4(w, warp_xor(lh_part));
             finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
@@ -489,10 +506,20 @@ int check_desc(const sp_desc &d) {
 
 uint32_t rows_of(uint64_t len) { return (uint32_t)((((len + 15u) >> 4) + 31u) >> 5); }
 
-int grid_for(const sp_ctx *ctx, uint64_t rows) {
-    // >= 4 rows per warp before adding CTAs; at most one CTA per SM
-    const uint64_t want = (rows + (uint64_t)kWarpsPerCta * 4u - 1u) / ((uint64_t)kWarpsPerCta * 4u);
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)ctx->num_sms));
+// Launch shape.  Every warp that owns rows ends its run with a 32-lane GHASH
+// combine whose nibble-table lookups hit 32 different L2 lines per load
+// (1,024 L2 requests per warp): fine for big batches (one combine per ~260
+// rows), but for small batches it is the whole cost if 16 warps of one SM do
+// it at once.  So small batches spread few working warps over many SMs
+// (>= 8 rows per warp); big ones use all 16 warps of every SM.
+// Tiny messages (NOP pads, tokens) are latency-bound in their epilogue, so a
+// batch also gets at least one warp per message.
+void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
+    const uint64_t sms = (uint64_t)ctx->num_sms;
+    const uint64_t want_warps =
+        std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / 8u, std::min(nmsgs, rows)), sms * kWarpsPerCta));
+    warps_used = (uint32_t)((want_warps + sms - 1) / sms);
+    grid = (int)((want_warps + warps_used - 1) / warps_used);
 }
 
 int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
@@ -516,7 +543,8 @@ int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_e
     if (row_end <= row_begin) return SP_OK;
     p.row_begin = row_begin;
     p.row_end = row_end;
-    const int grid = grid_for(ctx, row_end - row_begin);
+    int grid = 1;
+    launch_shape(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
     k_gcm<<<grid, kThreads, kSmemBytes, s>>>(p);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     SP_CUDA(cudaGetLastError(), "k_gcm launch");

@@ -75,6 +75,7 @@ struct KParams {
     uint64_t row_end;
     uint32_t nmsgs;
     uint32_t open;
+    uint32_t warps_used;   // warps per CTA that own rows (<= kWarpsPerCta)
 };
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }

@@ -1,0 +1,41 @@
+// Per-launch cost of small seal batches from C (no Python in the loop).
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <vector>
+#include "spgcm.h"
+
+int main() {
+    uint8_t key[32];
+    for (int i = 0; i < 32; ++i) key[i] = (uint8_t)i;
+    sp_ctx *ctx = nullptr;
+    if (sp_ctx_create(key, &ctx) != SP_OK) { printf("ctx: %s\n", sp_last_error()); return 1; }
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    const size_t sizes[] = {1, 2048, 65536, 229376, 1 << 20, 4 << 20, 32 << 20};
+    uint8_t *buf, *out, *tags;
+    cudaMalloc(&buf, 64u << 20);
+    cudaMalloc(&out, 64u << 20);
+    cudaMalloc(&tags, 16 * 64);
+    cudaMemset(buf, 7, 64u << 20);
+    for (size_t n : sizes) {
+        for (int nmsg : {1, 8, 32}) {
+            if (n * nmsg > (64u << 20)) continue;
+            std::vector<sp_desc> d(nmsg);
+            for (int i = 0; i < nmsg; ++i) d[i] = sp_desc{0, 0, (uint64_t)i, n, buf + i * n, out + i * n, tags + 16 * i, nullptr};
+            for (int w = 0; w < 20; ++w) sp_seal_batch(ctx, d.data(), nmsg, s);
+            cudaStreamSynchronize(s);
+            const int reps = 200;
+            cudaEvent_t a, b;
+            cudaEventCreate(&a); cudaEventCreate(&b);
+            cudaEventRecord(a, s);
+            for (int r = 0; r < reps; ++r) sp_seal_batch(ctx, d.data(), nmsg, s);
+            cudaEventRecord(b, s);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            printf("msgs=%2d x %9zu B : %8.2f us/launch  %8.2f GB/s\n", nmsg, n, ms * 1000 / reps,
+                   (double)n * nmsg * reps / (ms * 1e6));
+        }
+    }
+    sp_ctx_destroy(ctx);
+    return 0;
+}
