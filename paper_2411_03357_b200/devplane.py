@@ -70,6 +70,10 @@ class GpuPlane:
             self.s_land = torch.cuda.Stream(self.device)
         self._host_ready: dict[int, Any] = {}  # block id -> event after last D2H into it
         self._h2d_done: dict[int, Any] = {}    # block id -> event after last H2D from it
+        self._d2h_seals: list = []      # deferred swap-out seal descriptors
+        self._d2h_ready = torch.cuda.Event()
+        self._landings: list = []       # deferred host-endpoint opens + D2H copies
+        self._d2h_bytes = 0
         self._status = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
         self._status_used = 0
         self.bytes_h2d = 0
@@ -90,6 +94,7 @@ class GpuPlane:
 
     def check_auth(self) -> None:
         """Raise GcmAuthError if any open since the last check failed."""
+        self.flush_d2h()
         if self._status_used:
             self.s_comp.synchronize()
             self.s_land.synchronize()
@@ -110,6 +115,7 @@ class GpuPlane:
         `ready` event that the committing open waits on; on-the-fly seals run
         on the compute stream in issue order."""
         torch = self.torch
+        self.flush_d2h()
         total = sum(n for _, n in spans)
         first = spans[0][0]
         ev = self._host_ready.get(block.id)
@@ -149,28 +155,82 @@ class GpuPlane:
         return SpecBatch(self)
 
     def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
-        """Seal device plaintext `src` chunk-wise into a fresh staging buffer
-        (compute stream); messages carry a `ready` event for other streams."""
-        torch = self.torch
+        """Seal device plaintext `src` chunk-wise into fresh staging.  The
+        launch is deferred and merged with the following swap-outs (up to
+        BATCH_BYTES, or until any other device work needs ordering): one
+        sealing launch for a whole KV eviction instead of one per block."""
         total = sum(n for _, n in spans)
         first = spans[0][0]
         buf = self._empty(total + TAG * len(spans))
-        items, views = [], []
+        buf.record_stream(self.s_land)
+        msgs = []
         for i, (off, n) in enumerate(spans):
             view = buf[off - first: off - first + n]
             tag = buf[total + TAG * i: total + TAG * (i + 1)]
-            items.append((direction, iv0 + i, src[off:off + n], view, tag, n))
-            views.append((view, tag, n))
-        self.ctx.seal_batch(items, self.s_comp)
+            self._d2h_seals.append((direction, iv0 + i, src[off:off + n], view, tag, n))
+            msgs.append(DeviceCiphertext(view, tag, n, ready=self._d2h_ready))
+        self._d2h_bytes += total
+        return msgs
+
+    def flush_d2h(self) -> None:
+        """Issue the deferred swap-out work: one sealing launch (compute
+        stream), one host-endpoint open launch for every pending landing
+        (landing stream), then the D2H copies per block (copy stream)."""
+        torch = self.torch
+        if self._d2h_seals:
+            self.ctx.seal_batch(self._d2h_seals, self.s_comp)
+            self.launches += 1
+            self._d2h_ready.record(self.s_comp)
+            self._d2h_seals = []
+            self._d2h_ready = torch.cuda.Event()
+        if not self._landings:
+            self._d2h_bytes = 0
+            return
+        landings, self._landings = self._landings, []
+        self._d2h_bytes = 0
+        waited = set()
+        total = 0
+        for _, jobs, _ in landings:
+            for m, _, _ in jobs:
+                total += m.declared_len
+                if m.ready is not None and id(m.ready) not in waited:
+                    self.s_land.wait_event(m.ready)
+                    waited.add(id(m.ready))
+        with torch.cuda.stream(self.s_land):
+            buf = torch.empty(total, dtype=torch.uint8, device=self.device)
+        items, places, off = [], [], 0
+        for block, jobs, direction in landings:
+            for msg, iv, boff in jobs:
+                view = buf[off:off + msg.declared_len]
+                items.append((direction, iv, msg.payload, view, msg.auth_tag, msg.declared_len))
+                places.append((block, view, boff, msg.declared_len))
+                off += msg.declared_len
+                msg.payload.record_stream(self.s_land)
+        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_land)
         self.launches += 1
-        ready = torch.cuda.Event()
-        ready.record(self.s_comp)
-        buf.record_stream(self.s_land)
-        return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
+        opened = torch.cuda.Event()
+        opened.record(self.s_land)
+        self.s_d2h.wait_event(opened)
+        with torch.cuda.stream(self.s_d2h):
+            last = None
+            for block, view, boff, n in places:
+                if block is not last:
+                    pend = self._h2d_done.get(block.id)
+                    if pend is not None:
+                        self.s_d2h.wait_event(pend)
+                    last = block
+                torch.from_numpy(block.data[boff:boff + n]).copy_(view, non_blocking=True)
+            buf.record_stream(self.s_d2h)
+            ev = torch.cuda.Event()
+            ev.record(self.s_d2h)
+        for block, _, _ in landings:
+            self._host_ready[block.id] = ev
+        self.bytes_d2h += total
 
     def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
         """Seal small host payloads (NOP pads, token I/O) in one launch."""
         torch = self.torch
+        self.flush_d2h()
         total = sum(len(p) for p in payloads)
         staged = torch.empty(total, dtype=torch.uint8, pin_memory=True)
         staged.numpy()[:] = memoryview(b"".join(payloads)).cast("B")
@@ -194,6 +254,7 @@ class GpuPlane:
         scratch so their tags are still verified."""
         if not jobs:
             return
+        self.flush_d2h()  # a pending swap-out seal may read a buffer this open writes
         items = []
         waited = set()
         for msg, iv, dst in jobs:
@@ -207,47 +268,18 @@ class GpuPlane:
         self.launches += 1
 
     def land_on_host(self, block, jobs: list, direction: int) -> None:
-        """Host endpoint open of D2H messages (landing stream), then the
-        plaintext lands in `block` on the D2H copy stream (jobs: (msg, iv,
-        offset_in_block)).  Neither waits on the compute stream's commits, so
-        landings overlap the swap-ins; the copy engine is never held up by an
-        open kernel of a later landing."""
-        torch = self.torch
-        total = sum(m.declared_len for m, _, _ in jobs)
-        waited = set()
-        for m, _, _ in jobs:
-            if m.ready is not None and id(m.ready) not in waited:
-                self.s_land.wait_event(m.ready)
-                waited.add(id(m.ready))
-        with torch.cuda.stream(self.s_land):
-            buf = torch.empty(total, dtype=torch.uint8, device=self.device)
-        items, places, off = [], [], 0
-        for msg, iv, boff in jobs:
-            view = buf[off:off + msg.declared_len]
-            items.append((direction, iv, msg.payload, view, msg.auth_tag, msg.declared_len))
-            places.append((view, boff, msg.declared_len))
-            off += msg.declared_len
-            if hasattr(msg.payload, "record_stream"):
-                msg.payload.record_stream(self.s_land)
-        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_land)
-        self.launches += 1
-        opened = torch.cuda.Event()
-        opened.record(self.s_land)
-        self.s_d2h.wait_event(opened)
-        pend = self._h2d_done.get(block.id)
-        if pend is not None:
-            self.s_d2h.wait_event(pend)
-        with torch.cuda.stream(self.s_d2h):
-            for view, boff, n in places:
-                torch.from_numpy(block.data[boff:boff + n]).copy_(view, non_blocking=True)
-            buf.record_stream(self.s_d2h)
-            ev = torch.cuda.Event()
-            ev.record(self.s_d2h)
-        self.bytes_d2h += total
-        self._host_ready[block.id] = ev
+        """Host endpoint open of D2H messages, then the plaintext lands in
+        `block` (jobs: (msg, iv, offset_in_block)).  Deferred and batched with
+        the swap-out seals (see flush_d2h); the landing's open and copy never
+        wait on the compute stream's commits, so landings overlap swap-ins."""
+        self._landings.append((block, jobs, direction))
+        self._d2h_bytes += sum(m.declared_len for m, _, _ in jobs)
+        if self._d2h_bytes >= BATCH_BYTES:
+            self.flush_d2h()
 
     def host_sync(self, block_id: int | None = None) -> None:
         """Wait until D2H landings are visible to the host."""
+        self.flush_d2h()
         if block_id is None:
             self.s_d2h.synchronize()
             return
@@ -258,6 +290,7 @@ class GpuPlane:
     def before_host_write(self, block_id: int) -> None:
         """The host is about to mutate `block_id`: in-flight copies that
         read or write it must be finished first."""
+        self.flush_d2h()
         for table in (self._h2d_done, self._host_ready):
             ev = table.get(block_id)
             if ev is not None:
@@ -276,10 +309,13 @@ class GpuPlane:
         return view.cpu().numpy().tobytes()
 
     def digests(self, views: list) -> list:
+        self.flush_d2h()
         self.s_comp.synchronize()
+        self.s_land.synchronize()
         return [hashlib.sha256(v.cpu().numpy().tobytes()).hexdigest() for v in views]
 
     def finish(self) -> None:
+        self.flush_d2h()
         self.s_comp.synchronize()
         self.s_spec.synchronize()
         self.s_land.synchronize()
@@ -288,20 +324,26 @@ class GpuPlane:
         self.check_auth()
 
 
+BATCH_BYTES = 64 * 1024 * 1024  # flush a batched launch once it covers this much payload
+
+
 class SpecBatch:
     """Encrypt-ahead work of one engine entry point: one H2D copy per block
-    as tasks are added, ONE sealing launch on the speculation stream at
-    `launch()`.  Every message shares the batch's `ready` event (recorded at
-    launch, before any consumer can wait on it)."""
+    as tasks are added; sealing launches on the speculation stream cover up
+    to BATCH_BYTES each (small KV blocks share one launch, big weight chunks
+    start sealing while later chunks are still crossing PCIe).  Messages of a
+    sub-batch share its `ready` event, recorded before any consumer waits."""
 
     def __init__(self, plane: "GpuPlane") -> None:
         self.plane = plane
         self.items: list = []
+        self.bytes = 0
         self.ready = plane.torch.cuda.Event()
         self.last_copy = None
 
     def add(self, block, inner: int, spans: list, direction: int, iv0: int) -> list:
         p, torch = self.plane, self.plane.torch
+        p.flush_d2h()  # pending landings into this host block must be recorded first
         total = sum(n for _, n in spans)
         first = spans[0][0]
         ev = p._host_ready.get(block.id)
@@ -324,6 +366,9 @@ class SpecBatch:
             tag = buf[total + TAG * i: total + TAG * (i + 1)]
             self.items.append((direction, iv0 + i, view, view, tag, n))
             msgs.append(DeviceCiphertext(view, tag, n, ready=self.ready))
+        self.bytes += total
+        if self.bytes >= BATCH_BYTES:
+            self.launch()
         return msgs
 
     def launch(self) -> None:
@@ -334,6 +379,8 @@ class SpecBatch:
         p.ctx.seal_batch(self.items, p.s_spec)
         p.launches += 1
         self.ready.record(p.s_spec)
+        self.items, self.bytes = [], 0
+        self.ready = p.torch.cuda.Event()
 
 
 class _DrySpecBatch:
@@ -378,6 +425,9 @@ class DryPlane:
 
     def spec_batch(self):
         return _DrySpecBatch(self)
+
+    def flush_d2h(self):
+        pass
 
     def seal_device_chunks(self, src, spans, direction, iv0):
         return self._msgs([n for _, n in spans])
