@@ -81,9 +81,11 @@ def barrier(dist, device=None) -> None:
 
 # -- clocks -----------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line) started before and
+    stopped after the measured work; `mark()` brackets the timed regions and
+    only samples inside them are summarised (all samples if none fall inside)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -91,13 +93,14 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.windows: list = []
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(prefix="clk", suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -105,6 +108,7 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        time.sleep(0.05)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -112,22 +116,33 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def mark(self, t0: float, t1: float) -> None:
+        self.windows.append((t0, t1))
+
     def summary(self) -> dict:
+        import datetime
+
         rows = []
         try:
             for ln in open(self.path):
                 parts = [p.strip() for p in ln.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
-                    rows.append(parts)
+                if len(parts) >= 10 and parts[2].replace(".", "").isdigit():
+                    try:
+                        ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    except ValueError:
+                        ts = None
+                    rows.append((ts, parts[1:]))
         except OSError:
             pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in rows]
+        inside = [r for ts, r in rows if ts is not None and any(a - 0.02 <= ts <= b + 0.02 for a, b in self.windows)]
+        use = inside or [r for _, r in rows]
+        sm = [float(r[1]) for r in use]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "samples": len(rows)}
+        reasons = sorted({n for r in use for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(use[0][2]), "reasons": reasons,
+                "samples": len(use), "samples_in_timed_regions": len(inside)}
 
 
 # -- peaks / profiles -----------------------------------------------------------------
@@ -286,9 +301,11 @@ def run_gpu(args) -> None:
     barrier(dist, dev)
     torch.cuda.synchronize()
     launches0 = _native.launch_count()
-    with ClockSampler(local) as clk:
+    clk = ClockSampler(local).__enter__()
+    if True:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        wall0 = time.time()
         t_start.record(stream)
         for k in range(K):
             ev[k][0].record(stream)
@@ -298,6 +315,7 @@ def run_gpu(args) -> None:
             ev[k][2].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
+        clk.mark(wall0, time.time())
     gpu_launches = _native.launch_count() - launches0
     barrier(dist, dev)
     ms_local = t_start.elapsed_time(t_end) / K
@@ -326,9 +344,12 @@ def run_gpu(args) -> None:
     KE = max(1, min(K, 5))
     barrier(dist, dev)
     t0 = time.perf_counter()
+    w0 = time.time()
     for _ in range(KE):
         e2e_step()
     e2e_ms_local = (time.perf_counter() - t0) * 1000.0 / KE
+    clk.mark(w0, time.time())
+    clk.__exit__(None, None, None)
     barrier(dist, dev)
     e2e_ms = reduce_max(dist, e2e_ms_local, dev)
     e2e_value = 2 * total / (e2e_ms / 1000.0) / 1e9 * world
@@ -396,11 +417,12 @@ def run_gpu(args) -> None:
     }
 
     if not args.no_cpu_baseline:
-        sample_sizes = layer_sizes()[:8]
-        g1, w1 = cpu_sample(1, sample_sizes)
+        sizes_all = layer_sizes()
+        g1, w1 = cpu_sample(1, sizes_all, reps=args.cpu_reps)
         line["cpu_baseline"] = {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "port",
-                                "sample": f"8 x 32 MiB seal+open on 1 core via oracle/port.py "
-                                          f"(cryptography AESGCM, encrypt_at/decrypt_at framing), {w1:.1f} s"}
+                                "sample": f"the OPT-13B layer ({len(sizes_all)} messages) sealed+opened "
+                                          f"{args.cpu_reps}x on 1 core via oracle/port.py (cryptography AESGCM "
+                                          f"with encrypt_at/decrypt_at framing): {w1:.1f} s of CPU work"}
     if not args.no_offload and world == 1:
         line["offload"] = offload_bench(args)
     print(json.dumps(line), flush=True)
@@ -451,6 +473,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=8, help="layers sealed+opened by the 1-core CPU baseline")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=2)
     ap.add_argument("--offload-reps", type=int, default=3)
