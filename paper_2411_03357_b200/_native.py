@@ -12,7 +12,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-SPGCM_PATH = os.path.join(LIB_DIR, "libspgcm.so")
+SPGCM_PATH = os.environ.get("SPGCM_LIB") or os.path.join(LIB_DIR, "libspgcm.so")  # env: A/B builds
 
 SP_OK, SP_EINVAL, SP_EAUTH, SP_ECUDA, SP_ENODEV = 0, 1, 2, 3, 4
 

@@ -216,6 +216,10 @@ __device__ __forceinline__ uint4 aes256_ctr(const uint32_t *rk, uint32_t lc, con
 // Element layout: little-endian 32-bit words of the 16-byte GCM string
 // (byte 0 holds coefficients x^0..x^7, MSB first).  Multiplying by x^8 moves
 // every byte one position up; byte 15 falls off and is folded back with R8.
+// (Measured alternative, r1: computing R8 with IMAD/IMAD.HI shifts on the FMA
+// pipe and moving the byte shifts there too removes 15 shared wavefronts per
+// row but lengthens every Horner step's dependency chain; it ran at 422 GB/s
+// vs 483 GB/s for the table version, so the table stays.)
 __device__ __forceinline__ uint4 gmul_g(uint4 y, uint32_t lcm, uint32_t lcr) {
     uint4 z = lds128_at<kSmGh>(__byte_perm(y.w, lcm, SP_SEL(3)));
 #pragma unroll
