@@ -448,6 +448,7 @@ void key_expand(const uint8_t key[32], uint32_t rk[60]) {
 constexpr int kPinSlots = 4;
 
 struct Workspace {
+    std::mutex mu;  // calls on one stream from several host threads serialise here
     MsgDev *d_msgs = nullptr;
     size_t cap_msgs = 0;
     uint32_t *d_acc = nullptr;
@@ -617,6 +618,7 @@ int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, bool open) {
     if (!d) return fail(SP_EINVAL, "null descriptors");
     SP_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
     Workspace *ws = workspace_for(ctx->device, s);
+    std::lock_guard<std::mutex> lk(ws->mu);
     KParams p;
     uint64_t rows = 0;
     int rc = stage_batch(ctx, d, n, s, ws, p, rows, open);
@@ -759,6 +761,7 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
                     "cudaMemcpyAsync(tag)");
     }
     Workspace *ws = workspace_for(ctx->device, hp->s_k);
+    std::lock_guard<std::mutex> wlk(ws->mu);
     KParams p;
     uint64_t rows_chk = 0;
     rc = stage_batch(ctx, dd.data(), n, hp->s_k, ws, p, rows_chk, open);
