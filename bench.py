@@ -265,9 +265,15 @@ def run_gpu(args) -> None:
     from paper_2411_03357_b200.gcm import GcmContext
 
     rank, world, local = dist_env()
+    if args.same_device:  # multi-rank flow check on a 1-GPU box (with --dist-backend gloo)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, args.dist_backend)
+    if args.dist_backend != "nccl":
+        dev_sync = None
+    else:
+        dev_sync = dev
     sizes = layer_sizes()
     total = sum(sizes)
     n = len(sizes)
@@ -298,7 +304,7 @@ def run_gpu(args) -> None:
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    barrier(dist, dev)
+    barrier(dist, dev_sync)
     torch.cuda.synchronize()
     launches0 = _native.launch_count()
     clk = ClockSampler(local).__enter__()
@@ -317,9 +323,9 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
         clk.mark(wall0, time.time())
     gpu_launches = _native.launch_count() - launches0
-    barrier(dist, dev)
+    barrier(dist, dev_sync)
     ms_local = t_start.elapsed_time(t_end) / K
-    ms = reduce_max(dist, ms_local, dev)
+    ms = reduce_max(dist, ms_local, dev_sync)
     seal_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     open_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     value = 2 * total / (ms / 1000.0) / 1e9 * world  # whole job
@@ -342,7 +348,7 @@ def run_gpu(args) -> None:
         e2e_step()
     assert torch.equal(h_back, h_plain)
     KE = max(1, min(K, 5))
-    barrier(dist, dev)
+    barrier(dist, dev_sync)
     t0 = time.perf_counter()
     w0 = time.time()
     for _ in range(KE):
@@ -350,8 +356,8 @@ def run_gpu(args) -> None:
     e2e_ms_local = (time.perf_counter() - t0) * 1000.0 / KE
     clk.mark(w0, time.time())
     clk.__exit__(None, None, None)
-    barrier(dist, dev)
-    e2e_ms = reduce_max(dist, e2e_ms_local, dev)
+    barrier(dist, dev_sync)
+    e2e_ms = reduce_max(dist, e2e_ms_local, dev_sync)
     e2e_value = 2 * total / (e2e_ms / 1000.0) / 1e9 * world
     h2d_bytes = 2 * total + 16 * n
     d2h_bytes = 2 * total + 16 * n + 4 * n
@@ -473,6 +479,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barrier/timing (nccl)")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (flow check on a 1-GPU box)")
     ap.add_argument("--cpu-reps", type=int, default=8, help="layers sealed+opened by the 1-core CPU baseline")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=2)
