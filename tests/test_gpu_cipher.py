@@ -254,3 +254,74 @@ def test_full_size_batch_round_trip(ctx_for, torch_cuda):
         p = _host(items[i][2])
         c, t = oracle_port.seal(key, 0, 1000 + i, p)
         assert _host(items[i][3]) == c and _host(tags[i]) == t
+
+
+def test_random_batches_fuzz(ctx_for, torch_cuda):
+    """Randomised batches: 1..40 messages, sizes from 1 B to 5 MiB (skewed
+    small), arbitrary byte offsets, random directions and counters, mixed in
+    one launch; every ciphertext/tag vs the reference arithmetic, every open
+    back to the plaintext with status 0."""
+    torch = torch_cuda
+    rng = random.Random(2024)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    for _ in range(25):
+        k = rng.randrange(1, 41)
+        sizes = [min(5 * MIB, int(rng.paretovariate(0.7) * rng.choice([1, 16, 200, 3000]))) or 1 for _ in range(k)]
+        offs = [rng.randrange(0, 64) for _ in range(k)]
+        total = sum(s + o for s, o in zip(sizes, offs)) + 64
+        src = torch.randint(0, 256, (total,), dtype=torch.uint8, device="cuda")
+        dst = torch.zeros_like(src)
+        back = torch.zeros_like(src)
+        tags = torch.zeros((k, 17), dtype=torch.uint8, device="cuda")
+        st = torch.full((k,), 9, dtype=torch.int32, device="cuda")
+        items, oitems, meta, pos = [], [], [], 0
+        for i, (n, o) in enumerate(zip(sizes, offs)):
+            d = rng.randrange(2)
+            iv = rng.choice([0, rng.randrange(1 << 64), (1 << 64) - 1])
+            a = pos + o
+            items.append((d, iv, src[a:a + n], dst[a:a + n], tags[i, 1:17]))
+            oitems.append((d, iv, dst[a:a + n], back[a:a + n], tags[i, 1:17]))
+            meta.append((d, iv, a, n))
+            pos = a + n
+        ctx.seal_batch(items)
+        ctx.open_batch(oitems, st)
+        torch.cuda.synchronize()
+        assert int(st.abs().sum()) == 0
+        h_src, h_dst, h_back = src.cpu().numpy(), dst.cpu().numpy(), back.cpu().numpy()
+        h_tags = tags.cpu().numpy()
+        for i, (d, iv, a, n) in enumerate(meta):
+            p = h_src[a:a + n].tobytes()
+            c, t = oracle_port.seal(key, d, iv, p)
+            assert h_dst[a:a + n].tobytes() == c, (n, a)
+            assert h_tags[i, 1:17].tobytes() == t
+            assert h_back[a:a + n].tobytes() == p
+
+
+def test_host_batch_pieces_split_messages(ctx_for, torch_cuda):
+    """Host pipeline: messages straddle the 1..32 MiB piece schedule, so runs
+    of one message finish in different launches (accumulator path)."""
+    rng = random.Random(77)
+    key = bytes(range(50, 82))
+    ctx = ctx_for(key)
+    import torch
+
+    sizes = [3 * MIB + 5, 32 * MIB, 1, 17 * MIB + 3, 700_001]
+    src = [torch.from_numpy(np.frombuffer(rng.randbytes(n), dtype=np.uint8).copy()).pin_memory() for n in sizes]
+    dst = [torch.empty_like(s).pin_memory() for s in src]
+    back = [torch.empty_like(s).pin_memory() for s in src]
+    tags = [torch.empty(16, dtype=torch.uint8).pin_memory() for _ in sizes]
+    ctx.seal_host_batch([(0, 900 + i, s, d, t) for i, (s, d, t) in enumerate(zip(src, dst, tags))])
+    for i, n in enumerate(sizes):
+        c, t = oracle_port.seal(key, 0, 900 + i, src[i].numpy().tobytes())
+        assert dst[i].numpy().tobytes() == c and tags[i].numpy().tobytes() == t
+    ctx.open_host_batch([(0, 900 + i, d, b, t) for i, (d, b, t) in enumerate(zip(dst, back, tags))])
+    for s, b in zip(src, back):
+        assert torch.equal(s, b)
+    # a tampered message fails the whole call and its output is scrubbed
+    from paper_2411_03357_b200.gcm import GcmAuthError
+
+    dst[3][5] ^= 1
+    with pytest.raises(GcmAuthError):
+        ctx.open_host_batch([(0, 900 + i, d, b, t) for i, (d, b, t) in enumerate(zip(dst, back, tags))])
+    assert int(back[3].sum()) == 0
