@@ -21,6 +21,7 @@ only) — the schedule the reference's simulator prices, usable without a GPU.
 from __future__ import annotations
 
 import hashlib
+import os
 from dataclasses import dataclass, field
 from typing import Any
 
@@ -28,6 +29,29 @@ from . import gcm as _gcm
 from .channel import DeviceCiphertext
 
 TAG = 16
+NVTX = os.environ.get("SPGCM_NVTX", "0") == "1"  # NVTX ranges per plane operation (nsys/ncu timelines)
+
+
+def _nvtx(name):
+    """Decorator: wrap a plane method in an NVTX range when SPGCM_NVTX=1."""
+    def deco(fn):
+        if not NVTX:
+            return fn
+
+        def wrapped(self, *a, **kw):
+            import torch
+
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(self, *a, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+
+        wrapped.__name__ = fn.__name__
+        wrapped.__doc__ = fn.__doc__
+        return wrapped
+
+    return deco
 
 
 def open_message_sync(key: bytes, direction: int, iv: int, msg: DeviceCiphertext):
@@ -106,6 +130,7 @@ class GpuPlane:
                 raise _gcm.GcmAuthError("authentication failed on the device")
 
     # -- seals ---------------------------------------------------------------------
+    @_nvtx("spgcm.seal_host_chunks")
     def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int,
                          speculative: bool = False) -> list:
         """H2D the plaintext of `block` [inner + off, +n) for each span and
@@ -154,6 +179,7 @@ class GpuPlane:
     def spec_batch(self) -> "SpecBatch":
         return SpecBatch(self)
 
+    @_nvtx("spgcm.seal_device_chunks")
     def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
         """Seal device plaintext `src` chunk-wise into fresh staging.  The
         launch is deferred and merged with the following swap-outs (up to
@@ -172,6 +198,7 @@ class GpuPlane:
         self._d2h_bytes += total
         return msgs
 
+    @_nvtx("spgcm.flush_d2h")
     def flush_d2h(self) -> None:
         """Issue the deferred swap-out work: one sealing launch (compute
         stream), one host-endpoint open launch for every pending landing
@@ -227,6 +254,7 @@ class GpuPlane:
             self._host_ready[block.id] = ev
         self.bytes_d2h += total
 
+    @_nvtx("spgcm.seal_small")
     def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
         """Seal small host payloads (NOP pads, token I/O) in one launch."""
         torch = self.torch
@@ -249,6 +277,7 @@ class GpuPlane:
         return msgs
 
     # -- opens ---------------------------------------------------------------------
+    @_nvtx("spgcm.open_into")
     def open_into(self, jobs: list, direction: int) -> None:
         """jobs: (msg, iv, dst view or None).  One launch; NOPs open into
         scratch so their tags are still verified."""

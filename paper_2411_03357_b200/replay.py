@@ -40,6 +40,7 @@ class ReplayConfig:
     # the pinned blocks (benchmarks: AES-CTR cost is data-independent, and
     # seeding 4 GB at CPU speed would dominate setup time)
     fill: str = "seeded"
+    reference_compat: bool = True
 
 
 @dataclass
@@ -67,7 +68,7 @@ def build_engine(trace: Trace, config: ReplayConfig):
     engine = Engine(memory, cpu, gpu, predictor, EngineConfig(
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
-        record_stream=config.record_stream, plane=config.plane))
+        record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat))
     blocks = {}
     for spec in header.blocks:
         if spec.resident == "cpu":
