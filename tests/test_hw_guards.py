@@ -1,0 +1,87 @@
+"""Hardware write guards (libspguard): a store that bypasses
+HostMemory.write into a speculatively encrypted range must invalidate the
+record, so the stale ciphertext is never committed.  Run in a subprocess:
+the check installs a SIGSEGV handler."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import textwrap
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = textwrap.dedent('''
+    import sys
+    sys.path.insert(0, %r)
+    from paper_2411_03357_b200 import guards
+    from paper_2411_03357_b200.channel import new_channel
+    from paper_2411_03357_b200.engine import CopyRequest, Engine, EngineConfig
+    from paper_2411_03357_b200.memory import HostMemory, ModelLayer, prng_fill
+    from paper_2411_03357_b200.predictor import Prediction, TransferClass
+    from paper_2411_03357_b200.validator import RecordState
+    from tests.test_engine_scenarios import ScriptedPredictor
+
+    mem = HostMemory(pinned=False, hw_guards=True)
+    cpu, gpu = new_channel(seed=1)
+    b = mem.alloc(ModelLayer(1), 256 * 1024, prng_fill(3))
+    c = mem.alloc(ModelLayer(2), 256 * 1024, prng_fill(4))
+    eng = Engine(mem, cpu, gpu, ScriptedPredictor([[Prediction(b.id, 0, 0), Prediction(c.id, 1, 0)]], {b.id, c.id}),
+                 EngineConfig(leeway=0, plane="dry"))
+    eng.speculate_tick()
+    eng._complete_spec_tasks()
+    assert guards.active() == 2, guards.active()
+    rec_b = next(r for r in eng.validator.records.values() if r.block_id == b.id)
+    # 1) a direct store (numpy, no HostMemory.write) into b's guarded pages
+    b.data[100000] ^= 0xFF
+    assert guards.faults() == 1
+    # 2) the next engine entry turns it into an invalidation
+    h = eng.copy_h2d(CopyRequest("h2d", b.base, b.len, TransferClass.MODEL_WEIGHTS, block_id=b.id))
+    assert rec_b.state is RecordState.INVALIDATED, rec_b.state
+    assert h.verdict.value == "stale", h.verdict          # sent on the fly with the new bytes
+    assert eng.report()["write_faults"] == 1
+    # c is untouched: still a HIT
+    h2 = eng.copy_h2d(CopyRequest("h2d", c.base, c.len, TransferClass.MODEL_WEIGHTS, block_id=c.id))
+    assert h2.verdict.value == "hit", h2.verdict
+    # 3) released guards leave the pages writable; API writes never trap
+    c.data[7] = 1
+    mem.write(b.id, 0, b"xyz")
+    assert guards.active() == 0
+    eng.finish()
+    print("hw guards ok", guards.faults())
+''' % ROOT)
+
+
+def test_hw_guard_invalidates_on_direct_store():
+    out = subprocess.run([sys.executable, "-c", SCRIPT], capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "hw guards ok 1" in out.stdout
+
+
+def test_hw_guard_library_exports():
+    import re
+
+    from paper_2411_03357_b200 import guards
+
+    text = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "spguard.h")).read(), flags=re.S)
+    names = set(re.findall(r"\b(spg_[a-z_]+)\s*\(", text))
+    assert names == set(guards.SYMBOLS)
+    lib = guards.lib()
+    for n in names:
+        assert hasattr(lib, n)
+
+
+GPU_SCRIPT = SCRIPT.replace("HostMemory(pinned=False, hw_guards=True)", "HostMemory(pinned=True, hw_guards=True)") \
+                   .replace('plane="dry"', 'plane="gpu"')
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_hw_guard_on_pinned_memory_gpu():
+    """Same check on page-locked (cudaHostAlloc) blocks with the B200 plane:
+    mprotect works on pinned pages and DMA is unaffected."""
+    out = subprocess.run([sys.executable, "-c", GPU_SCRIPT], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "hw guards ok 1" in out.stdout
