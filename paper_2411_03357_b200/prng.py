@@ -17,6 +17,7 @@ from typing import Callable
 import numpy as np
 
 _CHUNK_WORDS = 1 << 22
+_SMALL = 64 * 1024  # below this, Random(seed).randbytes is faster than numpy setup
 
 
 def _bitgen_for(seed) -> np.random.MT19937:
@@ -35,6 +36,10 @@ def random_bytes(seed, n: int, out: np.ndarray | None = None) -> np.ndarray:
         raise ValueError("negative length")
     res = out if out is not None else np.empty(n, dtype=np.uint8)
     if n == 0:
+        return res
+    if n <= _SMALL:
+        # CPython's own generator is cheaper than injecting a numpy state
+        res[:] = np.frombuffer(random.Random(seed).randbytes(n), dtype=np.uint8)
         return res
     bg = _bitgen_for(seed)
     full, rem = divmod(n, 4)
