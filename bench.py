@@ -377,6 +377,10 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
     pcie_ms = (time.perf_counter() - t0) * 1000.0 / KE
 
+    offload = None
+    if not args.no_offload:
+        offload = offload_bench(args, dist, dev_sync, rank, world)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -429,19 +433,20 @@ def run_gpu(args) -> None:
                                 "sample": f"the OPT-13B layer ({len(sizes_all)} messages) sealed+opened "
                                           f"{args.cpu_reps}x on 1 core via oracle/port.py (cryptography AESGCM "
                                           f"with encrypt_at/decrypt_at framing): {w1:.1f} s of CPU work"}
-    if not args.no_offload and world == 1:
-        line["offload"] = offload_bench(args)
+    if offload is not None:
+        line["offload"] = offload
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def offload_bench(args) -> dict:
+def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
     """OPT-66B-shaped FlexGen weight offload (2 offloaded layers, 61 x 32 MiB
     blocks each) through the B200 engine vs the same swaps as plain copies —
-    the north star's 'within 10% of unencrypted swap throughput'.  Runs
-    alternate plain / encrypted; best of `reps` each (host-side variance of
-    pinned-memory copies is large on a shared box)."""
+    the north star's 'within 10% of unencrypted swap throughput'.  Every rank
+    replays its own trace on its own channel (seed = rank); a run's time is
+    the max over ranks, its bytes the sum.  Runs alternate plain / encrypted;
+    best of `reps` each (pinned-memory copy variance on a shared host)."""
     import torch
 
     from paper_2411_03357_b200 import workload
@@ -450,24 +455,33 @@ def offload_bench(args) -> dict:
     # one warm-up iteration (first touch of every block, allocator growth),
     # then `offload_iters` timed iterations
     iters = args.offload_iters + 1
-    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=iters)
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=iters, seed=rank)
     start = len(tr.events) // iters
-    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast")
+    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank)
+
+    def timed(fn):
+        barrier(dist, dev_sync)
+        r = fn()
+        wall = reduce_max(dist, r.wall_s, dev_sync)
+        return r, world * r.swap_bytes / wall / 1e9
+
     plain, enc, rep = [], [], None
     for _ in range(args.offload_reps):
-        plain.append(run_plain(tr, fill="fast", measure_from=start).swap_gbs)
-        r = run_engine(tr, cfg, measure_from=start)
-        enc.append(r.swap_gbs)
+        _, g = timed(lambda: run_plain(tr, fill="fast", measure_from=start))
+        plain.append(g)
+        r, g = timed(lambda: run_engine(tr, cfg, measure_from=start))
+        enc.append(g)
         rep = r.engine.report()
         del r
         torch.cuda.empty_cache()
-    return {"model": "opt-66b", "layers_offloaded": 2, "iterations": args.offload_iters,
-            "layer_bytes": workload.opt_layer_bytes("opt-66b"), "swap_bytes_timed": tr.swap_bytes() * args.offload_iters // iters,
-            "warmup_iterations": 1,
-            "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
+    return {"model": "opt-66b", "layers_offloaded_per_gpu": 2, "iterations": args.offload_iters,
+            "layer_bytes": workload.opt_layer_bytes("opt-66b"),
+            "swap_bytes_timed_per_gpu": tr.swap_bytes() * args.offload_iters // iters, "warmup_iterations": 1,
+            "n_gpus": world, "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
             "encrypted_runs": [round(x, 2) for x in enc], "plain_runs": [round(x, 2) for x in plain],
             "throughput_ratio": round(max(enc) / max(plain), 4),
-            "note": "tokens/s ratio == swap throughput ratio (same trace, same batch); random payload",
+            "note": "whole-job swap GB/s (sum over ranks / max time); tokens/s ratio == swap throughput ratio "
+                    "(same trace, same batch); random payload",
             "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "nops": rep["nops"],
             "sequence_hit_rate": rep["sequence_hit_rate"]}
 
