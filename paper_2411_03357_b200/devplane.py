@@ -67,18 +67,21 @@ def open_message_sync(key: bytes, direction: int, iv: int, msg: DeviceCiphertext
     return out
 
 
-@dataclass
-class _Pending:
-    """A sealed chunk whose device payload is the wire message."""
-
-    msg: DeviceCiphertext
-    iv: int
-
-
 class GpuPlane:
-    """Streams, staging and batched launches for one engine on one GPU."""
+    """Streams, staging and batched launches for one engine on one GPU.
+
+    Compute-stream work (on-the-fly and token/NOP seals, swap-out seals, every
+    open) is queued in issue order and flushed as one launch per run of
+    same-kind operations: at `flush()` (the engine calls it at the end of
+    every sync), before any host access, or when BATCH_BYTES of payload is
+    pending.  Small host payloads (tokens, NOP pads) are staged in a byte
+    arena that crosses PCIe in one copy per flush.  Speculative seals run on
+    their own stream as soon as their H2D copy lands (SpecBatch); host
+    landings of swap-outs run on the landing / D2H streams after the flush
+    that seals them."""
 
     kind = "gpu"
+    ARENA_BYTES = 1 << 20
 
     def __init__(self, key: bytes, device: int | None = None) -> None:
         import torch
@@ -94,10 +97,14 @@ class GpuPlane:
             self.s_land = torch.cuda.Stream(self.device)
         self._host_ready: dict[int, Any] = {}  # block id -> event after last D2H into it
         self._h2d_done: dict[int, Any] = {}    # block id -> event after last H2D from it
-        self._d2h_seals: list = []      # deferred swap-out seal descriptors
-        self._d2h_ready = torch.cuda.Event()
-        self._landings: list = []       # deferred host-endpoint opens + D2H copies
-        self._d2h_bytes = 0
+        self._ops: list = []                   # ("wait", ev) | ("seal", item) | ("open", item)
+        self._ops_bytes = 0
+        self._window = torch.cuda.Event()      # recorded after the flush of the current window
+        self._arena_host = bytearray()
+        self._arena_dev = None
+        self._arena_off = 0
+        self._landings: list = []              # (block, jobs, direction) for the next flush
+        self._landing_blocks: set = set()
         self._status = torch.zeros(1 << 16, dtype=torch.int32, device=self.device)
         self._status_used = 0
         self.bytes_h2d = 0
@@ -116,9 +123,34 @@ class GpuPlane:
         self._status_used += n
         return s
 
+    def _queue(self, kind: str, item, nbytes: int = 0) -> None:
+        self._ops.append((kind, item))
+        self._ops_bytes += nbytes
+        if self._ops_bytes >= BATCH_BYTES:
+            self.flush()
+
+    def _wait_for(self, ev) -> None:
+        """Order the compute queue after `ev` unless it belongs to the
+        current window (queue order already covers that)."""
+        if ev is not None and ev is not self._window:
+            self._ops.append(("wait", ev))
+
+    def _arena_views(self, n: int):
+        """Payload + tag views of n bytes in the current small-payload arena."""
+        need = ((n + 15) & ~15) + TAG
+        if self._arena_dev is None or self._arena_off + need > self._arena_dev.numel():
+            if self._arena_off:
+                self.flush()
+            self._arena_dev = self._empty(max(self.ARENA_BYTES, need))
+            self._arena_off = 0
+            self._arena_host = bytearray()
+        o = self._arena_off
+        self._arena_off += need
+        return self._arena_dev[o:o + n], self._arena_dev[o + need - TAG:o + need], o
+
     def check_auth(self) -> None:
         """Raise GcmAuthError if any open since the last check failed."""
-        self.flush_d2h()
+        self.flush()
         if self._status_used:
             self.s_comp.synchronize()
             self.s_land.synchronize()
@@ -129,92 +161,49 @@ class GpuPlane:
             if bad:
                 raise _gcm.GcmAuthError("authentication failed on the device")
 
-    # -- seals ---------------------------------------------------------------------
-    @_nvtx("spgcm.seal_host_chunks")
-    def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int,
-                         speculative: bool = False) -> list:
-        """H2D the plaintext of `block` [inner + off, +n) for each span and
-        seal chunk i at iv0 + i in place (one copy + one launch).
-
-        Speculative (encrypt-ahead) seals run on their own stream and carry a
-        `ready` event that the committing open waits on; on-the-fly seals run
-        on the compute stream in issue order."""
+    # -- flush ---------------------------------------------------------------------
+    @_nvtx("spgcm.flush")
+    def flush(self) -> None:
         torch = self.torch
-        self.flush_d2h()
-        total = sum(n for _, n in spans)
-        first = spans[0][0]
-        ev = self._host_ready.get(block.id)
-        if ev is not None:
-            self.s_h2d.wait_event(ev)
-        src = torch.from_numpy(block.data[inner + first: inner + first + total])
-        s_seal = self.s_spec if speculative else self.s_comp
-        with torch.cuda.stream(self.s_h2d):
-            # staging is allocated on the stream that first writes it (the
-            # copy engine) and marked as used by every stream that reads it,
-            # so the caching allocator never hands it out early
-            buf = torch.empty(total + TAG * len(spans), dtype=torch.uint8, device=self.device)
-            buf[:total].copy_(src if block.pinned is not None else src.pin_memory(), non_blocking=True)
-            buf.record_stream(self.s_comp)
-            if speculative:
-                buf.record_stream(self.s_spec)
-            done = torch.cuda.Event()
-            done.record(self.s_h2d)
-        self._h2d_done[block.id] = done
-        self.bytes_h2d += total
-        s_seal.wait_event(done)
-        items, views = [], []
-        for i, (off, n) in enumerate(spans):
-            view = buf[off - first: off - first + n]
-            tag = buf[total + TAG * i: total + TAG * (i + 1)]
-            items.append((direction, iv0 + i, view, view, tag, n))
-            views.append((view, tag, n))
-        self.ctx.seal_batch(items, s_seal)
-        self.launches += 1
-        ready = None
-        if speculative:
-            ready = torch.cuda.Event()
-            ready.record(self.s_spec)
-        return [DeviceCiphertext(v, t, n, ready=ready) for v, t, n in views]
+        if self._arena_host:
+            staged = torch.empty(len(self._arena_host), dtype=torch.uint8, pin_memory=True)
+            staged.numpy()[:] = memoryview(self._arena_host).cast("B")
+            with torch.cuda.stream(self.s_comp):
+                self._arena_dev[:len(self._arena_host)].copy_(staged, non_blocking=True)
+            # later payloads of this arena must start past the staged bytes
+            self._arena_host = bytearray()
+            self._arena_dev = None
+            self._arena_off = 0
+        if self._ops:
+            ops, self._ops, self._ops_bytes = self._ops, [], 0
+            i = 0
+            while i < len(ops):
+                kind = ops[i][0]
+                if kind == "wait":
+                    self.s_comp.wait_event(ops[i][1])
+                    i += 1
+                    continue
+                j = i
+                while j < len(ops) and ops[j][0] == kind:
+                    j += 1
+                items = [op[1] for op in ops[i:j]]
+                if kind == "seal":
+                    self.ctx.seal_batch(items, self.s_comp)
+                else:
+                    self.ctx.open_batch(items, self._status_slots(len(items)), self.s_comp)
+                self.launches += 1
+                i = j
+            self._window.record(self.s_comp)
+            self._window = torch.cuda.Event()
+        if self._landings:
+            self._flush_landings()
 
-    def spec_batch(self) -> "SpecBatch":
-        return SpecBatch(self)
+    flush_d2h = flush  # historical name (SpecBatch, engine)
 
-    @_nvtx("spgcm.seal_device_chunks")
-    def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
-        """Seal device plaintext `src` chunk-wise into fresh staging.  The
-        launch is deferred and merged with the following swap-outs (up to
-        BATCH_BYTES, or until any other device work needs ordering): one
-        sealing launch for a whole KV eviction instead of one per block."""
-        total = sum(n for _, n in spans)
-        first = spans[0][0]
-        buf = self._empty(total + TAG * len(spans))
-        buf.record_stream(self.s_land)
-        msgs = []
-        for i, (off, n) in enumerate(spans):
-            view = buf[off - first: off - first + n]
-            tag = buf[total + TAG * i: total + TAG * (i + 1)]
-            self._d2h_seals.append((direction, iv0 + i, src[off:off + n], view, tag, n))
-            msgs.append(DeviceCiphertext(view, tag, n, ready=self._d2h_ready))
-        self._d2h_bytes += total
-        return msgs
-
-    @_nvtx("spgcm.flush_d2h")
-    def flush_d2h(self) -> None:
-        """Issue the deferred swap-out work: one sealing launch (compute
-        stream), one host-endpoint open launch for every pending landing
-        (landing stream), then the D2H copies per block (copy stream)."""
+    def _flush_landings(self) -> None:
         torch = self.torch
-        if self._d2h_seals:
-            self.ctx.seal_batch(self._d2h_seals, self.s_comp)
-            self.launches += 1
-            self._d2h_ready.record(self.s_comp)
-            self._d2h_seals = []
-            self._d2h_ready = torch.cuda.Event()
-        if not self._landings:
-            self._d2h_bytes = 0
-            return
         landings, self._landings = self._landings, []
-        self._d2h_bytes = 0
+        self._landing_blocks = set()
         waited = set()
         total = 0
         for _, jobs, _ in landings:
@@ -254,61 +243,111 @@ class GpuPlane:
             self._host_ready[block.id] = ev
         self.bytes_d2h += total
 
+    def _before_host_read_of(self, block_id: int) -> None:
+        if block_id in self._landing_blocks:
+            self.flush()
+
+    # -- seals ---------------------------------------------------------------------
+    @_nvtx("spgcm.seal_host_chunks")
+    def seal_host_chunks(self, block, inner: int, spans: list, direction: int, iv0: int,
+                         speculative: bool = False) -> list:
+        """H2D the plaintext of `block` [inner + off, +n) for each span (copy
+        stream, now) and seal chunk i at iv0 + i in place.  Speculative seals
+        launch on their own stream (SpecBatch); on-the-fly seals join the
+        compute queue behind the copy's event."""
+        if speculative:
+            batch = SpecBatch(self)
+            msgs = batch.add(block, inner, spans, direction, iv0)
+            batch.launch()
+            return msgs
+        torch = self.torch
+        self._before_host_read_of(block.id)
+        total = sum(n for _, n in spans)
+        first = spans[0][0]
+        ev = self._host_ready.get(block.id)
+        if ev is not None:
+            self.s_h2d.wait_event(ev)
+        src = torch.from_numpy(block.data[inner + first: inner + first + total])
+        with torch.cuda.stream(self.s_h2d):
+            buf = torch.empty(total + TAG * len(spans), dtype=torch.uint8, device=self.device)
+            buf[:total].copy_(src if block.pinned is not None else src.pin_memory(), non_blocking=True)
+            buf.record_stream(self.s_comp)
+            buf.record_stream(self.s_land)
+            done = torch.cuda.Event()
+            done.record(self.s_h2d)
+        self._h2d_done[block.id] = done
+        self.bytes_h2d += total
+        self._ops.append(("wait", done))
+        msgs = []
+        for i, (off, n) in enumerate(spans):
+            view = buf[off - first: off - first + n]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            self._queue("seal", (direction, iv0 + i, view, view, tag, n), n)
+            msgs.append(DeviceCiphertext(view, tag, n, ready=self._window))
+        return msgs
+
+    def spec_batch(self) -> "SpecBatch":
+        return SpecBatch(self)
+
+    @_nvtx("spgcm.seal_device_chunks")
+    def seal_device_chunks(self, src, spans: list, direction: int, iv0: int) -> list:
+        """Seal device plaintext `src` chunk-wise into fresh staging (queued:
+        one sealing launch covers a whole KV eviction)."""
+        total = sum(n for _, n in spans)
+        first = spans[0][0]
+        buf = self._empty(total + TAG * len(spans))
+        buf.record_stream(self.s_land)
+        msgs = []
+        for i, (off, n) in enumerate(spans):
+            view = buf[off - first: off - first + n]
+            tag = buf[total + TAG * i: total + TAG * (i + 1)]
+            msgs.append(DeviceCiphertext(view, tag, n, ready=self._window))
+            self._queue("seal", (direction, iv0 + i, src[off:off + n], view, tag, n), n)
+        return msgs
+
     @_nvtx("spgcm.seal_small")
     def seal_bytes_device(self, payloads: list, direction: int, iv0: int, nop: bool = False) -> list:
-        """Seal small host payloads (NOP pads, token I/O) in one launch."""
-        torch = self.torch
-        self.flush_d2h()
-        total = sum(len(p) for p in payloads)
-        staged = torch.empty(total, dtype=torch.uint8, pin_memory=True)
-        staged.numpy()[:] = memoryview(b"".join(payloads)).cast("B")
-        buf = self._empty(total + TAG * len(payloads))
-        with torch.cuda.stream(self.s_comp):
-            buf[:total].copy_(staged, non_blocking=True)
-        items, msgs, off = [], [], 0
+        """Seal small host payloads (NOP pads, token I/O): staged in the byte
+        arena, sealed by the next flush's launch."""
+        msgs = []
         for i, p in enumerate(payloads):
-            view = buf[off:off + len(p)]
-            tag = buf[total + TAG * i: total + TAG * (i + 1)]
-            items.append((direction, iv0 + i, view, view, tag, len(p)))
-            msgs.append(DeviceCiphertext(view, tag, len(p), nop=nop))
-            off += len(p)
-        self.ctx.seal_batch(items, self.s_comp)
-        self.launches += 1
+            n = len(p)
+            view, tag, o = self._arena_views(n)
+            host = self._arena_host
+            if len(host) < o:
+                host.extend(bytes(o - len(host)))
+            host[o:o + n] = p
+            msg = DeviceCiphertext(view, tag, n, nop=nop, ready=self._window)
+            self._queue("seal", (direction, iv0 + i, view, view, tag, n), n)
+            msgs.append(msg)
         return msgs
 
     # -- opens ---------------------------------------------------------------------
     @_nvtx("spgcm.open_into")
     def open_into(self, jobs: list, direction: int) -> None:
-        """jobs: (msg, iv, dst view or None).  One launch; NOPs open into
+        """jobs: (msg, iv, dst view or None), queued in order; NOPs open into
         scratch so their tags are still verified."""
-        if not jobs:
-            return
-        self.flush_d2h()  # a pending swap-out seal may read a buffer this open writes
-        items = []
-        waited = set()
         for msg, iv, dst in jobs:
-            if msg.ready is not None and id(msg.ready) not in waited:
-                self.s_comp.wait_event(msg.ready)
-                waited.add(id(msg.ready))
+            self._wait_for(msg.ready)
             if dst is None:
                 dst = self._empty(msg.declared_len)
-            items.append((direction, iv, msg.payload, dst, msg.auth_tag, msg.declared_len))
-        self.ctx.open_batch(items, self._status_slots(len(items)), self.s_comp)
-        self.launches += 1
+            self._queue("open", (direction, iv, msg.payload, dst, msg.auth_tag, msg.declared_len), msg.declared_len)
 
     def land_on_host(self, block, jobs: list, direction: int) -> None:
         """Host endpoint open of D2H messages, then the plaintext lands in
-        `block` (jobs: (msg, iv, offset_in_block)).  Deferred and batched with
-        the swap-out seals (see flush_d2h); the landing's open and copy never
-        wait on the compute stream's commits, so landings overlap swap-ins."""
+        `block` (jobs: (msg, iv, offset_in_block)).  Issued by the next flush
+        (after the seals it depends on), on the landing / D2H streams, so
+        landings overlap swap-ins and never wait on the compute stream's
+        later commits."""
         self._landings.append((block, jobs, direction))
-        self._d2h_bytes += sum(m.declared_len for m, _, _ in jobs)
-        if self._d2h_bytes >= BATCH_BYTES:
-            self.flush_d2h()
+        self._landing_blocks.add(block.id)
+        self._ops_bytes += sum(m.declared_len for m, _, _ in jobs)
+        if self._ops_bytes >= BATCH_BYTES:
+            self.flush()
 
     def host_sync(self, block_id: int | None = None) -> None:
         """Wait until D2H landings are visible to the host."""
-        self.flush_d2h()
+        self.flush()
         if block_id is None:
             self.s_d2h.synchronize()
             return
@@ -319,7 +358,7 @@ class GpuPlane:
     def before_host_write(self, block_id: int) -> None:
         """The host is about to mutate `block_id`: in-flight copies that
         read or write it must be finished first."""
-        self.flush_d2h()
+        self.flush()
         for table in (self._h2d_done, self._host_ready):
             ev = table.get(block_id)
             if ev is not None:
@@ -334,17 +373,18 @@ class GpuPlane:
             return t.to(self.device, non_blocking=False)
 
     def to_host_bytes(self, view) -> bytes:
+        self.flush()
         self.s_comp.synchronize()
         return view.cpu().numpy().tobytes()
 
     def digests(self, views: list) -> list:
-        self.flush_d2h()
+        self.flush()
         self.s_comp.synchronize()
         self.s_land.synchronize()
         return [hashlib.sha256(v.cpu().numpy().tobytes()).hexdigest() for v in views]
 
     def finish(self) -> None:
-        self.flush_d2h()
+        self.flush()
         self.s_comp.synchronize()
         self.s_spec.synchronize()
         self.s_land.synchronize()
@@ -372,7 +412,7 @@ class SpecBatch:
 
     def add(self, block, inner: int, spans: list, direction: int, iv0: int) -> list:
         p, torch = self.plane, self.plane.torch
-        p.flush_d2h()  # pending landings into this host block must be recorded first
+        p._before_host_read_of(block.id)  # a pending landing into this block must be issued first
         total = sum(n for _, n in spans)
         first = spans[0][0]
         ev = p._host_ready.get(block.id)
@@ -455,8 +495,10 @@ class DryPlane:
     def spec_batch(self):
         return _DrySpecBatch(self)
 
-    def flush_d2h(self):
+    def flush(self):
         pass
+
+    flush_d2h = flush
 
     def seal_device_chunks(self, src, spans, direction, iv0):
         return self._msgs([n for _, n in spans])
