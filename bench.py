@@ -498,7 +498,7 @@ def main() -> None:
     ap.add_argument("--cpu-reps", type=int, default=8, help="layers sealed+opened by the 1-core CPU baseline")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=2)
-    ap.add_argument("--offload-reps", type=int, default=3)
+    ap.add_argument("--offload-reps", type=int, default=4)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

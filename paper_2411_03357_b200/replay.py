@@ -223,7 +223,8 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
                 (b.pinned if b.pinned is not None else torch.from_numpy(b.data)).copy_(d, non_blocking=True)
                 d.record_stream(s_d2h)
         elif isinstance(ev, SyncEvent):
-            s_h2d.synchronize()
+            # like the engine, the batch boundary orders the device side only
+            # (later swap-outs wait on the swap-in stream); the host runs on
             pending_in.clear()
         elif isinstance(ev, SmallIoEvent):
             payload = torch.frombuffer(bytearray(ev.size), dtype=torch.uint8)
