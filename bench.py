@@ -467,11 +467,14 @@ def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1)
         wall = reduce_max(dist, r.wall_s, dev_sync)
         return r, world * r.swap_bytes / wall / 1e9
 
+    from paper_2411_03357_b200.replay import prepare_memory
+
+    memory = prepare_memory(tr, cfg)  # one set of pinned host blocks for every run
     plain, enc, rep = [], [], None
     for _ in range(args.offload_reps):
-        _, g = timed(lambda: run_plain(tr, fill="fast", measure_from=start))
+        _, g = timed(lambda: run_plain(tr, fill="fast", measure_from=start, memory=memory))
         plain.append(g)
-        r, g = timed(lambda: run_engine(tr, cfg, measure_from=start))
+        r, g = timed(lambda: run_engine(tr, cfg, measure_from=start, memory=memory))
         enc.append(g)
         rep = r.engine.report()
         del r

@@ -56,10 +56,27 @@ class ReplayResult:
         return self.swap_bytes / self.wall_s / 1e9 if self.wall_s > 0 else 0.0
 
 
-def build_engine(trace: Trace, config: ReplayConfig):
-    """Engine + block table exactly as simulator.py:253-284 builds them."""
-    header = trace.header
+def prepare_memory(trace: Trace, config: ReplayConfig) -> HostMemory:
+    """Host blocks of `trace` (ids = header order), allocated and filled once;
+    reusable by several replays (see HostMemory.reset_runtime_state)."""
     memory = HostMemory()
+    for spec in trace.header.blocks:
+        if spec.resident == "cpu":
+            memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, config))
+        else:
+            memory.alloc(spec.kind, spec.nbytes)
+    return memory
+
+
+def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None = None):
+    """Engine + block table exactly as simulator.py:253-284 builds them
+    (optionally over pre-built host blocks from `prepare_memory`)."""
+    header = trace.header
+    reuse = memory is not None
+    if reuse:
+        memory.reset_runtime_state()
+    else:
+        memory = HostMemory()
     cpu, gpu = new_channel(seed=config.seed)
     pconf = PredictorConfig() if config.predictor_chunk_bytes is None else \
         PredictorConfig(chunk_bytes=config.predictor_chunk_bytes)
@@ -72,11 +89,11 @@ def build_engine(trace: Trace, config: ReplayConfig):
     blocks = {}
     for spec in header.blocks:
         if spec.resident == "cpu":
-            block = memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, config))
+            block = memory.block(spec.id) if reuse else memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, config))
             if isinstance(spec.kind, (ModelLayer, KvCache)):
                 predictor.observe_swap_out(block.id)
         else:
-            block = memory.alloc(spec.kind, spec.nbytes)
+            block = memory.block(spec.id) if reuse else memory.alloc(spec.kind, spec.nbytes)
             if config.plane == "gpu":
                 dev = engine.plane.new_device_buffer(spec.nbytes)
                 if config.fill == "fast":
@@ -129,13 +146,13 @@ def _swap_bytes_from(trace: Trace, start: int) -> int:
 
 
 def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool = False,
-               measure_from: int = 0) -> ReplayResult:
+               measure_from: int = 0, memory: HostMemory | None = None) -> ReplayResult:
     """Replay `trace`; with `catch`, an engine exception (e.g. the reference's
     defect C2 EngineError) is returned in `error` with the engine state at
     the point of failure, as the parity harness needs.  With `measure_from`,
     the clock starts (after draining the GPU) at that event index and
     `swap_bytes` counts only the swaps from there on (warm-up excluded)."""
-    engine, blocks = build_engine(trace, config)
+    engine, blocks = build_engine(trace, config, memory)
     if config.plane == "gpu":
         engine.plane.finish()
     mark = {"t0": time.perf_counter()}
@@ -181,20 +198,22 @@ def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConf
     engine.finish()
 
 
-def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: int = 0) -> ReplayResult:
+def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: int = 0,
+              memory: HostMemory | None = None) -> ReplayResult:
     """NoCc on the GPU: the same swaps as plain pinned copies, no crypto."""
     import torch
 
-    memory = HostMemory()
+    cfg = ReplayConfig(fill=fill)
+    if memory is None:
+        memory = prepare_memory(trace, cfg)
+    else:
+        memory.reset_runtime_state()
     dev = torch.device("cuda", torch.cuda.current_device())
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
     blocks, device_mem = {}, {}
-    cfg = ReplayConfig(fill=fill)
     for spec in trace.header.blocks:
-        if spec.resident == "cpu":
-            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes, _fill_for(spec, cfg))
-        else:
-            blocks[spec.id] = memory.alloc(spec.kind, spec.nbytes)
+        blocks[spec.id] = memory.block(spec.id)
+        if spec.resident != "cpu":
             d = torch.empty(spec.nbytes, dtype=torch.uint8, device=dev)
             if fill == "fast":
                 _fast_random(d, spec.content_seed)
