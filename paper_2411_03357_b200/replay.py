@@ -209,7 +209,9 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
     else:
         memory.reset_runtime_state()
     dev = torch.device("cuda", torch.cuda.current_device())
-    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    from .devplane import device_streams
+
+    s_h2d, s_d2h = device_streams(dev, 2)
     blocks, device_mem = {}, {}
     for spec in trace.header.blocks:
         blocks[spec.id] = memory.block(spec.id)
@@ -222,6 +224,7 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
             device_mem[spec.id] = d
     torch.cuda.synchronize()
     pending_in: list = []
+    host_ready: dict = {}
     t0 = time.perf_counter()
     for k, ev in enumerate(trace.events):
         if k == measure_from and k:
@@ -229,6 +232,9 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
             t0 = time.perf_counter()
         if isinstance(ev, SwapInRequest):
             b = blocks[ev.block]
+            landed = host_ready.pop(ev.block, None)
+            if landed is not None:  # the block's last swap-out must land before it is read again
+                s_h2d.wait_event(landed)
             with torch.cuda.stream(s_h2d):
                 d = torch.empty(b.len, dtype=torch.uint8, device=dev)
                 d.copy_(b.pinned if b.pinned is not None else torch.from_numpy(b.data), non_blocking=True)
@@ -241,6 +247,8 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
             with torch.cuda.stream(s_d2h):
                 (b.pinned if b.pinned is not None else torch.from_numpy(b.data)).copy_(d, non_blocking=True)
                 d.record_stream(s_d2h)
+                host_ready[ev.block] = torch.cuda.Event()
+                host_ready[ev.block].record(s_d2h)
         elif isinstance(ev, SyncEvent):
             # like the engine, the batch boundary orders the device side only
             # (later swap-outs wait on the swap-in stream); the host runs on
