@@ -13,6 +13,7 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
 SPGCM_PATH = os.environ.get("SPGCM_LIB") or os.path.join(LIB_DIR, "libspgcm.so")  # env: A/B builds
+SPPIPE_PATH = os.path.join(LIB_DIR, "libsppipe.so")
 
 SP_OK, SP_EINVAL, SP_EAUTH, SP_ECUDA, SP_ENODEV = 0, 1, 2, 3, 4
 
@@ -84,3 +85,149 @@ def last_error() -> str:
 
 def launch_count() -> int:
     return int(load_spgcm().sp_launch_count())
+
+
+# ---- libsppipe (include/sppipe.h) ------------------------------------------------------
+SP_EENGINE, SP_EOVERLAP, SP_ESTATE, SP_EUNKNOWN_BLOCK, SP_EBOUNDS, SP_EGUARD, SP_EAMBIGUOUS, SP_EIVREUSE, \
+    SP_EKEY = range(10, 19)
+
+SPPIPE_SYMBOLS = (
+    "sp_pred_create", "sp_pred_destroy", "sp_pred_classify", "sp_pred_observe_out", "sp_pred_observe_in",
+    "sp_pred_observe_sync", "sp_pred_recognize", "sp_pred_cycle_entry", "sp_pred_predict_batches",
+    "sp_pred_outstanding", "sp_pred_in_batch_count", "sp_pred_decision_count", "sp_pred_decision",
+    "sp_pipe_create", "sp_pipe_destroy", "sp_pipe_register_block", "sp_pipe_seed_device", "sp_pipe_submit_h2d",
+    "sp_pipe_submit_d2h", "sp_pipe_small_io", "sp_pipe_sync", "sp_pipe_speculate", "sp_pipe_relinquish",
+    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay",
+    "sp_pipe_handle_done", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv", "sp_pipe_recv_iv",
+    "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
+    "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_last_error",
+)
+
+
+class SpPredConfig(ctypes.Structure):
+    _fields_ = [
+        ("small_io_threshold", ctypes.c_uint64),
+        ("swap_min", ctypes.c_uint64),
+        ("chunk_bytes", ctypes.c_uint64),
+        ("warmup_matches", ctypes.c_int64),
+        ("history_cap", ctypes.c_int64),
+        ("layer_param_bytes", ctypes.c_uint64),
+        ("kv_block_bytes", ctypes.c_uint64),
+    ]
+
+
+class SpPrediction(ctypes.Structure):
+    _fields_ = [("block", ctypes.c_int64), ("predicted_iv", ctypes.c_uint64), ("leeway", ctypes.c_uint64),
+                ("batch", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class SpDecision(ctypes.Structure):
+    _fields_ = [("event", ctypes.c_int32), ("pattern", ctypes.c_int32), ("confidence", ctypes.c_int64),
+                ("after_batches", ctypes.c_int64)]
+
+
+class SpPipeConfig(ctypes.Structure):
+    _fields_ = [
+        ("window", ctypes.c_uint32), ("leeway", ctypes.c_uint32), ("depth", ctypes.c_uint32),
+        ("workers", ctypes.c_uint32), ("chunk_bytes", ctypes.c_uint64), ("nop_bytes", ctypes.c_uint32),
+        ("ring_slots", ctypes.c_uint32), ("speculate", ctypes.c_uint8), ("defer_swap_decrypt", ctypes.c_uint8),
+        ("record_stream", ctypes.c_uint8), ("strict_auth", ctypes.c_uint8), ("reference_compat", ctypes.c_uint8),
+        ("dry", ctypes.c_uint8), ("reserved", ctypes.c_uint8 * 2), ("initial_h2d_iv", ctypes.c_uint64),
+        ("initial_d2h_iv", ctypes.c_uint64), ("batch_bytes", ctypes.c_uint64), ("reserve_bytes", ctypes.c_uint64),
+    ]
+
+
+class SpAction(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("flags", ctypes.c_int32), ("iv", ctypes.c_int64),
+                ("nbytes", ctypes.c_uint64), ("record_id", ctypes.c_int64), ("task_id", ctypes.c_int64),
+                ("count", ctypes.c_int64), ("seq", ctypes.c_int64)]
+
+
+class SpSent(ctypes.Structure):
+    _fields_ = [("iv", ctypes.c_uint64), ("size", ctypes.c_uint64), ("nop", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class SpDelivery(ctypes.Structure):
+    _fields_ = [("seq", ctypes.c_uint64), ("addr", ctypes.c_uint64), ("size", ctypes.c_uint64)]
+
+
+class SpEvent(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("cls", ctypes.c_int32), ("block", ctypes.c_int64),
+                ("base", ctypes.c_uint64), ("len", ctypes.c_uint64), ("payload", ctypes.c_uint64)]
+
+
+_pipe_lib = None
+
+
+def load_sppipe() -> ctypes.CDLL:
+    """Load libsppipe.so (links libspgcm.so from the same directory)."""
+    global _pipe_lib
+    with _lock:
+        if _pipe_lib is not None:
+            return _pipe_lib
+        if not os.path.exists(SPPIPE_PATH):
+            raise NativeUnavailable(
+                f"{SPPIPE_PATH} is missing; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(SPPIPE_PATH)
+        vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        P = ctypes.POINTER
+        sig = {
+            "sp_pred_create": [P(SpPredConfig), P(vp)],
+            "sp_pred_classify": [vp, u64, P(i32)],
+            "sp_pred_observe_out": [vp, i64],
+            "sp_pred_observe_in": [vp, P(i64), i32],
+            "sp_pred_observe_sync": [vp],
+            "sp_pred_recognize": [vp, P(i32), P(i64), P(i64), P(i64)],
+            "sp_pred_cycle_entry": [vp, i64, P(i64), i32, P(i32)],
+            "sp_pred_predict_batches": [vp, u64, u64, i32, P(SpPrediction), i32, P(i32)],
+            "sp_pred_outstanding": [vp, P(i64), i64, P(i64)],
+            "sp_pred_decision": [vp, i64, P(SpDecision)],
+            "sp_pipe_create": [P(SpPipeConfig), ctypes.c_char_p, vp, P(vp)],
+            "sp_pipe_register_block": [vp, i64, u64, u64, i32, vp],
+            "sp_pipe_seed_device": [vp, i64, vp, u64, i32],
+            "sp_pipe_submit_h2d": [vp, u64, u64, i32, i64, P(u64), P(i32)],
+            "sp_pipe_submit_d2h": [vp, u64, u64, i32, i64, P(u64)],
+            "sp_pipe_small_io": [vp, i32, vp, u64],
+            "sp_pipe_sync": [vp], "sp_pipe_speculate": [vp], "sp_pipe_relinquish": [vp, P(i64)],
+            "sp_pipe_drain_decrypts": [vp], "sp_pipe_finish": [vp], "sp_pipe_flush": [vp, i32],
+            "sp_pipe_app_write": [vp, i64, u64, vp, u64, P(i64)],
+            "sp_pipe_app_read": [vp, i64, u64, u64, vp],
+            "sp_pipe_replay": [vp, P(SpEvent), u64, vp, P(u64)],
+            "sp_pipe_handle_done": [vp, u64, P(i32)],
+            "sp_pipe_report": [vp, P(i64), i32, P(i32)],
+            "sp_pipe_actions": [vp, i64, P(SpAction), i64, P(i64)],
+            "sp_pipe_sent_log": [vp, i32, i64, P(SpSent), i64, P(i64)],
+            "sp_pipe_delivered": [vp, i32, i64, P(SpDelivery), vp],
+            "sp_pipe_stats": [vp, P(u64), P(u64), P(u64)],
+        }
+        for name, args in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        for name in ("sp_pred_destroy", "sp_pipe_destroy"):
+            getattr(lib, name).argtypes = [vp]
+            getattr(lib, name).restype = None
+        for name in ("sp_pred_in_batch_count", "sp_pred_decision_count"):
+            getattr(lib, name).argtypes = [vp]
+            getattr(lib, name).restype = i64
+        for name in ("sp_pipe_action_count",):
+            getattr(lib, name).argtypes = [vp]
+            getattr(lib, name).restype = i64
+        lib.sp_pipe_sent_count.argtypes = [vp, i32]
+        lib.sp_pipe_sent_count.restype = i64
+        lib.sp_pipe_delivered_count.argtypes = [vp, i32]
+        lib.sp_pipe_delivered_count.restype = i64
+        for name in ("sp_pipe_send_iv", "sp_pipe_recv_iv"):
+            getattr(lib, name).argtypes = [vp, i32]
+            getattr(lib, name).restype = u64
+        lib.sp_pipe_counter_name.argtypes = [i32]
+        lib.sp_pipe_counter_name.restype = ctypes.c_char_p
+        lib.sp_pipe_last_error.restype = ctypes.c_char_p
+        _pipe_lib = lib
+        return lib
+
+
+def pipe_error() -> str:
+    return load_sppipe().sp_pipe_last_error().decode(errors="replace")

@@ -1,0 +1,1899 @@
+// libsppipe — native speculative pipeline for the encrypted swap path.
+//
+// Control plane: the reference's engine/validator/predictor/channel counters
+// (/root/reference/pkg/src/specpipe/{engine,validator,predictor,channel,memory}.py)
+// restated in C++ with the same decisions in the same order, so the same
+// trace yields identical sent logs, actions, report() counters and decision
+// logs (tests/test_native_engine.py against the reference goldens).
+//
+// Data plane (B200): five long-lived streams per device
+//   h2d   plaintext of swap-ins crosses PCIe from the caller's pinned blocks
+//   spec  encrypt-ahead seals (SpecBatch, engine.py:487-513), <= batch_bytes per launch
+//   comp  ordered queue of on-the-fly / NOP / swap-out seals and every
+//         receiver open, flushed as one k_gcm launch per run of same-kind ops
+//   land  host-endpoint opens of swap-outs (deferred decrypts)
+//   d2h   plaintext lands in the caller's host blocks
+// Cross-stream order uses CUDA events only.  Device staging comes from a
+// stream-ordered CUDA memory pool (cudaMallocFromPoolAsync) kept reserved for
+// the life of the process (release threshold = max), so steady state never
+// calls cudaMalloc; a buffer is returned to the pool on the stream of its
+// last use once every other stream that touched it has passed its fence.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "spgcm.h"
+#include "sppipe.h"
+#include "sppred.hpp"
+
+namespace sppipe {
+
+// ---- error classes (Python exception names) -----------------------------------
+struct EngineErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct OverlapErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct StateErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct BoundsErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct GuardErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct KeyErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct AuthErr : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaErr : std::runtime_error { using std::runtime_error::runtime_error; };
+
+thread_local std::string g_err;
+
+inline void ck(cudaError_t e, const char *where) {
+    if (e != cudaSuccess) throw CudaErr(std::string(where) + ": " + cudaGetErrorString(e));
+}
+inline void ck_sp(int rc, const char *where) {
+    if (rc == SP_OK) return;
+    if (rc == SP_EINVAL) throw ValueErr(std::string(where) + ": " + sp_last_error());
+    throw CudaErr(std::string(where) + ": " + sp_last_error());
+}
+
+std::string hex(uint64_t v) {
+    char b[32];
+    snprintf(b, sizeof b, "%#llx", (unsigned long long)v);
+    return b;
+}
+
+constexpr uint64_t kTag = 16;
+constexpr int H2D = 0, D2H = 1;
+inline uint64_t round16(uint64_t n) { return (n + 15u) & ~uint64_t(15); }
+
+// ---- events and device buffers ------------------------------------------------
+class Plane;
+
+struct Fence {
+    cudaEvent_t ev = nullptr;
+    cudaStream_t stream = nullptr;
+    bool recorded = false;
+    Plane *plane = nullptr;
+    ~Fence();
+};
+using FenceP = std::shared_ptr<Fence>;
+
+struct Buf {
+    Plane *plane = nullptr;
+    uint8_t *ptr = nullptr;
+    uint64_t size = 0;
+    std::vector<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
+    uint64_t last_use = 0;
+    cudaStream_t last_stream = nullptr;
+    void use(cudaStream_t s, const FenceP &f, uint64_t tick) {
+        last_use = tick;
+        last_stream = s;
+        for (auto &u : uses)
+            if (u.first == s) {
+                u.second = f;
+                return;
+            }
+        uses.emplace_back(s, f);
+    }
+    ~Buf();
+};
+using BufP = std::shared_ptr<Buf>;
+
+// A sealed message on the wire (channel.CiphertextMsg / DeviceCiphertext).
+struct Msg {
+    BufP buf;  // payload at off, tag at tag_off (null in the dry plane)
+    uint64_t off = 0, tag_off = 0, len = 0;
+    bool nop = false;
+    FenceP ready;  // producer's fence (recorded at its launch)
+};
+using MsgP = std::shared_ptr<Msg>;
+
+struct View {
+    BufP buf;
+    uint64_t off = 0, len = 0;
+    uint8_t *ptr() const { return buf->ptr + off; }
+};
+
+// ---- host memory model (memory.py) ---------------------------------------------
+struct Block {
+    int64_t id;
+    uint64_t base, len;
+    int kind;
+    uint8_t *host;
+};
+
+struct WriteGuard {
+    uint64_t base, len;
+    int64_t owner;
+    bool active;
+};
+
+class HostMem {
+  public:
+    std::map<int64_t, Block> blocks;            // id -> block
+    std::map<uint64_t, int64_t> by_base;        // base -> id
+    std::map<int64_t, WriteGuard> write_guards;  // owner (record id) -> guard (insertion order == id order)
+    std::map<int64_t, std::pair<uint64_t, uint64_t>> read_guards;  // task id -> (base, len)
+
+    Block &block(int64_t id) {
+        auto it = blocks.find(id);
+        if (it == blocks.end()) throw KeyErr(std::to_string(id));
+        return it->second;
+    }
+    // memory.py block_at: the block containing [base, base+len)
+    std::pair<Block *, uint64_t> block_at(uint64_t base, uint64_t len) {
+        auto it = by_base.upper_bound(base);
+        if (it != by_base.begin()) {
+            --it;
+            Block &b = blocks.at(it->second);
+            if (b.base <= base && base + len <= b.base + b.len) return {&b, base - b.base};
+        }
+        throw BoundsErr("range (" + hex(base) + ", " + std::to_string(len) + ") is not inside any block");
+    }
+    static bool overlaps(uint64_t ab, uint64_t al, uint64_t bb, uint64_t bl) { return ab < bb + bl && bb < ab + al; }
+
+    void install_write_guard(uint64_t base, uint64_t len, int64_t owner) {
+        for (auto &kv : write_guards) {
+            const WriteGuard &g = kv.second;
+            if (g.active && overlaps(base, len, g.base, g.len))
+                throw GuardErr("write guard (" + hex(base) + ", " + std::to_string(len) + ") overlaps guard of record " +
+                               std::to_string(g.owner));
+        }
+        write_guards[owner] = WriteGuard{base, len, owner, true};
+    }
+    void release_write_guard(int64_t owner) { write_guards.erase(owner); }
+    void install_read_guard(uint64_t base, uint64_t len, int64_t task) {
+        for (auto &kv : read_guards)
+            if (overlaps(base, len, kv.second.first, kv.second.second))
+                throw GuardErr("read guard (" + hex(base) + ", " + std::to_string(len) + ") overlaps task " +
+                               std::to_string(kv.first));
+        read_guards[task] = {base, len};
+    }
+    void release_read_guard(int64_t task) { read_guards.erase(task); }
+    std::vector<int64_t> read_guards_over(uint64_t base, uint64_t len) const {
+        std::vector<int64_t> out;
+        for (auto &kv : read_guards)
+            if (overlaps(base, len, kv.second.first, kv.second.second)) out.push_back(kv.first);
+        return out;
+    }
+};
+
+// ---- validator (validator.py:104-230) ----------------------------------------------
+enum RecState { PENDING = 0, COMMITTED = 1, INVALIDATED = 2 };
+enum Verdict { V_HIT = 0, V_AHEAD = 1, V_BEHIND = 2, V_STALE = 3, V_MISS = 4, V_NONE = 5 };
+
+struct Record {
+    int64_t id;
+    uint64_t base, len, iv;
+    std::vector<MsgP> chunks;  // released (emptied) once the record leaves the window
+    std::vector<uint64_t> chunk_lens;
+    RecState state = PENDING;
+    int64_t block_id;  // INT64_MIN = None
+    uint64_t span() const { return chunk_lens.size(); }
+    uint64_t last_iv() const { return iv + span() - 1; }
+};
+
+struct RangeKey {
+    uint64_t base, len;
+    bool operator==(const RangeKey &o) const { return base == o.base && len == o.len; }
+};
+struct RangeHash {
+    size_t operator()(const RangeKey &k) const { return (size_t)(k.base * 0x9e3779b97f4a7c15ull ^ (k.len + (k.len << 17))); }
+};
+
+class Validator {
+  public:
+    Validator(HostMem &m, uint64_t window) : mem(m), window(window) {}
+    HostMem &mem;
+    uint64_t window;
+    std::deque<Record> records;  // id i at index i-1
+    int64_t next_id = 1;
+    std::unordered_map<RangeKey, int64_t, RangeHash> by_range, stale;
+    std::unordered_map<uint64_t, int64_t> by_iv;
+    std::set<int64_t> order;                        // pending ids (label order == id order)
+    std::set<std::pair<uint64_t, int64_t>> bases;  // (base, id) of pending
+    int64_t counters[5] = {0, 0, 0, 0, 0};
+    int64_t evicted = 0;
+
+    Record &rec(int64_t id) { return records[(size_t)(id - 1)]; }
+
+    int64_t label(std::vector<MsgP> chunks, std::vector<uint64_t> lens, uint64_t base, uint64_t len, uint64_t iv,
+                  int64_t block_id) {
+        // pending ranges are disjoint: only the last one starting below the end can intersect
+        auto it = bases.lower_bound({base + len, INT64_MIN});
+        if (it != bases.begin()) {
+            --it;
+            if (it->first + rec(it->second).len > base)
+                throw OverlapErr("range (" + hex(base) + ", " + std::to_string(len) + ") overlaps pending record " +
+                                 std::to_string(it->second));
+        }
+        uint64_t span = lens.size();
+        for (uint64_t v = iv; v < iv + span; ++v)
+            if (by_iv.count(v)) throw OverlapErr("counter " + std::to_string(v) + " already claimed by a pending record");
+        if (order.size() >= window) {
+            invalidate(*order.begin());
+            ++evicted;
+        }
+        Record r;
+        r.id = next_id++;
+        r.base = base;
+        r.len = len;
+        r.iv = iv;
+        r.chunks = std::move(chunks);
+        r.chunk_lens = std::move(lens);
+        r.block_id = block_id;
+        records.push_back(std::move(r));
+        Record &x = records.back();
+        by_range[{base, len}] = x.id;
+        for (uint64_t v = iv; v < iv + span; ++v) by_iv[v] = x.id;
+        order.insert(x.id);
+        bases.insert({base, x.id});
+        stale.erase({base, len});
+        mem.install_write_guard(base, len, x.id);
+        return x.id;
+    }
+
+    Verdict validate(uint64_t base, uint64_t len, uint64_t cur, int64_t &rid) {
+        rid = -1;
+        Verdict v;
+        auto it = by_range.find({base, len});
+        if (it != by_range.end()) {
+            Record &r = rec(it->second);
+            rid = r.id;
+            v = r.iv == cur ? V_HIT : (r.iv > cur ? V_AHEAD : V_BEHIND);
+        } else {
+            auto s = stale.find({base, len});
+            if (s != stale.end()) {
+                rid = s->second;
+                v = V_STALE;
+            } else {
+                v = V_MISS;
+            }
+        }
+        counters[v]++;
+        return v;
+    }
+
+    void drop_pending(Record &r) {
+        by_range.erase({r.base, r.len});
+        for (uint64_t v = r.iv; v < r.iv + r.span(); ++v) by_iv.erase(v);
+        order.erase(r.id);
+        bases.erase({r.base, r.id});
+        mem.release_write_guard(r.id);
+    }
+    void commit(int64_t id) {
+        Record &r = rec(id);
+        if (r.state != PENDING) throw StateErr("record " + std::to_string(id) + " is " + state_name(r.state) + ", not pending");
+        drop_pending(r);
+        r.state = COMMITTED;
+    }
+    void invalidate(int64_t id) {
+        Record &r = rec(id);
+        if (r.state != PENDING) throw StateErr("record " + std::to_string(id) + " is " + state_name(r.state) + ", not pending");
+        drop_pending(r);
+        r.state = INVALIDATED;
+        stale[{r.base, r.len}] = r.id;
+        r.chunks.clear();  // device payloads go back to the pool
+    }
+    void on_write_fault(int64_t owner) {
+        if (owner >= 1 && owner < next_id && rec(owner).state == PENDING) invalidate(owner);
+    }
+    std::vector<int64_t> pending_ids() const { return std::vector<int64_t>(order.begin(), order.end()); }
+    int64_t pending_at_iv(uint64_t iv) const {
+        auto it = by_iv.find(iv);
+        return it == by_iv.end() ? -1 : it->second;
+    }
+    bool has_pending_range(uint64_t base, uint64_t len) const { return by_range.count({base, len}) != 0; }
+    int64_t invalidate_pending_below(uint64_t iv) {
+        std::vector<int64_t> doomed;
+        for (int64_t id : order)
+            if (rec(id).last_iv() < iv) doomed.push_back(id);
+        for (int64_t id : doomed) invalidate(id);
+        return (int64_t)doomed.size();
+    }
+    static const char *state_name(RecState s) {
+        return s == PENDING ? "pending" : (s == COMMITTED ? "committed" : "invalidated");
+    }
+};
+
+// ---- data plane -----------------------------------------------------------------------
+struct Streams {
+    cudaStream_t comp, spec, h2d, d2h, land;
+};
+
+struct DevicePool {
+    cudaMemPool_t pool = nullptr;
+    uint64_t reserved = 0;
+};
+
+std::mutex g_dev_mu;
+std::map<int, Streams> g_streams;
+std::map<int, DevicePool> g_pools;
+
+Streams streams_for(int dev) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto it = g_streams.find(dev);
+    if (it != g_streams.end()) return it->second;
+    Streams s;
+    cudaStream_t *all[5] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land};
+    for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
+    g_streams[dev] = s;
+    return s;
+}
+
+cudaMemPool_t pool_for(int dev, uint64_t reserve, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevicePool &p = g_pools[dev];
+    if (!p.pool) {
+        cudaMemPoolProps props;
+        memset(&props, 0, sizeof props);
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        ck(cudaMemPoolCreate(&p.pool, &props), "cudaMemPoolCreate");
+        uint64_t thr = UINT64_MAX;
+        ck(cudaMemPoolSetAttribute(p.pool, cudaMemPoolAttrReleaseThreshold, &thr), "pool threshold");
+        int zero = 0;
+        // never make an allocating stream wait on another stream's pending free
+        ck(cudaMemPoolSetAttribute(p.pool, cudaMemPoolReuseAllowInternalDependencies, &zero), "pool deps");
+    }
+    if (reserve > p.reserved) {
+        void *ptr = nullptr;
+        ck(cudaMallocFromPoolAsync(&ptr, reserve, p.pool, s), "pool reserve");
+        ck(cudaFreeAsync(ptr, s), "pool reserve free");
+        ck(cudaStreamSynchronize(s), "pool reserve sync");
+        p.reserved = reserve;
+    }
+    return p.pool;
+}
+
+struct Op {
+    int kind;  // 0 wait, 1 seal, 2 open
+    FenceP wait;
+    sp_desc d;
+    BufP a, b, c;  // buffers the op touches (kept alive until issued)
+};
+
+struct Landing {
+    Block *block;
+    std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;  // msg, iv, offset in block
+    int dir;
+};
+
+class Plane {
+  public:
+    bool dry;
+    int dev = 0;
+    Streams s{};
+    cudaMemPool_t pool = nullptr;
+    sp_ctx *ctx = nullptr;
+    uint64_t batch_bytes;
+    uint64_t tick = 0;
+    std::vector<cudaEvent_t> free_events;
+    struct Garbage {
+        uint8_t *ptr;
+        std::vector<std::pair<cudaStream_t, FenceP>> uses;
+        cudaStream_t last;
+    };
+    std::vector<Garbage> garbage;
+    bool collecting = false;
+
+    // compute queue
+    std::vector<Op> ops;
+    uint64_t ops_bytes = 0;
+    FenceP window;
+    // small-payload arena
+    std::vector<uint8_t> arena_host;
+    BufP arena_dev;
+    uint64_t arena_off = 0;
+    struct PinnedArena {
+        uint8_t *ptr;
+        uint64_t cap;
+        FenceP done;
+    };
+    std::vector<PinnedArena> pinned_free, pinned_busy;
+    static constexpr uint64_t kArenaBytes = 1 << 20;
+    // landings
+    std::vector<Landing> landings;
+    std::unordered_set<int64_t> landing_blocks;
+    std::unordered_map<int64_t, FenceP> host_ready;  // block -> fence after last D2H into it
+    std::unordered_map<int64_t, FenceP> h2d_done;    // block -> fence after last H2D from it
+    // status words of opens
+    int32_t *status = nullptr;
+    uint64_t status_cap = 1 << 16, status_used = 0;
+    uint64_t bytes_h2d = 0, bytes_d2h = 0, launches = 0;
+    BufP zero_scratch;
+
+    Plane(bool dry_, const uint8_t key[32], uint64_t batch, uint64_t reserve) : dry(dry_), batch_bytes(batch) {
+        if (dry) return;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        s = streams_for(dev);
+        pool = pool_for(dev, reserve, s.comp);
+        int rc = sp_ctx_create(key, &ctx);
+        if (rc) throw CudaErr(std::string("sp_ctx_create: ") + sp_last_error());
+        ck(cudaMalloc(&status, status_cap * sizeof(int32_t)), "cudaMalloc(status)");
+        ck(cudaMemset(status, 0, status_cap * sizeof(int32_t)), "cudaMemset(status)");
+        window = new_fence();
+    }
+    ~Plane() {
+        if (dry) return;
+        try {
+            finish_streams();
+        } catch (...) {
+        }
+        ops.clear();
+        landings.clear();
+        host_ready.clear();
+        h2d_done.clear();
+        arena_dev.reset();
+        zero_scratch.reset();
+        window.reset();
+        collect();
+        cudaStreamSynchronize(s.comp);
+        for (auto &a : pinned_free) cudaFreeHost(a.ptr);
+        for (auto &a : pinned_busy) {
+            a.done.reset();
+            cudaFreeHost(a.ptr);
+        }
+        for (cudaEvent_t e : free_events) cudaEventDestroy(e);
+        if (status) cudaFree(status);
+        if (ctx) sp_ctx_destroy(ctx);
+    }
+
+    // -- events / buffers --------------------------------------------------------------
+    FenceP new_fence() {
+        auto f = std::make_shared<Fence>();
+        f->plane = this;
+        if (!free_events.empty()) {
+            f->ev = free_events.back();
+            free_events.pop_back();
+        } else {
+            ck(cudaEventCreateWithFlags(&f->ev, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        return f;
+    }
+    void record(const FenceP &f, cudaStream_t st) {
+        ck(cudaEventRecord(f->ev, st), "cudaEventRecord");
+        f->stream = st;
+        f->recorded = true;
+    }
+    FenceP record_new(cudaStream_t st) {
+        FenceP f = new_fence();
+        record(f, st);
+        return f;
+    }
+    void wait(cudaStream_t st, const FenceP &f) {
+        if (!f) return;
+        if (!f->recorded) throw std::logic_error("wait on an unrecorded fence");
+        if (f->stream == st) return;  // stream order covers it
+        ck(cudaStreamWaitEvent(st, f->ev, 0), "cudaStreamWaitEvent");
+    }
+    BufP alloc(uint64_t n, cudaStream_t st) {
+        auto b = std::make_shared<Buf>();
+        b->plane = this;
+        b->size = n;
+        if (!dry) {
+            void *p = nullptr;
+            ck(cudaMallocFromPoolAsync(&p, std::max<uint64_t>(n, 16), pool, st), "cudaMallocFromPoolAsync");
+            b->ptr = static_cast<uint8_t *>(p);
+            b->last_stream = st;
+            b->uses.emplace_back(st, FenceP());
+        }
+        return b;
+    }
+    void retire(Buf *b) {
+        if (dry || !b->ptr) return;
+        garbage.push_back({b->ptr, std::move(b->uses), b->last_stream});
+    }
+    // Return retired buffers to the pool on the stream of their last use,
+    // after every other stream that touched them has passed its fence.
+    void collect() {
+        if (dry || collecting) return;
+        collecting = true;
+        std::vector<Garbage> g;
+        g.swap(garbage);
+        for (auto &x : g) {
+            cudaStream_t fs = x.last;
+            for (auto &u : x.uses) {
+                if (u.first == fs) continue;
+                if (u.second && u.second->recorded) {
+                    ck(cudaStreamWaitEvent(fs, u.second->ev, 0), "cudaStreamWaitEvent(free)");
+                } else {
+                    FenceP f = record_new(u.first);
+                    ck(cudaStreamWaitEvent(fs, f->ev, 0), "cudaStreamWaitEvent(free)");
+                }
+            }
+            x.uses.clear();
+            ck(cudaFreeAsync(x.ptr, fs), "cudaFreeAsync");
+        }
+        collecting = false;
+    }
+
+    // -- status slots -------------------------------------------------------------------
+    int32_t *status_slot() {
+        if (status_used + 1 > status_cap) check_auth();
+        return status + status_used++;
+    }
+    void check_auth() {
+        if (dry) return;
+        flush();
+        if (!status_used) return;
+        ck(cudaStreamSynchronize(s.comp), "sync comp");
+        ck(cudaStreamSynchronize(s.land), "sync land");
+        ck(cudaStreamSynchronize(s.d2h), "sync d2h");
+        std::vector<int32_t> h(status_used);
+        ck(cudaMemcpy(h.data(), status, status_used * sizeof(int32_t), cudaMemcpyDeviceToHost), "status read");
+        int64_t bad = 0;
+        for (int32_t v : h) bad += v != 0;
+        ck(cudaMemset(status, 0, status_used * sizeof(int32_t)), "status clear");
+        status_used = 0;
+        if (bad) throw AuthErr("authentication failed on the device");
+    }
+
+    // -- compute queue ------------------------------------------------------------------
+    void queue(Op &&op, uint64_t nbytes) {
+        ops.push_back(std::move(op));
+        ops_bytes += nbytes;
+        if (ops_bytes >= batch_bytes) flush();
+    }
+    void wait_for(const FenceP &f) {
+        if (f && f != window) {
+            Op op{};
+            op.kind = 0;
+            op.wait = f;
+            ops.push_back(std::move(op));
+        }
+    }
+
+    void flush() {
+        if (dry) return;
+        if (!arena_host.empty()) {
+            PinnedArena pa = pinned_arena(arena_host.size());
+            memcpy(pa.ptr, arena_host.data(), arena_host.size());
+            ck(cudaMemcpyAsync(arena_dev->ptr, pa.ptr, arena_host.size(), cudaMemcpyHostToDevice, s.comp),
+               "arena H2D");
+            pa.done = record_new(s.comp);
+            arena_dev->use(s.comp, pa.done, ++tick);
+            pinned_busy.push_back(pa);
+            bytes_h2d += arena_host.size();
+            arena_host.clear();
+            arena_dev.reset();
+            arena_off = 0;
+        }
+        if (!ops.empty()) {
+            std::vector<Op> q;
+            q.swap(ops);
+            ops_bytes = 0;
+            std::vector<sp_desc> descs;
+            size_t i = 0;
+            while (i < q.size()) {
+                if (q[i].kind == 0) {
+                    wait(s.comp, q[i].wait);
+                    ++i;
+                    continue;
+                }
+                size_t j = i;
+                descs.clear();
+                while (j < q.size() && q[j].kind == q[i].kind) descs.push_back(q[j++].d);
+                int rc = q[i].kind == 1 ? sp_seal_batch(ctx, descs.data(), (int)descs.size(), s.comp)
+                                        : sp_open_batch(ctx, descs.data(), (int)descs.size(), s.comp);
+                ck_sp(rc, q[i].kind == 1 ? "sp_seal_batch" : "sp_open_batch");
+                ++launches;
+                i = j;
+            }
+            record(window, s.comp);
+            ++tick;
+            for (auto &op : q) {
+                if (op.a) op.a->use(s.comp, window, tick);
+                if (op.b) op.b->use(s.comp, window, tick);
+                if (op.c) op.c->use(s.comp, window, tick);
+            }
+            window = new_fence();
+        }
+        if (!landings.empty()) flush_landings();
+        collect();
+    }
+
+    PinnedArena pinned_arena(uint64_t need) {
+        for (size_t k = 0; k < pinned_busy.size();) {
+            if (cudaEventQuery(pinned_busy[k].done->ev) == cudaSuccess) {
+                pinned_busy[k].done.reset();
+                pinned_free.push_back(pinned_busy[k]);
+                pinned_busy.erase(pinned_busy.begin() + (long)k);
+            } else {
+                ++k;
+            }
+        }
+        for (size_t k = 0; k < pinned_free.size(); ++k)
+            if (pinned_free[k].cap >= need) {
+                PinnedArena a = pinned_free[k];
+                pinned_free.erase(pinned_free.begin() + (long)k);
+                return a;
+            }
+        PinnedArena a{nullptr, std::max(need, kArenaBytes), nullptr};
+        ck(cudaHostAlloc(reinterpret_cast<void **>(&a.ptr), a.cap, cudaHostAllocDefault), "cudaHostAlloc(arena)");
+        return a;
+    }
+
+    void flush_landings() {
+        std::vector<Landing> ls;
+        ls.swap(landings);
+        landing_blocks.clear();
+        uint64_t total = 0;
+        std::unordered_set<Fence *> waited;
+        for (auto &l : ls)
+            for (auto &j : l.jobs) {
+                const MsgP &m = std::get<0>(j);
+                total += m->len;
+                if (m->ready && !waited.count(m->ready.get())) {
+                    wait(s.land, m->ready);
+                    waited.insert(m->ready.get());
+                }
+            }
+        BufP buf = alloc(total, s.land);
+        std::vector<sp_desc> descs;
+        struct Place {
+            Block *block;
+            uint64_t off, boff, n;
+        };
+        std::vector<Place> places;
+        uint64_t off = 0;
+        for (auto &l : ls)
+            for (auto &j : l.jobs) {
+                const MsgP &m = std::get<0>(j);
+                sp_desc d{};
+                d.dir = (uint32_t)l.dir;
+                d.iv = std::get<1>(j);
+                d.len = m->len;
+                d.src = m->buf->ptr + m->off;
+                d.dst = buf->ptr + off;
+                d.tag = m->buf->ptr + m->tag_off;
+                d.status = status_slot();
+                descs.push_back(d);
+                places.push_back({l.block, off, std::get<2>(j), m->len});
+                off += m->len;
+            }
+        ck_sp(sp_open_batch(ctx, descs.data(), (int)descs.size(), s.land), "sp_open_batch(landing)");
+        ++launches;
+        FenceP opened = record_new(s.land);
+        ++tick;
+        buf->use(s.land, opened, tick);
+        for (auto &l : ls)
+            for (auto &j : l.jobs) std::get<0>(j)->buf->use(s.land, opened, tick);
+        wait(s.d2h, opened);
+        Block *last = nullptr;
+        for (auto &p : places) {
+            if (p.block != last) {
+                auto it = h2d_done.find(p.block->id);
+                if (it != h2d_done.end() && it->second) wait(s.d2h, it->second);
+                last = p.block;
+            }
+            ck(cudaMemcpyAsync(p.block->host + p.boff, buf->ptr + p.off, p.n, cudaMemcpyDeviceToHost, s.d2h),
+               "landing D2H");
+        }
+        FenceP ev = record_new(s.d2h);
+        buf->use(s.d2h, ev, ++tick);
+        for (auto &l : ls) host_ready[l.block->id] = ev;
+        bytes_d2h += total;
+    }
+
+    void before_host_read_of(int64_t block_id) {
+        if (landing_blocks.count(block_id)) flush();
+    }
+
+    // -- seals ----------------------------------------------------------------------------
+    // H2D the plaintext of `block` [inner+off, +n) per span into one staging
+    // buffer; returns the staging buffer (payload views at off-first, tags after).
+    BufP stage_h2d(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, FenceP &done) {
+        before_host_read_of(b.id);
+        uint64_t total = 0;
+        for (auto &sp : spans) total += sp.second;
+        uint64_t first = spans[0].first;
+        auto it = host_ready.find(b.id);
+        if (it != host_ready.end() && it->second) wait(s.h2d, it->second);
+        BufP buf = alloc(round16(total) + kTag * spans.size(), s.h2d);
+        ck(cudaMemcpyAsync(buf->ptr, b.host + inner + first, total, cudaMemcpyHostToDevice, s.h2d), "swap-in H2D");
+        done = record_new(s.h2d);
+        buf->use(s.h2d, done, ++tick);
+        h2d_done[b.id] = done;
+        bytes_h2d += total;
+        return buf;
+    }
+
+    std::vector<MsgP> seal_host_chunks(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans,
+                                       int dir, uint64_t iv0) {
+        std::vector<MsgP> msgs;
+        if (dry) {
+            for (auto &sp : spans) {
+                auto m = std::make_shared<Msg>();
+                m->len = sp.second;
+                msgs.push_back(m);
+                bytes_h2d += sp.second;
+            }
+            return msgs;
+        }
+        FenceP done;
+        BufP buf = stage_h2d(b, inner, spans, done);
+        uint64_t first = spans[0].first, total = 0;
+        for (auto &sp : spans) total += sp.second;
+        wait_for(done);
+        for (size_t i = 0; i < spans.size(); ++i) {
+            auto m = std::make_shared<Msg>();
+            m->buf = buf;
+            m->off = spans[i].first - first;
+            m->len = spans[i].second;
+            m->tag_off = round16(total) + kTag * i;
+            m->ready = window;
+            Op op{};
+            op.kind = 1;
+            op.d.dir = (uint32_t)dir;
+            op.d.iv = iv0 + i;
+            op.d.len = m->len;
+            op.d.src = buf->ptr + m->off;
+            op.d.dst = buf->ptr + m->off;
+            op.d.tag = buf->ptr + m->tag_off;
+            op.a = buf;
+            queue(std::move(op), m->len);
+            msgs.push_back(m);
+        }
+        return msgs;
+    }
+
+    // Encrypt-ahead work of one engine entry point (devplane.SpecBatch).
+    struct SpecBatch {
+        Plane *p;
+        std::vector<sp_desc> items;
+        std::vector<BufP> bufs;
+        uint64_t bytes = 0;
+        FenceP ready;
+        FenceP last_copy;
+        explicit SpecBatch(Plane *pl) : p(pl) {
+            if (!p->dry) ready = p->new_fence();
+        }
+        std::vector<MsgP> add(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
+                              uint64_t iv0) {
+            std::vector<MsgP> msgs;
+            if (p->dry) {
+                for (auto &sp : spans) {
+                    auto m = std::make_shared<Msg>();
+                    m->len = sp.second;
+                    msgs.push_back(m);
+                    p->bytes_h2d += sp.second;
+                }
+                return msgs;
+            }
+            FenceP done;
+            BufP buf = p->stage_h2d(b, inner, spans, done);
+            last_copy = done;
+            uint64_t first = spans[0].first, total = 0;
+            for (auto &sp : spans) total += sp.second;
+            for (size_t i = 0; i < spans.size(); ++i) {
+                auto m = std::make_shared<Msg>();
+                m->buf = buf;
+                m->off = spans[i].first - first;
+                m->len = spans[i].second;
+                m->tag_off = round16(total) + kTag * i;
+                m->ready = ready;
+                sp_desc d{};
+                d.dir = (uint32_t)dir;
+                d.iv = iv0 + i;
+                d.len = m->len;
+                d.src = buf->ptr + m->off;
+                d.dst = buf->ptr + m->off;
+                d.tag = buf->ptr + m->tag_off;
+                items.push_back(d);
+                msgs.push_back(m);
+            }
+            bufs.push_back(buf);
+            bytes += total;
+            if (bytes >= p->batch_bytes) launch();
+            return msgs;
+        }
+        void launch() {
+            if (p->dry || items.empty()) return;
+            p->wait(p->s.spec, last_copy);
+            ck_sp(sp_seal_batch(p->ctx, items.data(), (int)items.size(), p->s.spec), "sp_seal_batch(spec)");
+            ++p->launches;
+            p->record(ready, p->s.spec);
+            ++p->tick;
+            for (auto &b : bufs) b->use(p->s.spec, ready, p->tick);
+            items.clear();
+            bufs.clear();
+            bytes = 0;
+            ready = p->new_fence();
+        }
+    };
+
+    std::vector<MsgP> seal_device_chunks(const View &src, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
+                                         uint64_t iv0) {
+        std::vector<MsgP> msgs;
+        if (dry) {
+            for (auto &sp : spans) {
+                auto m = std::make_shared<Msg>();
+                m->len = sp.second;
+                msgs.push_back(m);
+            }
+            return msgs;
+        }
+        uint64_t total = 0, first = spans[0].first;
+        for (auto &sp : spans) total += sp.second;
+        BufP buf = alloc(round16(total) + kTag * spans.size(), s.comp);
+        for (size_t i = 0; i < spans.size(); ++i) {
+            auto m = std::make_shared<Msg>();
+            m->buf = buf;
+            m->off = spans[i].first - first;
+            m->len = spans[i].second;
+            m->tag_off = round16(total) + kTag * i;
+            m->ready = window;
+            Op op{};
+            op.kind = 1;
+            op.d.dir = (uint32_t)dir;
+            op.d.iv = iv0 + i;
+            op.d.len = m->len;
+            op.d.src = src.buf->ptr + src.off + spans[i].first;
+            op.d.dst = buf->ptr + m->off;
+            op.d.tag = buf->ptr + m->tag_off;
+            op.a = buf;
+            op.b = src.buf;
+            queue(std::move(op), m->len);
+            msgs.push_back(m);
+        }
+        return msgs;
+    }
+
+    // NOP pads and token I/O: staged in the byte arena (one PCIe copy per flush).
+    std::vector<MsgP> seal_bytes(const std::vector<std::pair<const uint8_t *, uint64_t>> &payloads, int dir, uint64_t iv0,
+                                 bool nop) {
+        std::vector<MsgP> msgs;
+        for (size_t i = 0; i < payloads.size(); ++i) {
+            uint64_t n = payloads[i].second;
+            auto m = std::make_shared<Msg>();
+            m->len = n;
+            m->nop = nop;
+            if (!dry) {
+                uint64_t need = round16(n) + kTag;
+                if (!arena_dev || arena_off + need > arena_dev->size) {
+                    if (arena_off) flush();
+                    arena_dev = alloc(std::max(kArenaBytes, need), s.comp);
+                    arena_off = 0;
+                    arena_host.clear();
+                }
+                uint64_t o = arena_off;
+                arena_off += need;
+                if (arena_host.size() < o + n) arena_host.resize(o + n, 0);
+                if (payloads[i].first) memcpy(arena_host.data() + o, payloads[i].first, n);
+                else memset(arena_host.data() + o, 0, n);
+                m->buf = arena_dev;
+                m->off = o;
+                m->tag_off = o + need - kTag;
+                m->ready = window;
+                Op op{};
+                op.kind = 1;
+                op.d.dir = (uint32_t)dir;
+                op.d.iv = iv0 + i;
+                op.d.len = n;
+                op.d.src = arena_dev->ptr + o;
+                op.d.dst = arena_dev->ptr + o;
+                op.d.tag = arena_dev->ptr + m->tag_off;
+                op.a = arena_dev;
+                queue(std::move(op), n);
+            }
+            msgs.push_back(m);
+        }
+        return msgs;
+    }
+
+    // -- opens ----------------------------------------------------------------------------
+    // jobs: (msg, iv, dst view or empty) -> queued receiver opens.
+    void open_into(std::vector<std::tuple<MsgP, uint64_t, View>> &jobs, int dir) {
+        if (dry) return;
+        for (auto &j : jobs) {
+            const MsgP &m = std::get<0>(j);
+            wait_for(m->ready);
+            View dst = std::get<2>(j);
+            if (!dst.buf) dst = View{alloc(m->len, s.comp), 0, m->len};
+            Op op{};
+            op.kind = 2;
+            op.d.dir = (uint32_t)dir;
+            op.d.iv = std::get<1>(j);
+            op.d.len = m->len;
+            op.d.src = m->buf->ptr + m->off;
+            op.d.dst = dst.ptr();
+            op.d.tag = m->buf->ptr + m->tag_off;
+            op.d.status = status_slot();
+            op.a = m->buf;
+            op.b = dst.buf;
+            queue(std::move(op), m->len);
+        }
+    }
+
+    void land_on_host(Block &b, std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs, int dir) {
+        uint64_t n = 0;
+        for (auto &j : jobs) n += std::get<0>(j)->len;
+        if (dry) {
+            bytes_d2h += n;
+            return;
+        }
+        landings.push_back({&b, std::move(jobs), dir});
+        landing_blocks.insert(b.id);
+        ops_bytes += n;
+        if (ops_bytes >= batch_bytes) flush();
+    }
+
+    View new_device_buffer(uint64_t n) { return View{alloc(n, s.comp), 0, n}; }
+
+    void host_sync(int64_t block_id) {
+        if (dry) return;
+        flush();
+        if (block_id == INT64_MIN) {
+            ck(cudaStreamSynchronize(s.d2h), "sync d2h");
+            return;
+        }
+        auto it = host_ready.find(block_id);
+        if (it != host_ready.end() && it->second) ck(cudaEventSynchronize(it->second->ev), "host_ready sync");
+    }
+    void before_host_write(int64_t block_id) {
+        if (dry) return;
+        flush();
+        for (auto *t : {&h2d_done, &host_ready}) {
+            auto it = t->find(block_id);
+            if (it != t->end() && it->second) ck(cudaEventSynchronize(it->second->ev), "host write sync");
+        }
+    }
+    void finish_streams() {
+        flush();
+        cudaStream_t all[5] = {s.comp, s.spec, s.land, s.h2d, s.d2h};
+        for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    }
+    void finish() {
+        if (dry) return;
+        finish_streams();
+        check_auth();
+    }
+    void copy_to_host(const View &v, void *out) {
+        flush();
+        ck(cudaStreamSynchronize(s.comp), "sync comp");
+        ck(cudaStreamSynchronize(s.land), "sync land");
+        ck(cudaMemcpy(out, v.ptr(), v.len, cudaMemcpyDeviceToHost), "copy to host");
+    }
+};
+
+Fence::~Fence() {
+    if (plane && ev) plane->free_events.push_back(ev);
+}
+Buf::~Buf() {
+    if (plane) plane->retire(this);
+}
+
+// ---- engine (engine.py:171-624) --------------------------------------------------------
+enum Counter {
+    C_HIT, C_IV_AHEAD, C_IV_BEHIND, C_STALE, C_MISS, C_COMMITTED_SENDS, C_ON_THE_FLY, C_DATA_MSGS, C_NOPS,
+    C_RELINQUISHES, C_RELINQUISHED_RECORDS, C_NOP_BURNED_RECORDS, C_EXPIRED_RECORDS, C_DEFERRED_DECRYPTS,
+    C_SYNC_DECRYPTS, C_WRITE_FAULTS, C_READ_FAULTS, C_SPEC_ENCRYPTS, C_REPLANS, C_REPLANNED_RECORDS, C_SPEC_SKIPPED,
+    C_SPEC_CANCELLED, C_SMALL_IO_H2D, C_SMALL_IO_D2H, C_SYNCS, C_SEQ_BATCHES, C_SEQ_HITS, C_SUSPENDED,
+    C_SUSPENDED_FALLBACK, C_FINAL_DISCARDED, C_OTF_BURNED_RECORDS, C_COUNT
+};
+const char *kCounterNames[] = {
+    "hit", "iv_ahead", "iv_behind", "stale", "miss", "committed_sends", "on_the_fly", "data_msgs", "nops",
+    "relinquishes", "relinquished_records", "nop_burned_records", "expired_records", "deferred_decrypts",
+    "sync_decrypts", "write_faults", "read_faults", "spec_encrypts", "replans", "replanned_records",
+    "spec_skipped", "spec_cancelled", "small_io_h2d", "small_io_d2h", "syncs", "seq_batches", "seq_hits",
+    "suspended", "suspended_fallback", "final_discarded", "otf_burned_records",
+    // derived entries appended by sp_pipe_report
+    "ring_violations", "ring_high_water", "send_iv", "gpu_send_iv", "otf_burned_present",
+};
+constexpr int kReportCount = C_COUNT + 5;
+
+struct SpecTask {
+    int64_t block_id;
+    uint64_t base, len, iv;
+    bool cancelled = false;
+};
+struct Req {
+    int dir;
+    uint64_t base, len;
+    int cls;
+    int64_t block_id;
+};
+struct Suspended {
+    Req req;
+    int64_t record;
+    uint64_t seq;
+};
+struct Deferred {
+    int64_t task_id, block_id;
+    uint64_t base, len;
+    std::vector<std::tuple<MsgP, uint64_t, uint64_t>> chunks;  // msg, iv, offset
+    bool done = false, landing = false;
+};
+struct Meta {
+    int kind;  // 0 data, 1 small_io, 2 nop
+    uint64_t seq;
+    int64_t block_id;  // INT64_MIN none
+    uint64_t base, offset, nbytes;
+};
+struct Lane {
+    std::deque<MsgP> queue;
+    std::vector<sp_sent> log;
+};
+struct Recorded {
+    uint64_t seq, addr, n;
+    View view;
+};
+
+constexpr int64_t NONE = INT64_MIN;
+
+std::vector<std::pair<uint64_t, uint64_t>> chunk_spans(uint64_t length, uint64_t chunk) {
+    std::vector<std::pair<uint64_t, uint64_t>> out;
+    for (uint64_t off = 0; off < length; off += chunk) out.push_back({off, std::min(chunk, length - off)});
+    return out;
+}
+
+class Engine {
+  public:
+    sp_pipe_config cfg;
+    Plane plane;  // destroyed last (fences/buffers below point into it)
+    HostMem mem;
+    Predictor *pred;
+    Validator val;
+    Lane lanes[2];
+    uint64_t send_iv[2], recv_iv[2];  // [H2D]: cpu send / gpu recv; [D2H]: gpu send / cpu recv
+    std::vector<sp_action> actions;
+    int64_t counters[C_COUNT] = {};
+    bool otf_burned_present = false;
+    uint64_t initial_send_iv;
+    std::deque<SpecTask> spec_queue;
+    std::vector<Suspended> suspended;
+    std::set<uint64_t> suspended_seqs;
+    std::vector<int64_t> batch_ins, predicted_queue;
+    std::map<int64_t, Deferred> deferred;
+    int64_t next_task_id = 1;
+    uint64_t next_seq = 0, next_label_iv = 0;
+    std::deque<Meta> h2d_meta;
+    std::unordered_map<int64_t, View> device_mem;
+    std::vector<Recorded> delivered, d2h_stream;
+    int64_t ring_occupied = 0, ring_high = 0, ring_insertions = 0, ring_violations = 0;
+
+    Engine(const sp_pipe_config &c, const uint8_t key[32], Predictor *p)
+        : cfg(c), plane(c.dry != 0, key, c.batch_bytes ? c.batch_bytes : (64ull << 20), c.reserve_bytes), pred(p),
+          val(mem, c.window) {
+        send_iv[H2D] = c.initial_h2d_iv;
+        send_iv[D2H] = c.initial_d2h_iv;
+        recv_iv[H2D] = c.initial_h2d_iv;
+        recv_iv[D2H] = c.initial_d2h_iv;
+        initial_send_iv = c.initial_h2d_iv;
+    }
+
+    // -- channel (channel.py:146-215) --
+    void send(int dir, const MsgP &m) {
+        lanes[dir].log.push_back({send_iv[dir], m->len, m->nop ? 1 : 0, 0});
+        lanes[dir].queue.push_back(m);
+        send_iv[dir] += 1;
+    }
+    bool pending(int dir) const { return !lanes[dir].queue.empty(); }
+    std::pair<MsgP, uint64_t> take(int dir) {
+        if (lanes[dir].queue.empty()) throw EngineErr("channel empty");
+        MsgP m = lanes[dir].queue.front();
+        lanes[dir].queue.pop_front();
+        return {m, recv_iv[dir]++};
+    }
+
+    uint64_t seq() { return ++next_seq; }
+    void act(int kind, int64_t iv = -1, uint64_t nbytes = 0, int64_t record = -1, int64_t task = -1, bool committed = false,
+             bool otf = false, int64_t count = 0, int64_t sq = -1) {
+        sp_action a{};
+        a.kind = kind;
+        a.flags = (committed ? 1 : 0) | (otf ? 2 : 0);
+        a.iv = iv;
+        a.nbytes = nbytes;
+        a.record_id = record;
+        a.task_id = task;
+        a.count = count;
+        a.seq = sq;
+        actions.push_back(a);
+    }
+
+    // -- deferred decrypts --
+    void resolve_decrypts_over(uint64_t base, uint64_t len, bool blocking) {
+        for (int64_t tid : mem.read_guards_over(base, len)) {
+            auto it = deferred.find(tid);
+            if (it != deferred.end()) apply_decrypt(tid, blocking);
+        }
+    }
+    void apply_decrypt(int64_t tid, bool blocking) {
+        auto it = deferred.find(tid);
+        if (it == deferred.end() || it->second.done) return;
+        Deferred &t = it->second;
+        if (!t.landing) land(t);
+        mem.release_read_guard(t.task_id);
+        t.done = true;
+        int64_t task_id = t.task_id;
+        uint64_t len = t.len;
+        deferred.erase(it);
+        if (blocking) {
+            counters[C_SYNC_DECRYPTS]++;
+            act(SP_ACT_RESOLVE_DECRYPT, -1, len, -1, task_id);
+        }
+    }
+    void land(Deferred &t) {
+        Block &b = mem.block(t.block_id);
+        uint64_t inner = t.base - b.base;
+        std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
+        for (auto &c : t.chunks) jobs.emplace_back(std::get<0>(c), std::get<1>(c), inner + std::get<2>(c));
+        plane.land_on_host(b, std::move(jobs), D2H);
+        t.landing = true;
+    }
+
+    View device_buffer(int64_t block_id) {
+        auto it = device_mem.find(block_id);
+        if (it != device_mem.end()) return it->second;
+        View v = plane.dry ? View{} : plane.new_device_buffer(mem.block(block_id).len);
+        device_mem[block_id] = v;
+        return v;
+    }
+
+    void drain_soon() {
+        if (cfg.strict_auth) drain_gpu();
+    }
+
+    // GPU endpoint receives everything queued on the H2D lane: one batched open.
+    void drain_gpu() {
+        std::vector<std::tuple<MsgP, uint64_t, View>> jobs;
+        while (pending(H2D)) {
+            auto mi = take(H2D);
+            Meta meta = h2d_meta.front();
+            h2d_meta.pop_front();
+            if (mi.first->nop) {
+                jobs.emplace_back(mi.first, mi.second, View{});
+                continue;
+            }
+            View dst;
+            if (meta.block_id != NONE) {
+                Block &b = mem.block(meta.block_id);
+                uint64_t inner = meta.base - b.base + meta.offset;
+                View whole = device_buffer(meta.block_id);
+                dst = View{whole.buf, whole.off + inner, meta.nbytes};
+            } else if (!plane.dry) {
+                dst = plane.new_device_buffer(meta.nbytes);
+            }
+            jobs.emplace_back(mi.first, mi.second, dst);
+            if (cfg.record_stream) delivered.push_back({meta.seq, meta.base + meta.offset, meta.nbytes, dst});
+        }
+        plane.open_into(jobs, H2D);
+        if (cfg.strict_auth) plane.check_auth();
+    }
+
+    void send_h2d(const MsgP &m, int64_t record, const Meta &meta, uint64_t sq) {
+        ring_insertions++;
+        if (record != NONE && val.rec(record).state != COMMITTED) ring_violations++;
+        ring_occupied++;
+        ring_high = std::max(ring_high, ring_occupied);
+        uint64_t iv = send_iv[H2D];
+        if (record == NONE && !cfg.reference_compat) {
+            int64_t claimed = val.pending_at_iv(iv);
+            if (claimed >= 0) {
+                val.invalidate(claimed);
+                counters[C_OTF_BURNED_RECORDS]++;
+                otf_burned_present = true;
+            }
+        }
+        send(H2D, m);
+        h2d_meta.push_back(meta);
+        ring_occupied--;
+        counters[C_DATA_MSGS]++;
+        act(SP_ACT_H2D_DATA, (int64_t)iv, m->len, record == NONE ? -1 : record, -1, record != NONE, record == NONE, 0,
+            (int64_t)sq);
+    }
+
+    // -- host-to-device (engine.py:295-349) --
+    int submit_h2d(const Req &r, uint64_t &sq) {
+        complete_spec_tasks();
+        sq = seq();
+        if (r.cls == TC_SMALL) {
+            counters[C_SMALL_IO_H2D]++;
+            send_on_the_fly(r, sq);
+            return V_NONE;
+        }
+        int64_t rid;
+        Verdict v = val.validate(r.base, r.len, send_iv[H2D], rid);
+        counters[C_HIT + v]++;
+        batch_ins.push_back(r.block_id);
+        if (v == V_HIT) {
+            commit_and_send(rid, sq);
+        } else if (v == V_AHEAD) {
+            counters[C_SUSPENDED]++;
+            suspended.push_back({r, rid, sq});
+            suspended_seqs.insert(sq);
+        } else {
+            if (v == V_BEHIND) relinquish();
+            send_on_the_fly(r, sq);
+        }
+        return v;
+    }
+
+    void send_on_the_fly(const Req &r, uint64_t sq) {
+        for (auto &t : spec_queue)
+            if (!t.cancelled && t.base == r.base && t.len == r.len) {
+                t.cancelled = true;
+                counters[C_SPEC_CANCELLED]++;
+            }
+        resolve_decrypts_over(r.base, r.len, true);
+        auto bi = mem.block_at(r.base, r.len);
+        auto spans = chunk_spans(r.len, cfg.chunk_bytes);
+        auto msgs = plane.seal_host_chunks(*bi.first, bi.second, spans, H2D, send_iv[H2D]);
+        for (size_t i = 0; i < spans.size(); ++i)
+            send_h2d(msgs[i], NONE, Meta{0, sq, r.block_id, r.base, spans[i].first, spans[i].second}, sq);
+        drain_soon();
+        counters[C_ON_THE_FLY]++;
+        suspended_seqs.erase(sq);
+    }
+
+    void commit_and_send(int64_t rid, uint64_t sq) {
+        Record &rec = val.rec(rid);
+        if (rec.iv != send_iv[H2D])
+            throw EngineErr("commit at counter " + std::to_string(send_iv[H2D]) + " for record at " + std::to_string(rec.iv));
+        val.commit(rid);
+        uint64_t off = 0;
+        std::vector<MsgP> chunks = val.rec(rid).chunks;
+        std::vector<uint64_t> lens = val.rec(rid).chunk_lens;
+        int64_t block_id = val.rec(rid).block_id;
+        uint64_t base = val.rec(rid).base;
+        for (size_t i = 0; i < lens.size(); ++i) {
+            MsgP m = plane.dry ? std::make_shared<Msg>() : chunks[i];
+            if (plane.dry) m->len = lens[i];
+            send_h2d(m, rid, Meta{0, sq, block_id, base, off, lens[i]}, sq);
+            off += lens[i];
+        }
+        val.rec(rid).chunks.clear();  // the lane now owns the payloads
+        drain_soon();
+        counters[C_COMMITTED_SENDS]++;
+        suspended_seqs.erase(sq);
+    }
+
+    // -- device-to-host (engine.py:353-393) --
+    uint64_t submit_d2h(const Req &r) {
+        complete_spec_tasks();
+        if (pending(H2D)) drain_gpu();
+        uint64_t sq = seq();
+        auto it = device_mem.find(r.block_id);
+        if (it == device_mem.end()) throw EngineErr("device does not hold block " + std::to_string(r.block_id));
+        View buf = it->second;
+        Block &b = mem.block(r.block_id);
+        uint64_t inner = r.base - b.base;
+        bool swap = r.cls == TC_WEIGHTS || r.cls == TC_KV;
+        auto spans = chunk_spans(r.len, cfg.chunk_bytes);
+        View src{buf.buf, buf.off + inner, r.len};
+        auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H]);
+        for (auto &m : msgs) send(D2H, m);
+        if (inner == 0 && r.len == b.len) device_mem.erase(r.block_id);
+        std::vector<std::tuple<MsgP, uint64_t, uint64_t>> taken;
+        for (auto &sp : spans) {
+            auto mi = take(D2H);
+            taken.emplace_back(mi.first, mi.second, sp.first);
+        }
+        if (swap && cfg.defer_swap_decrypt) {
+            int64_t tid = next_task_id++;
+            Deferred t;
+            t.task_id = tid;
+            t.block_id = r.block_id;
+            t.base = r.base;
+            t.len = r.len;
+            t.chunks = std::move(taken);
+            deferred[tid] = std::move(t);
+            mem.install_read_guard(r.base, r.len, tid);
+            land(deferred[tid]);
+            counters[C_DEFERRED_DECRYPTS]++;
+            act(SP_ACT_D2H_DATA, -1, r.len, -1, tid, false, false, 0, (int64_t)sq);
+        } else {
+            std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
+            for (auto &t : taken) jobs.emplace_back(std::get<0>(t), std::get<1>(t), inner + std::get<2>(t));
+            plane.land_on_host(b, std::move(jobs), D2H);
+            act(SP_ACT_D2H_DATA, -1, r.len, -1, -1, true, false, 0, (int64_t)sq);
+        }
+        if (swap) pred->observe_swap_out(r.block_id);
+        return sq;
+    }
+
+    // -- token-sized transfers (engine.py:397-416) --
+    void small_io(int dir, const uint8_t *payload, uint64_t size) {
+        complete_spec_tasks();
+        uint64_t sq = seq();
+        if (dir == H2D) {
+            counters[C_SMALL_IO_H2D]++;
+            auto msgs = plane.seal_bytes({{payload, size}}, H2D, send_iv[H2D], false);
+            send_h2d(msgs[0], NONE, Meta{1, sq, NONE, 0, 0, size}, sq);
+            drain_soon();
+        } else {
+            counters[C_SMALL_IO_D2H]++;
+            auto msgs = plane.seal_bytes({{payload, size}}, D2H, send_iv[D2H], false);
+            send(D2H, msgs[0]);
+            auto mi = take(D2H);
+            View dst = plane.dry ? View{} : plane.new_device_buffer(size);
+            std::vector<std::tuple<MsgP, uint64_t, View>> jobs{{mi.first, mi.second, dst}};
+            plane.open_into(jobs, D2H);
+            if (cfg.record_stream) d2h_stream.push_back({sq, 0, size, dst});
+            counters[C_SYNC_DECRYPTS]++;
+            act(SP_ACT_D2H_DATA, -1, size, -1, -1, true, false, 0, (int64_t)sq);
+        }
+    }
+
+    // -- application access (engine.py:420-440) --
+    int64_t app_write(int64_t block_id, uint64_t offset, const uint8_t *data, uint64_t n) {
+        complete_spec_tasks();
+        Block &b = mem.block(block_id);
+        resolve_decrypts_over(b.base + offset, n, true);
+        plane.before_host_write(block_id);
+        if (offset + n > b.len)
+            throw BoundsErr("access (" + std::to_string(offset) + ", " + std::to_string(n) + ") outside block " +
+                            std::to_string(b.id) + " of " + std::to_string(b.len) + " bytes");
+        uint64_t base = b.base + offset;
+        std::vector<int64_t> owners;
+        for (auto &kv : mem.write_guards)
+            if (kv.second.active && HostMem::overlaps(base, n, kv.second.base, kv.second.len)) owners.push_back(kv.first);
+        for (int64_t o : owners) {
+            mem.write_guards.erase(o);
+            val.on_write_fault(o);
+        }
+        if (b.host) memcpy(b.host + offset, data, n);
+        counters[C_WRITE_FAULTS] += (int64_t)owners.size();
+        return (int64_t)owners.size();
+    }
+
+    void app_read(int64_t block_id, uint64_t offset, uint64_t n, uint8_t *out) {
+        complete_spec_tasks();
+        plane.host_sync(block_id);
+        Block &b = mem.block(block_id);
+        if (offset + n > b.len)
+            throw BoundsErr("access (" + std::to_string(offset) + ", " + std::to_string(n) + ") outside block " +
+                            std::to_string(b.id) + " of " + std::to_string(b.len) + " bytes");
+        auto faults = mem.read_guards_over(b.base + offset, n);
+        if (!faults.empty()) {
+            counters[C_READ_FAULTS] += (int64_t)faults.size();
+            for (int64_t tid : faults)
+                if (deferred.count(tid)) apply_decrypt(tid, true);
+            plane.host_sync(block_id);
+        }
+        if (b.host) memcpy(out, b.host + offset, n);
+    }
+
+    // -- pipeline control (engine.py:442-535) --
+    void speculate_tick() {
+        complete_spec_tasks();
+        if (!cfg.speculate) return;
+        auto flat = pred->predict_batches(send_iv[H2D], cfg.leeway, (int)cfg.depth);
+        predicted_queue.clear();
+        for (auto &p : flat) predicted_queue.push_back(p.block);
+        std::vector<int64_t> planned;
+        {
+            std::vector<std::pair<uint64_t, int64_t>> recs;
+            for (int64_t id : val.order) recs.push_back({val.rec(id).iv, id});
+            std::stable_sort(recs.begin(), recs.end(),
+                             [](const std::pair<uint64_t, int64_t> &a, const std::pair<uint64_t, int64_t> &b) {
+                                 return a.first < b.first;
+                             });
+            for (auto &r : recs) planned.push_back(val.rec(r.second).block_id);
+            for (auto &t : spec_queue)
+                if (!t.cancelled) planned.push_back(t.block_id);
+        }
+        bool diverged = false;
+        for (size_t i = 0; i < std::min(planned.size(), flat.size()); ++i)
+            if (planned[i] != flat[i].block) {
+                diverged = true;
+                break;
+            }
+        if (diverged) {
+            int64_t n = discard_pipeline();
+            counters[C_REPLANS]++;
+            counters[C_REPLANNED_RECORDS] += n;
+            act(SP_ACT_RELINQUISH, -1, 0, -1, -1, false, false, n);
+        }
+        int64_t room = (int64_t)cfg.window - (int64_t)val.order.size() - (int64_t)spec_queue.size();
+        std::unordered_set<int64_t> queued;
+        for (auto &t : spec_queue)
+            if (!t.cancelled) queued.insert(t.block_id);
+        for (auto &p : flat) {
+            if (room <= 0) break;
+            Block &b = mem.block(p.block);
+            if (queued.count(p.block) || val.has_pending_range(b.base, b.len)) continue;
+            uint64_t iv = std::max<uint64_t>(p.iv, next_label_iv);
+            next_label_iv = iv + chunk_spans(b.len, cfg.chunk_bytes).size();
+            spec_queue.push_back(SpecTask{p.block, b.base, b.len, iv, false});
+            queued.insert(p.block);
+            --room;
+        }
+    }
+
+    void complete_spec_tasks() {
+        if (spec_queue.empty()) return;
+        Plane::SpecBatch batch(&plane);
+        try {
+            label_spec_tasks(batch);
+        } catch (...) {
+            batch.launch();
+            throw;
+        }
+        batch.launch();
+    }
+
+    void label_spec_tasks(Plane::SpecBatch &batch) {
+        while (!spec_queue.empty()) {
+            SpecTask t = spec_queue.front();
+            spec_queue.pop_front();
+            if (t.cancelled || !pred->is_outstanding(t.block_id) || val.has_pending_range(t.base, t.len)) {
+                counters[C_SPEC_SKIPPED]++;
+                continue;
+            }
+            resolve_decrypts_over(t.base, t.len, false);
+            Block &b = mem.block(t.block_id);
+            auto spans = chunk_spans(t.len, cfg.chunk_bytes);
+            auto msgs = batch.add(b, t.base - b.base, spans, H2D, t.iv);
+            std::vector<uint64_t> lens;
+            for (auto &sp : spans) lens.push_back(sp.second);
+            int64_t rid = val.label(plane.dry ? std::vector<MsgP>() : msgs, lens, t.base, t.len, t.iv, t.block_id);
+            counters[C_SPEC_ENCRYPTS]++;
+            act(SP_ACT_SPEC_ENCRYPT, (int64_t)t.iv, t.len, rid);
+        }
+    }
+
+    int64_t discard_pipeline() {
+        int64_t n = 0;
+        for (int64_t id : val.pending_ids()) {
+            val.invalidate(id);
+            ++n;
+        }
+        for (auto &t : spec_queue)
+            if (!t.cancelled) {
+                t.cancelled = true;
+                counters[C_SPEC_CANCELLED]++;
+            }
+        next_label_iv = 0;
+        return n;
+    }
+
+    int64_t relinquish() {
+        int64_t n = discard_pipeline();
+        counters[C_RELINQUISHES]++;
+        counters[C_RELINQUISHED_RECORDS] += n;
+        act(SP_ACT_RELINQUISH, -1, 0, -1, -1, false, false, n);
+        return n;
+    }
+
+    void pad_to(uint64_t target, int64_t keep_id) {
+        if (target <= send_iv[H2D]) return;
+        uint64_t gap = target - send_iv[H2D];
+        std::vector<std::pair<const uint8_t *, uint64_t>> pads(gap, {nullptr, (uint64_t)cfg.nop_bytes});
+        auto msgs = plane.seal_bytes(pads, H2D, send_iv[H2D], true);
+        for (auto &m : msgs) {
+            int64_t burned = val.pending_at_iv(send_iv[H2D]);
+            if (burned >= 0 && burned != keep_id) {
+                val.invalidate(burned);
+                counters[C_NOP_BURNED_RECORDS]++;
+            }
+            uint64_t iv = send_iv[H2D];
+            send(H2D, m);
+            h2d_meta.push_back(Meta{2, 0, NONE, 0, 0, cfg.nop_bytes});
+            counters[C_NOPS]++;
+            act(SP_ACT_NOP, (int64_t)iv, cfg.nop_bytes);
+        }
+        drain_soon();
+    }
+
+    // -- batch boundary (engine.py:537-577) --
+    void sync() {
+        complete_spec_tasks();
+        std::vector<Suspended> susp(suspended);
+        std::stable_sort(susp.begin(), susp.end(),
+                         [this](const Suspended &a, const Suspended &b) { return val.rec(a.record).iv < val.rec(b.record).iv; });
+        for (auto &s : susp) {
+            if (val.rec(s.record).state != PENDING) {
+                counters[C_SUSPENDED_FALLBACK]++;
+                send_on_the_fly(s.req, s.seq);
+                continue;
+            }
+            pad_to(val.rec(s.record).iv, s.record);
+            commit_and_send(s.record, s.seq);
+        }
+        suspended.clear();
+        if (pending(H2D)) drain_gpu();
+        counters[C_EXPIRED_RECORDS] += val.invalidate_pending_below(send_iv[H2D]);
+        drain_decrypts();
+        plane.flush();
+        if (!batch_ins.empty()) {
+            std::vector<int64_t> batch(batch_ins);
+            batch_ins.clear();
+            counters[C_SEQ_BATCHES]++;
+            size_t k = batch.size();
+            bool hit = false;
+            if (predicted_queue.size() >= k) {
+                std::set<int64_t> a(predicted_queue.begin(), predicted_queue.begin() + (long)k), b(batch.begin(), batch.end());
+                hit = a == b;
+            }
+            if (hit) {
+                counters[C_SEQ_HITS]++;
+                predicted_queue.erase(predicted_queue.begin(), predicted_queue.begin() + (long)k);
+            } else {
+                predicted_queue.clear();
+            }
+            pred->observe_swap_in(batch);
+        }
+        pred->observe_sync();
+        act(SP_ACT_SYNC_POINT);
+        counters[C_SYNCS]++;
+        speculate_tick();
+    }
+
+    void drain_decrypts() {
+        std::vector<int64_t> ids;
+        for (auto &kv : deferred) ids.push_back(kv.first);
+        for (int64_t id : ids) apply_decrypt(id, false);
+    }
+
+    void finish() {
+        if (!suspended.empty() || !batch_ins.empty()) sync();
+        drain_decrypts();
+        for (int64_t id : val.pending_ids()) {
+            val.invalidate(id);
+            counters[C_FINAL_DISCARDED]++;
+        }
+        spec_queue.clear();
+        if (pending(H2D)) drain_gpu();
+        plane.finish();
+        audit();
+    }
+
+    void audit() {
+        uint64_t expect = initial_send_iv + (uint64_t)counters[C_DATA_MSGS] + (uint64_t)counters[C_NOPS];
+        if (send_iv[H2D] != expect)
+            throw EngineErr("counter ledger violated: send counter " + std::to_string(send_iv[H2D]) + ", expected " +
+                            std::to_string(expect));
+        if (ring_violations)
+            throw EngineErr(std::to_string(ring_violations) + " uncommitted payloads reached the shared ring");
+    }
+
+    void seed_device(int64_t block_id, const void *src, uint64_t n, bool src_dev) {
+        if (plane.dry) {
+            device_mem[block_id] = View{};
+            return;
+        }
+        View v = plane.new_device_buffer(n);
+        ck(cudaMemcpyAsync(v.ptr(), src, n, src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, plane.s.comp),
+           "seed_device copy");
+        ck(cudaStreamSynchronize(plane.s.comp), "seed_device sync");
+        device_mem[block_id] = v;
+    }
+
+    // Replay driver (simulator.py:404-426 dispatch, workload event kinds).
+    void replay(const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
+        for (uint64_t k = 0; k < n; ++k) {
+            const sp_event &e = ev[k];
+            uint64_t sq;
+            switch (e.kind) {
+                case SP_EV_SWAP_IN: submit_h2d(Req{H2D, e.base, e.len, e.cls, e.block}, sq); break;
+                case SP_EV_SWAP_OUT: submit_d2h(Req{D2H, e.base, e.len, e.cls, e.block}); break;
+                case SP_EV_SMALL_IO_H2D: small_io(H2D, payloads ? payloads + e.payload : nullptr, e.len); break;
+                case SP_EV_SMALL_IO_D2H: small_io(D2H, payloads ? payloads + e.payload : nullptr, e.len); break;
+                case SP_EV_SYNC: sync(); break;
+                case SP_EV_APP_WRITE: app_write(e.block, e.base, payloads + e.payload, e.len); break;
+                default: break;
+            }
+            if (done) *done = k + 1;
+        }
+    }
+};
+
+}  // namespace sppipe
+
+using namespace sppipe;
+
+struct sp_pred {
+    Predictor p;
+    explicit sp_pred(const PredConfig &c) : p(c) {}
+};
+struct sp_pipe {
+    std::unique_ptr<Engine> e;
+};
+
+namespace {
+
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return SP_OK;
+    } catch (const EngineErr &x) {
+        g_err = x.what();
+        return SP_EENGINE;
+    } catch (const OverlapErr &x) {
+        g_err = x.what();
+        return SP_EOVERLAP;
+    } catch (const StateErr &x) {
+        g_err = x.what();
+        return SP_ESTATE;
+    } catch (const UnknownBlockErr &x) {
+        g_err = x.what();
+        return SP_EUNKNOWN_BLOCK;
+    } catch (const BoundsErr &x) {
+        g_err = x.what();
+        return SP_EBOUNDS;
+    } catch (const GuardErr &x) {
+        g_err = x.what();
+        return SP_EGUARD;
+    } catch (const AmbiguousProfileErr &x) {
+        g_err = x.what();
+        return SP_EAMBIGUOUS;
+    } catch (const KeyErr &x) {
+        g_err = x.what();
+        return SP_EKEY;
+    } catch (const AuthErr &x) {
+        g_err = x.what();
+        return SP_EAUTH;
+    } catch (const ValueErr &x) {
+        g_err = x.what();
+        return SP_EINVAL;
+    } catch (const CudaErr &x) {
+        g_err = x.what();
+        return SP_ECUDA;
+    } catch (const std::exception &x) {
+        g_err = x.what();
+        return SP_ECUDA;
+    }
+}
+
+PredConfig to_pred_config(const sp_pred_config *c) {
+    PredConfig pc;
+    if (c) {
+        pc.small_io_threshold = c->small_io_threshold;
+        pc.swap_min = c->swap_min;
+        pc.chunk_bytes = c->chunk_bytes;
+        pc.warmup_matches = c->warmup_matches;
+        pc.history_cap = c->history_cap;
+        pc.layer_param_bytes = c->layer_param_bytes;
+        pc.kv_block_bytes = c->kv_block_bytes;
+    }
+    return pc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sp_pipe_last_error(void) { return g_err.c_str(); }
+
+// ---- predictor ---------------------------------------------------------------------------
+int sp_pred_create(const sp_pred_config *cfg, sp_pred **out) {
+    if (!out) return SP_EINVAL;
+    return guarded([&] { *out = new sp_pred(to_pred_config(cfg)); });
+}
+void sp_pred_destroy(sp_pred *p) { delete p; }
+int sp_pred_classify(sp_pred *p, uint64_t size, int32_t *cls) {
+    return guarded([&] { *cls = (int32_t)p->p.classify_size(size); });
+}
+int sp_pred_observe_out(sp_pred *p, int64_t block) {
+    return guarded([&] { p->p.observe_swap_out(block); });
+}
+int sp_pred_observe_in(sp_pred *p, const int64_t *blocks, int32_t n) {
+    return guarded([&] { p->p.observe_swap_in(std::vector<int64_t>(blocks, blocks + (n > 0 ? n : 0))); });
+}
+int sp_pred_observe_sync(sp_pred *p) {
+    return guarded([&] { p->p.observe_sync(); });
+}
+int sp_pred_recognize(sp_pred *p, int32_t *kind, int64_t *confidence, int64_t *phase, int64_t *cycle_len) {
+    return guarded([&] {
+        Hypothesis h = p->p.recognize();
+        *kind = h.kind;
+        *confidence = h.confidence;
+        *phase = h.phase;
+        *cycle_len = (int64_t)h.cycle.size();
+    });
+}
+int sp_pred_cycle_entry(sp_pred *p, int64_t i, int64_t *blocks, int32_t cap, int32_t *n) {
+    return guarded([&] {
+        Hypothesis h = p->p.recognize();
+        if (i < 0 || i >= (int64_t)h.cycle.size()) throw KeyErr("cycle entry " + std::to_string(i));
+        const auto &b = p->p.batch_of(h.cycle[(size_t)i]);
+        *n = (int32_t)b.size();
+        for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k) blocks[k] = b[(size_t)k];
+    });
+}
+int sp_pred_predict_batches(sp_pred *p, uint64_t current_iv, uint64_t leeway, int32_t depth, sp_prediction *out,
+                            int32_t cap, int32_t *n) {
+    return guarded([&] {
+        auto v = p->p.predict_batches(current_iv, leeway, depth);
+        *n = (int32_t)v.size();
+        for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k)
+            out[k] = sp_prediction{v[(size_t)k].block, v[(size_t)k].iv, v[(size_t)k].leeway, v[(size_t)k].batch, 0};
+    });
+}
+int sp_pred_outstanding(sp_pred *p, int64_t *out, int64_t cap, int64_t *n) {
+    return guarded([&] {
+        const auto &v = p->p.outstanding_in_order();
+        *n = (int64_t)v.size();
+        for (int64_t k = 0; k < std::min<int64_t>(cap, *n); ++k) out[k] = v[(size_t)k];
+    });
+}
+int64_t sp_pred_in_batch_count(sp_pred *p) { return (int64_t)p->p.in_batch_count(); }
+int64_t sp_pred_decision_count(sp_pred *p) { return (int64_t)p->p.decision_log.size(); }
+int sp_pred_decision(sp_pred *p, int64_t i, sp_decision *out) {
+    if (i < 0 || i >= (int64_t)p->p.decision_log.size()) return SP_EKEY;
+    const Decision &d = p->p.decision_log[(size_t)i];
+    *out = sp_decision{d.event, d.pattern, d.confidence, d.after_batches};
+    return SP_OK;
+}
+
+// ---- pipe ----------------------------------------------------------------------------------
+int sp_pipe_create(const sp_pipe_config *cfg, const uint8_t key[SP_KEY_BYTES], sp_pred *pred, sp_pipe **out) {
+    if (!cfg || !key || !pred || !out) {
+        g_err = "null argument";
+        return SP_EINVAL;
+    }
+    return guarded([&] {
+        auto p = new sp_pipe();
+        try {
+            p->e.reset(new Engine(*cfg, key, &pred->p));
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+void sp_pipe_destroy(sp_pipe *p) { delete p; }
+
+int sp_pipe_register_block(sp_pipe *p, int64_t id, uint64_t base, uint64_t len, int32_t kind, void *host) {
+    return guarded([&] {
+        auto &m = p->e->mem;
+        m.blocks[id] = Block{id, base, len, kind, static_cast<uint8_t *>(host)};
+        m.by_base[base] = id;
+    });
+}
+int sp_pipe_seed_device(sp_pipe *p, int64_t block, const void *src, uint64_t len, int32_t src_is_device) {
+    return guarded([&] { p->e->seed_device(block, src, len, src_is_device != 0); });
+}
+int sp_pipe_submit_h2d(sp_pipe *p, uint64_t base, uint64_t len, int32_t cls, int64_t block, uint64_t *seq,
+                       int32_t *verdict) {
+    return guarded([&] {
+        uint64_t sq = 0;
+        int v = p->e->submit_h2d(Req{H2D, base, len, cls, block}, sq);
+        if (seq) *seq = sq;
+        if (verdict) *verdict = v;
+    });
+}
+int sp_pipe_submit_d2h(sp_pipe *p, uint64_t base, uint64_t len, int32_t cls, int64_t block, uint64_t *seq) {
+    return guarded([&] {
+        uint64_t sq = p->e->submit_d2h(Req{D2H, base, len, cls, block});
+        if (seq) *seq = sq;
+    });
+}
+int sp_pipe_small_io(sp_pipe *p, int32_t dir, const void *payload, uint64_t size) {
+    if (dir != H2D && dir != D2H) {
+        g_err = "unknown direction";
+        return SP_EINVAL;
+    }
+    return guarded([&] { p->e->small_io(dir, static_cast<const uint8_t *>(payload), size); });
+}
+int sp_pipe_sync(sp_pipe *p) {
+    return guarded([&] { p->e->sync(); });
+}
+int sp_pipe_speculate(sp_pipe *p) {
+    return guarded([&] { p->e->speculate_tick(); });
+}
+int sp_pipe_relinquish(sp_pipe *p, int64_t *count) {
+    return guarded([&] {
+        int64_t n = p->e->relinquish();
+        if (count) *count = n;
+    });
+}
+int sp_pipe_drain_decrypts(sp_pipe *p) {
+    return guarded([&] { p->e->drain_decrypts(); });
+}
+int sp_pipe_finish(sp_pipe *p) {
+    return guarded([&] { p->e->finish(); });
+}
+int sp_pipe_flush(sp_pipe *p, int32_t wait) {
+    return guarded([&] {
+        if (p->e->plane.dry) return;
+        if (wait) p->e->plane.finish_streams();
+        else p->e->plane.flush();
+    });
+}
+int sp_pipe_app_write(sp_pipe *p, int64_t block, uint64_t offset, const void *data, uint64_t n, int64_t *faults) {
+    return guarded([&] {
+        int64_t f = p->e->app_write(block, offset, static_cast<const uint8_t *>(data), n);
+        if (faults) *faults = f;
+    });
+}
+int sp_pipe_app_read(sp_pipe *p, int64_t block, uint64_t offset, uint64_t n, void *out) {
+    return guarded([&] { p->e->app_read(block, offset, n, static_cast<uint8_t *>(out)); });
+}
+int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
+    if (done) *done = 0;
+    return guarded([&] { p->e->replay(ev, n, payloads, done); });
+}
+int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done) {
+    *done = (seq >= 1 && seq <= p->e->next_seq && !p->e->suspended_seqs.count(seq)) ? 1 : 0;
+    return SP_OK;
+}
+
+int sp_pipe_report(sp_pipe *p, int64_t *out, int32_t cap, int32_t *n) {
+    Engine &e = *p->e;
+    int64_t v[kReportCount];
+    for (int i = 0; i < C_COUNT; ++i) v[i] = e.counters[i];
+    v[C_COUNT + 0] = e.ring_violations;
+    v[C_COUNT + 1] = e.ring_high;
+    v[C_COUNT + 2] = (int64_t)e.send_iv[H2D];
+    v[C_COUNT + 3] = (int64_t)e.send_iv[D2H];
+    v[C_COUNT + 4] = e.otf_burned_present ? 1 : 0;
+    *n = kReportCount;
+    for (int i = 0; i < std::min<int32_t>(cap, kReportCount); ++i) out[i] = v[i];
+    return SP_OK;
+}
+const char *sp_pipe_counter_name(int32_t i) {
+    if (i < 0 || i >= kReportCount) return nullptr;
+    return kCounterNames[i];
+}
+uint64_t sp_pipe_send_iv(sp_pipe *p, int32_t dir) { return p->e->send_iv[dir & 1]; }
+uint64_t sp_pipe_recv_iv(sp_pipe *p, int32_t dir) { return p->e->recv_iv[dir & 1]; }
+int64_t sp_pipe_action_count(sp_pipe *p) { return (int64_t)p->e->actions.size(); }
+int sp_pipe_actions(sp_pipe *p, int64_t from, sp_action *out, int64_t cap, int64_t *n) {
+    auto &a = p->e->actions;
+    int64_t k = 0;
+    for (int64_t i = from; i < (int64_t)a.size() && k < cap; ++i) out[k++] = a[(size_t)i];
+    *n = k;
+    return SP_OK;
+}
+int64_t sp_pipe_sent_count(sp_pipe *p, int32_t dir) { return (int64_t)p->e->lanes[dir & 1].log.size(); }
+int sp_pipe_sent_log(sp_pipe *p, int32_t dir, int64_t from, sp_sent *out, int64_t cap, int64_t *n) {
+    auto &l = p->e->lanes[dir & 1].log;
+    int64_t k = 0;
+    for (int64_t i = from; i < (int64_t)l.size() && k < cap; ++i) out[k++] = l[(size_t)i];
+    *n = k;
+    return SP_OK;
+}
+int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which) {
+    return (int64_t)(which ? p->e->d2h_stream.size() : p->e->delivered.size());
+}
+int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, void *bytes) {
+    auto &v = which ? p->e->d2h_stream : p->e->delivered;
+    if (i < 0 || i >= (int64_t)v.size()) return SP_EKEY;
+    const Recorded &r = v[(size_t)i];
+    *out = sp_delivery{r.seq, r.addr, r.n};
+    if (!bytes) return SP_OK;
+    return guarded([&] {
+        if (p->e->plane.dry || !r.view.buf) throw ValueErr("the dry plane holds no bytes");
+        if (p->e->pending(H2D)) p->e->drain_gpu();
+        p->e->plane.copy_to_host(r.view, bytes);
+    });
+}
+int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches) {
+    if (bytes_h2d) *bytes_h2d = p->e->plane.bytes_h2d;
+    if (bytes_d2h) *bytes_d2h = p->e->plane.bytes_d2h;
+    if (launches) *launches = p->e->plane.launches;
+    return SP_OK;
+}
+
+}  // extern "C"

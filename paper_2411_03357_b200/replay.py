@@ -41,6 +41,12 @@ class ReplayConfig:
     # seeding 4 GB at CPU speed would dominate setup time)
     fill: str = "seeded"
     reference_compat: bool = True
+    # "python": engine.Engine over devplane.GpuPlane; "native": libsppipe
+    # (native_engine.NativeEngine), dispatching the whole trace in one
+    # sp_pipe_replay call unless `native_dispatch` is "python" (per event)
+    engine: str = "python"
+    native_dispatch: str = "replay"
+    reserve_bytes: int = 0
 
 
 @dataclass
@@ -80,12 +86,20 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
     cpu, gpu = new_channel(seed=config.seed)
     pconf = PredictorConfig() if config.predictor_chunk_bytes is None else \
         PredictorConfig(chunk_bytes=config.predictor_chunk_bytes)
-    predictor = Predictor(header.profile, pconf)
+    native = config.engine == "native"
     spec_on = config.system == "specpipe"
-    engine = Engine(memory, cpu, gpu, predictor, EngineConfig(
+    econf = EngineConfig(
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
-        record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat))
+        record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat)
+    if native:
+        from .native_engine import NativeEngine, NativePredictor
+
+        predictor = NativePredictor(header.profile, pconf)
+        engine = NativeEngine(memory, cpu, gpu, predictor, econf, reserve_bytes=config.reserve_bytes)
+    else:
+        predictor = Predictor(header.profile, pconf)
+        engine = Engine(memory, cpu, gpu, predictor, econf)
     blocks = {}
     for spec in header.blocks:
         if spec.resident == "cpu":
@@ -95,7 +109,7 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
         else:
             block = memory.block(spec.id) if reuse else memory.alloc(spec.kind, spec.nbytes)
             if config.plane == "gpu":
-                dev = engine.plane.new_device_buffer(spec.nbytes)
+                dev = _device_bytes(spec.nbytes) if native else engine.plane.new_device_buffer(spec.nbytes)
                 if config.fill == "fast":
                     _fast_random(dev, spec.content_seed)
                 else:
@@ -104,9 +118,58 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
                     dev.copy_(torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)))
                 engine.seed_device(block.id, dev)
             else:
-                engine.seed_device(block.id, engine.plane.new_device_buffer(spec.nbytes))
+                from .devplane import _DryPayload
+
+                engine.seed_device(block.id, _DryPayload(spec.nbytes) if native else
+                                   engine.plane.new_device_buffer(spec.nbytes))
         blocks[spec.id] = (block, classify(spec.nbytes, header.profile, pconf))
     return engine, blocks
+
+
+def _device_bytes(n: int):
+    import torch
+
+    return torch.empty(n, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def _drain(engine, config: ReplayConfig) -> None:
+    """Issue and finish all device work queued so far (clock boundaries)."""
+    if config.plane != "gpu":
+        return
+    if config.engine == "native":
+        engine.flush(wait=True)
+    else:
+        engine.plane.finish()
+
+
+_EV_CODES = {"h2d": 2, "d2h": 3}
+
+
+def encode_events(trace: Trace, blocks: dict, config: ReplayConfig, start: int = 0, stop: int | None = None):
+    """Trace events -> sp_event tuples + payload bytes (small I/O and app
+    writes, generated exactly as the per-event driver does)."""
+    from .native_engine import _CLASS
+
+    events, payload = [], bytearray()
+    io_index = sum(1 for e in trace.events[:start] if isinstance(e, SmallIoEvent))
+    for ev in trace.events[start:stop]:
+        if isinstance(ev, SwapInRequest):
+            block, cls = blocks[ev.block]
+            events.append((0, _CLASS[cls], block.id, block.base, block.len, 0))
+        elif isinstance(ev, SwapOut):
+            block, cls = blocks[ev.block]
+            events.append((1, _CLASS[cls], block.id, block.base, block.len, 0))
+        elif isinstance(ev, SmallIoEvent):
+            events.append((_EV_CODES[ev.direction], 2, 0, 0, ev.size, len(payload)))
+            payload += small_io_payload(config.seed, io_index, ev.size)
+            io_index += 1
+        elif isinstance(ev, SyncEvent):
+            events.append((4, 0, 0, 0, 0, 0))
+        elif isinstance(ev, AppWriteEvent):
+            block, _ = blocks[ev.block]
+            events.append((5, 0, block.id, ev.offset, ev.size, len(payload)))
+            payload += app_write_payload(ev.data_seed, ev.size)
+    return events, bytes(payload)
 
 
 def _fast_random(dev_tensor, seed: int) -> None:
@@ -153,17 +216,18 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
     the clock starts (after draining the GPU) at that event index and
     `swap_bytes` counts only the swaps from there on (warm-up excluded)."""
     engine, blocks = build_engine(trace, config, memory)
-    if config.plane == "gpu":
-        engine.plane.finish()
+    _drain(engine, config)
     mark = {"t0": time.perf_counter()}
 
     def at_mark() -> None:
-        if config.plane == "gpu":
-            engine.plane.finish()
+        _drain(engine, config)
         mark["t0"] = time.perf_counter()
 
     try:
-        _dispatch_all(engine, blocks, trace, config, measure_from, at_mark)
+        if config.engine == "native" and config.native_dispatch == "replay":
+            _replay_native(engine, blocks, trace, config, measure_from, at_mark)
+        else:
+            _dispatch_all(engine, blocks, trace, config, measure_from, at_mark)
     except Exception as exc:
         if not catch:
             raise
@@ -171,6 +235,19 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
                             f"{type(exc).__name__}: {exc}")
     wall = time.perf_counter() - mark["t0"]
     return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
+
+
+def _replay_native(engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,
+                   at_mark=None) -> None:
+    """The whole trace through sp_pipe_replay (one native call per segment)."""
+    cut = measure_from if measure_from and at_mark is not None else 0
+    if cut:
+        events, payload = encode_events(trace, blocks, config, 0, cut)
+        engine.replay_events(events, payload)
+        at_mark()
+    events, payload = encode_events(trace, blocks, config, cut)
+    engine.replay_events(events, payload)
+    engine.finish()
 
 
 def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,

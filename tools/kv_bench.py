@@ -14,6 +14,11 @@ for pol in ("lifo", "fifo"):
         if plane == "gpu":
             run_engine(tr, ReplayConfig(plane="gpu", reference_compat=False, fill="fast"))
             enc = run_engine(tr, ReplayConfig(plane="gpu", reference_compat=False, fill="fast"))
-            pl = run_plain(tr, fill="fast")
-            line += f" | enc {enc.wall_s*1e3:.1f} ms ({enc.swap_gbs:.2f} GB/s) plain {pl.wall_s*1e3:.1f} ms ({pl.swap_gbs:.2f} GB/s)"
+            ncfg = ReplayConfig(plane="gpu", reference_compat=False, fill="fast", engine="native")
+            run_engine(tr, ncfg)
+            nat = min((run_engine(tr, ncfg) for _ in range(3)), key=lambda r: r.wall_s)
+            run_plain(tr, fill="fast")
+            pl = min((run_plain(tr, fill="fast") for _ in range(3)), key=lambda r: r.wall_s)
+            line += (f" | py-engine {enc.wall_s*1e3:.1f} ms ({enc.swap_gbs:.2f} GB/s) native {nat.wall_s*1e3:.1f} ms "
+                     f"({nat.swap_gbs:.2f} GB/s) plain {pl.wall_s*1e3:.1f} ms ({pl.swap_gbs:.2f} GB/s)")
         print(line, flush=True)

@@ -31,7 +31,8 @@ def main() -> None:
     t = time.perf_counter()
     memory = prepare_memory(tr, cfg)
     print(f"prepare_memory {time.perf_counter() - t:.2f}s", flush=True)
-    res = {"plain": [], "enc": [], "enc_host_s": []}
+    ncfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=0, engine="native")
+    res = {"plain": [], "enc": [], "enc_host_s": [], "native": [], "native_host_s": []}
     for _ in range(args.reps):
         r = run_plain(tr, fill="fast", memory=memory)
         res["plain"].append(round(r.swap_gbs, 2))
@@ -41,9 +42,16 @@ def main() -> None:
         res["enc"].append(round(r.swap_gbs, 2))
         rep = r.engine.report()
         del r
+        c0 = time.process_time()
+        r = run_engine(tr, ncfg, memory=memory)
+        res["native_host_s"].append(round(time.process_time() - c0, 3))
+        res["native"].append(round(r.swap_gbs, 2))
+        assert r.engine.report() == rep
+        del r
         if args.empty_cache:
             torch.cuda.empty_cache()
-        print(res["plain"][-1], res["enc"][-1], res["enc_host_s"][-1], flush=True)
+        print(res["plain"][-1], res["enc"][-1], res["enc_host_s"][-1], res["native"][-1], res["native_host_s"][-1],
+              flush=True)
     res["report"] = {k: rep[k] for k in ("hit", "iv_ahead", "nops", "miss") if k in rep}
     print(json.dumps(res), flush=True)
     if args.no_trace:
@@ -55,6 +63,10 @@ def main() -> None:
     print("profiled enc run GB/s", round(r.swap_gbs, 2), flush=True)
     os.makedirs(os.path.dirname(args.trace_out), exist_ok=True)
     prof.export_chrome_trace(args.trace_out)
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+        r = run_engine(tr, ncfg, memory=memory)
+    print("profiled native run GB/s", round(r.swap_gbs, 2), flush=True)
+    prof.export_chrome_trace(args.trace_out.replace(".json", "_native.json"))
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         r = run_plain(tr, fill="fast", memory=memory)
     print("profiled plain run GB/s", round(r.swap_gbs, 2), flush=True)
