@@ -62,7 +62,7 @@ typedef void *sp_stream_t;
  * src/dst take the vectorised path. */
 typedef struct sp_desc {
     uint32_t dir;       /* SP_DIR_H2D or SP_DIR_D2H */
-    uint32_t reserved;
+    uint32_t reserved;  /* sp_crypt_batch only: SP_OP_SEAL or SP_OP_OPEN; ignored elsewhere */
     uint64_t iv;        /* 64-bit channel counter, any value in [0, 2^64) */
     uint64_t len;       /* 1 .. SP_MAX_MESSAGE_BYTES */
     const void *src;
@@ -91,6 +91,12 @@ int sp_open(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len,
  * (engine.py:579-581).  Stream-ordered. */
 int sp_seal_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
 int sp_open_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
+/* Seals and opens mixed in ONE launch (desc.reserved picks the operation):
+ * the pipeline's independent NOP/on-the-fly/swap-out seals and receiver
+ * opens of one flush.  Messages of one call must not overlap in memory. */
+#define SP_OP_SEAL 0u
+#define SP_OP_OPEN 1u
+int sp_crypt_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
 
 /* Host-buffer entry points: the exact call shape of encrypt_at / decrypt_at
  * (bytes in, bytes out).  H2D copies, kernels and D2H copies are pipelined

@@ -20,7 +20,7 @@ SP_OK, SP_EINVAL, SP_EAUTH, SP_ECUDA, SP_ENODEV = 0, 1, 2, 3, 4
 # Every symbol include/spgcm.h declares (checked by tests/test_abi.py).
 SPGCM_SYMBOLS = (
     "sp_ctx_create", "sp_ctx_destroy", "sp_seal", "sp_open", "sp_seal_batch", "sp_open_batch",
-    "sp_seal_host", "sp_open_host", "sp_seal_host_batch", "sp_open_host_batch",
+    "sp_crypt_batch", "sp_seal_host", "sp_open_host", "sp_seal_host_batch", "sp_open_host_batch",
     "sp_last_error", "sp_version", "sp_launch_count", "sp_ctx_round_keys", "sp_ctx_hash_key",
 )
 
@@ -64,7 +64,7 @@ def load_spgcm() -> ctypes.CDLL:
         lib.sp_ctx_destroy.restype = None
         lib.sp_seal.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, vp, ctypes.c_size_t, vp, vp, vp]
         lib.sp_open.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, vp, ctypes.c_size_t, vp, vp, vp, vp]
-        for name in ("sp_seal_batch", "sp_open_batch"):
+        for name in ("sp_seal_batch", "sp_open_batch", "sp_crypt_batch"):
             getattr(lib, name).argtypes = [vp, ctypes.POINTER(SpDesc), ctypes.c_int, vp]
         for name in ("sp_seal_host_batch", "sp_open_host_batch"):
             getattr(lib, name).argtypes = [vp, ctypes.POINTER(SpDesc), ctypes.c_int]

@@ -77,7 +77,7 @@ __device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams 
                                                uint32_t lct, int lane) {
     const uint4 ek = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
     const uint4 tag = xor4(S, ek);
-    if (!p.open) {
+    if (!(md.dir & kOpenBit)) {
         if (lane == 0) {
             if ((reinterpret_cast<uintptr_t>(md.tag) & 15u) == 0)
                 *reinterpret_cast<uint4 *>(md.tag) = tag;
@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
         const int64_t nblk = (int64_t)((md.len + 15u) >> 4);
         const int tail = (int)(md.len & 15u);
         const bool vec = ((reinterpret_cast<uintptr_t>(md.src) | reinterpret_cast<uintptr_t>(md.dst)) & 15u) == 0;
-        const uint32_t x0 = bswap32(md.dir) ^ p.rk[0];
+        const uint32_t x0 = bswap32(md.dir & 0xffu) ^ p.rk[0];
+        const bool opening = (md.dir & kOpenBit) != 0;
         const uint32_t x1 = bswap32((uint32_t)(md.iv >> 32)) ^ p.rk[1];
         const uint32_t x2 = bswap32((uint32_t)md.iv) ^ p.rk[2];
         const int64_t base_i = nblk - 32 * (int64_t)md.rows + lane;  // block of this lane in local row 0
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
                 uint8_t *dptr = md.dst + 16 * i;
                 if (vec && nb == 16) __stcs(reinterpret_cast<uint4 *>(dptr), out);
                 else store_bytes(dptr, out, nb);
-                if (!p.open) gin = out;
+                if (!opening) gin = out;
             } else {
                 gin = make_uint4(0, 0, 0, 0);
             }
@@ -552,14 +553,17 @@ int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_e
     return SP_OK;
 }
 
-// Build device message table for a batch; returns total rows.
+// Build device message table for a batch; returns total rows.  mode: 0 all
+// seal, 1 all open, 2 per message (desc.reserved = SP_OP_SEAL / SP_OP_OPEN).
 int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Workspace *ws, KParams &p,
-                uint64_t &rows, bool open) {
+                uint64_t &rows, int mode) {
     ws->h_msgs.resize((size_t)n);
     rows = 0;
     for (int i = 0; i < n; ++i) {
         int rc = check_desc(d[i]);
         if (rc) return rc;
+        if (mode == 2 && d[i].reserved > SP_OP_OPEN) return fail(SP_EINVAL, "op must be SP_OP_SEAL or SP_OP_OPEN");
+        const bool open = mode == 1 || (mode == 2 && d[i].reserved == SP_OP_OPEN);
         if (open && !d[i].status) return fail(SP_EINVAL, "open needs a status pointer");
         MsgDev &m = ws->h_msgs[(size_t)i];
         m.src = static_cast<const uint8_t *>(d[i].src);
@@ -568,7 +572,7 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
         m.status = d[i].status;
         m.len = d[i].len;
         m.iv = d[i].iv;
-        m.dir = d[i].dir;
+        m.dir = d[i].dir | (open ? kOpenBit : 0u);
         m.rows = rows_of(d[i].len);
         m.row_begin = rows;
         rows += m.rows;
@@ -608,11 +612,10 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
     p.msgs = ws->d_msgs;
     p.acc = ws->d_acc;
     p.nmsgs = (uint32_t)n;
-    p.open = open ? 1u : 0u;
     return SP_OK;
 }
 
-int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, bool open) {
+int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, int mode) {
     if (!ctx) return fail(SP_EINVAL, "null context");
     if (n <= 0) return n == 0 ? SP_OK : fail(SP_EINVAL, "negative batch size");
     if (!d) return fail(SP_EINVAL, "null descriptors");
@@ -621,7 +624,7 @@ int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, bool open) {
     std::lock_guard<std::mutex> lk(ws->mu);
     KParams p;
     uint64_t rows = 0;
-    int rc = stage_batch(ctx, d, n, s, ws, p, rows, open);
+    int rc = stage_batch(ctx, d, n, s, ws, p, rows, mode);
     if (rc) return rc;
     return launch_rows(ctx, p, 0, rows, s);
 }
@@ -764,7 +767,7 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
     std::lock_guard<std::mutex> wlk(ws->mu);
     KParams p;
     uint64_t rows_chk = 0;
-    rc = stage_batch(ctx, dd.data(), n, hp->s_k, ws, p, rows_chk, open);
+    rc = stage_batch(ctx, dd.data(), n, hp->s_k, ws, p, rows_chk, open ? 1 : 0);
     if (rc) return rc;
 
     // walk pieces of whole rows across the flattened batch
@@ -918,11 +921,15 @@ int sp_ctx_hash_key(const sp_ctx *c, uint8_t out[16]) {
 }
 
 int sp_seal_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
-    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), false);
+    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), 0);
 }
 
 int sp_open_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
-    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), true);
+    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), 1);
+}
+
+int sp_crypt_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
+    return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), 2);
 }
 
 int sp_seal(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len, void *dst, void *tag16,

@@ -63,6 +63,10 @@ struct MsgDev {
 // device array filled from a pinned staging ring.
 constexpr uint32_t kInline = 32;
 
+// MsgDev.dir: low byte = channel direction (nonce word 0), this bit = open
+// (verify + decrypt) instead of seal, so one launch can mix both.
+constexpr uint32_t kOpenBit = 0x100u;
+
 struct KParams {
     MsgDev inl[kInline];
     uint32_t rk[60];
@@ -74,7 +78,7 @@ struct KParams {
     uint64_t row_begin;    // rows [row_begin, row_end) of the flattened batch
     uint64_t row_end;
     uint32_t nmsgs;
-    uint32_t open;
+    uint32_t reserved;
     uint32_t warps_used;   // warps per CTA that own rows (<= kWarpsPerCta)
 };
 

@@ -334,6 +334,20 @@ struct DevicePool {
 std::mutex g_dev_mu;
 std::map<int, Streams> g_streams;
 std::map<int, DevicePool> g_pools;
+std::map<std::pair<int, std::string>, sp_ctx *> g_ctx;  // key setup once per (device, key)
+std::vector<std::pair<uint8_t *, uint64_t>> g_pinned;   // idle pinned arenas (process-wide)
+
+sp_ctx *ctx_for(int dev, const uint8_t key[32]) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    auto k = std::make_pair(dev, std::string(reinterpret_cast<const char *>(key), 32));
+    auto it = g_ctx.find(k);
+    if (it != g_ctx.end()) return it->second;
+    sp_ctx *c = nullptr;
+    int rc = sp_ctx_create(key, &c);
+    if (rc) throw CudaErr(std::string("sp_ctx_create: ") + sp_last_error());
+    g_ctx[k] = c;
+    return c;
+}
 
 Streams streams_for(int dev) {
     std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -372,11 +386,20 @@ cudaMemPool_t pool_for(int dev, uint64_t reserve, cudaStream_t s) {
     return p.pool;
 }
 
+// One queued seal/open of the compute stream.  The regions it reads and
+// writes give the dependencies flush() schedules by: an op runs in a later
+// launch than every earlier op it conflicts with (RAW, WAR, WAW), independent
+// seals and opens share launches (sp_crypt_batch).
+struct Region {
+    const Buf *buf;
+    uint64_t lo, hi;
+};
 struct Op {
-    int kind;  // 0 wait, 1 seal, 2 open
-    FenceP wait;
-    sp_desc d;
-    BufP a, b, c;  // buffers the op touches (kept alive until issued)
+    sp_desc d;     // d.reserved = SP_OP_SEAL / SP_OP_OPEN
+    FenceP wait;   // produced on another stream (staging copy, spec batch, earlier window)
+    BufP a, b;     // buffers the op touches (kept alive until issued)
+    Region r[2], w[2];
+    int nr = 0, nw = 0;
 };
 
 struct Landing {
@@ -434,8 +457,7 @@ class Plane {
         ck(cudaGetDevice(&dev), "cudaGetDevice");
         s = streams_for(dev);
         pool = pool_for(dev, reserve, s.comp);
-        int rc = sp_ctx_create(key, &ctx);
-        if (rc) throw CudaErr(std::string("sp_ctx_create: ") + sp_last_error());
+        ctx = ctx_for(dev, key);
         ck(cudaMalloc(&status, status_cap * sizeof(int32_t)), "cudaMalloc(status)");
         ck(cudaMemset(status, 0, status_cap * sizeof(int32_t)), "cudaMemset(status)");
         window = new_fence();
@@ -455,14 +477,17 @@ class Plane {
         window.reset();
         collect();
         cudaStreamSynchronize(s.comp);
-        for (auto &a : pinned_free) cudaFreeHost(a.ptr);
-        for (auto &a : pinned_busy) {
-            a.done.reset();
-            cudaFreeHost(a.ptr);
+        {
+            // every copy out of the arenas is done (streams drained): hand them on
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            for (auto &a : pinned_free) g_pinned.push_back({a.ptr, a.cap});
+            for (auto &a : pinned_busy) {
+                a.done.reset();
+                g_pinned.push_back({a.ptr, a.cap});
+            }
         }
         for (cudaEvent_t e : free_events) cudaEventDestroy(e);
         if (status) cudaFree(status);
-        if (ctx) sp_ctx_destroy(ctx);
     }
 
     // -- events / buffers --------------------------------------------------------------
@@ -557,17 +582,29 @@ class Plane {
 
     // -- compute queue ------------------------------------------------------------------
     void queue(Op &&op, uint64_t nbytes) {
+        if (op.wait == window) op.wait.reset();  // queue order covers the current window
         ops.push_back(std::move(op));
         ops_bytes += nbytes;
         if (ops_bytes >= batch_bytes) flush();
     }
-    void wait_for(const FenceP &f) {
-        if (f && f != window) {
-            Op op{};
-            op.kind = 0;
-            op.wait = f;
-            ops.push_back(std::move(op));
-        }
+    static Op make_op(uint32_t opkind, uint32_t dir, uint64_t iv, uint64_t len, const View &src, const View &dst,
+                      const BufP &tagbuf, uint64_t tag_off, int32_t *status) {
+        Op op;
+        op.d.dir = dir;
+        op.d.reserved = opkind;
+        op.d.iv = iv;
+        op.d.len = len;
+        op.d.src = src.ptr();
+        op.d.dst = dst.ptr();
+        op.d.tag = tagbuf->ptr + tag_off;
+        op.d.status = status;
+        op.a = src.buf;
+        op.b = dst.buf;
+        op.r[op.nr++] = Region{src.buf.get(), src.off, src.off + len};
+        op.w[op.nw++] = Region{dst.buf.get(), dst.off, dst.off + len};
+        if (opkind == SP_OP_SEAL) op.w[op.nw++] = Region{tagbuf.get(), tag_off, tag_off + kTag};
+        else op.r[op.nr++] = Region{tagbuf.get(), tag_off, tag_off + kTag};
+        return op;
     }
 
     void flush() {
@@ -589,29 +626,52 @@ class Plane {
             std::vector<Op> q;
             q.swap(ops);
             ops_bytes = 0;
+            // level = 1 + max level of the earlier ops it conflicts with
+            struct Touch {
+                uint64_t lo, hi;
+                int level;
+                bool write;
+            };
+            std::unordered_map<const Buf *, std::vector<Touch>> touched;
+            std::vector<int> level(q.size(), 0);
+            int top = 0;
+            for (size_t i = 0; i < q.size(); ++i) {
+                const Op &op = q[i];
+                int lv = 0;
+                auto scan = [&](const Region &rg, bool write) {
+                    auto it = touched.find(rg.buf);
+                    if (it == touched.end()) return;
+                    for (const Touch &t : it->second)
+                        if ((write || t.write) && t.lo < rg.hi && rg.lo < t.hi) lv = std::max(lv, t.level + 1);
+                };
+                for (int k = 0; k < op.nr; ++k) scan(op.r[k], false);
+                for (int k = 0; k < op.nw; ++k) scan(op.w[k], true);
+                level[i] = lv;
+                top = std::max(top, lv);
+                for (int k = 0; k < op.nr; ++k) touched[op.r[k].buf].push_back({op.r[k].lo, op.r[k].hi, lv, false});
+                for (int k = 0; k < op.nw; ++k) touched[op.w[k].buf].push_back({op.w[k].lo, op.w[k].hi, lv, true});
+            }
             std::vector<sp_desc> descs;
-            size_t i = 0;
-            while (i < q.size()) {
-                if (q[i].kind == 0) {
-                    wait(s.comp, q[i].wait);
-                    ++i;
-                    continue;
-                }
-                size_t j = i;
+            std::unordered_set<Fence *> waited;
+            for (int lv = 0; lv <= top; ++lv) {
                 descs.clear();
-                while (j < q.size() && q[j].kind == q[i].kind) descs.push_back(q[j++].d);
-                int rc = q[i].kind == 1 ? sp_seal_batch(ctx, descs.data(), (int)descs.size(), s.comp)
-                                        : sp_open_batch(ctx, descs.data(), (int)descs.size(), s.comp);
-                ck_sp(rc, q[i].kind == 1 ? "sp_seal_batch" : "sp_open_batch");
+                for (size_t i = 0; i < q.size(); ++i) {
+                    if (level[i] != lv) continue;
+                    if (q[i].wait && !waited.count(q[i].wait.get())) {
+                        wait(s.comp, q[i].wait);
+                        waited.insert(q[i].wait.get());
+                    }
+                    descs.push_back(q[i].d);
+                }
+                if (descs.empty()) continue;
+                ck_sp(sp_crypt_batch(ctx, descs.data(), (int)descs.size(), s.comp), "sp_crypt_batch");
                 ++launches;
-                i = j;
             }
             record(window, s.comp);
             ++tick;
             for (auto &op : q) {
                 if (op.a) op.a->use(s.comp, window, tick);
                 if (op.b) op.b->use(s.comp, window, tick);
-                if (op.c) op.c->use(s.comp, window, tick);
             }
             window = new_fence();
         }
@@ -635,6 +695,15 @@ class Plane {
                 pinned_free.erase(pinned_free.begin() + (long)k);
                 return a;
             }
+        {
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            for (size_t k = 0; k < g_pinned.size(); ++k)
+                if (g_pinned[k].second >= need) {
+                    PinnedArena a{g_pinned[k].first, g_pinned[k].second, nullptr};
+                    g_pinned.erase(g_pinned.begin() + (long)k);
+                    return a;
+                }
+        }
         PinnedArena a{nullptr, std::max(need, kArenaBytes), nullptr};
         ck(cudaHostAlloc(reinterpret_cast<void **>(&a.ptr), a.cap, cudaHostAllocDefault), "cudaHostAlloc(arena)");
         return a;
@@ -741,23 +810,16 @@ class Plane {
         BufP buf = stage_h2d(b, inner, spans, done);
         uint64_t first = spans[0].first, total = 0;
         for (auto &sp : spans) total += sp.second;
-        wait_for(done);
         for (size_t i = 0; i < spans.size(); ++i) {
             auto m = std::make_shared<Msg>();
             m->buf = buf;
             m->off = spans[i].first - first;
             m->len = spans[i].second;
             m->tag_off = round16(total) + kTag * i;
-            m->ready = window;
-            Op op{};
-            op.kind = 1;
-            op.d.dir = (uint32_t)dir;
-            op.d.iv = iv0 + i;
-            op.d.len = m->len;
-            op.d.src = buf->ptr + m->off;
-            op.d.dst = buf->ptr + m->off;
-            op.d.tag = buf->ptr + m->tag_off;
-            op.a = buf;
+            View v{buf, m->off, m->len};
+            Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, m->len, v, v, buf, m->tag_off, nullptr);
+            op.wait = done;
+            m->ready = window;  // before queue(): a threshold flush there issues this op in this window
             queue(std::move(op), m->len);
             msgs.push_back(m);
         }
@@ -849,17 +911,10 @@ class Plane {
             m->off = spans[i].first - first;
             m->len = spans[i].second;
             m->tag_off = round16(total) + kTag * i;
+            Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, m->len,
+                            View{src.buf, src.off + spans[i].first, m->len}, View{buf, m->off, m->len}, buf,
+                            m->tag_off, nullptr);
             m->ready = window;
-            Op op{};
-            op.kind = 1;
-            op.d.dir = (uint32_t)dir;
-            op.d.iv = iv0 + i;
-            op.d.len = m->len;
-            op.d.src = src.buf->ptr + src.off + spans[i].first;
-            op.d.dst = buf->ptr + m->off;
-            op.d.tag = buf->ptr + m->tag_off;
-            op.a = buf;
-            op.b = src.buf;
             queue(std::move(op), m->len);
             msgs.push_back(m);
         }
@@ -891,16 +946,9 @@ class Plane {
                 m->buf = arena_dev;
                 m->off = o;
                 m->tag_off = o + need - kTag;
+                View v{arena_dev, o, n};
+                Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, n, v, v, arena_dev, m->tag_off, nullptr);
                 m->ready = window;
-                Op op{};
-                op.kind = 1;
-                op.d.dir = (uint32_t)dir;
-                op.d.iv = iv0 + i;
-                op.d.len = n;
-                op.d.src = arena_dev->ptr + o;
-                op.d.dst = arena_dev->ptr + o;
-                op.d.tag = arena_dev->ptr + m->tag_off;
-                op.a = arena_dev;
                 queue(std::move(op), n);
             }
             msgs.push_back(m);
@@ -914,20 +962,12 @@ class Plane {
         if (dry) return;
         for (auto &j : jobs) {
             const MsgP &m = std::get<0>(j);
-            wait_for(m->ready);
             View dst = std::get<2>(j);
             if (!dst.buf) dst = View{alloc(m->len, s.comp), 0, m->len};
-            Op op{};
-            op.kind = 2;
-            op.d.dir = (uint32_t)dir;
-            op.d.iv = std::get<1>(j);
-            op.d.len = m->len;
-            op.d.src = m->buf->ptr + m->off;
-            op.d.dst = dst.ptr();
-            op.d.tag = m->buf->ptr + m->tag_off;
-            op.d.status = status_slot();
-            op.a = m->buf;
-            op.b = dst.buf;
+            int32_t *st = status_slot();
+            Op op = make_op(SP_OP_OPEN, (uint32_t)dir, std::get<1>(j), m->len, View{m->buf, m->off, m->len}, dst,
+                            m->buf, m->tag_off, st);
+            op.wait = m->ready;
             queue(std::move(op), m->len);
         }
     }

@@ -325,3 +325,58 @@ def test_host_batch_pieces_split_messages(ctx_for, torch_cuda):
     with pytest.raises(GcmAuthError):
         ctx.open_host_batch([(0, 900 + i, d, b, t) for i, (d, b, t) in enumerate(zip(dst, back, tags))])
     assert int(back[3].sum()) == 0
+
+
+def test_mixed_seal_open_batch(ctx_for, torch_cuda):
+    """sp_crypt_batch: seals and opens interleaved in one launch (the data
+    plane's level-scheduled flushes) — seals match the oracle bit for bit,
+    authentic opens return the plaintext, a tampered one fails and is zeroed."""
+    import ctypes
+
+    from paper_2411_03357_b200 import _native
+
+    torch = torch_cuda
+    rng = random.Random(77)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    lib = _native.load_spgcm()
+    n = 48
+    sizes = [rng.choice([1, 17, 2048, 229_376, rng.randrange(1, 3 * MIB)]) for _ in range(n)]
+    plains = [rng.randbytes(s) for s in sizes]
+    ivs = [rng.randrange(1 << 64) for _ in range(n)]
+    dirs = [rng.randrange(2) for _ in range(n)]
+    refs = [oracle_port.seal(key, d, iv, p) for d, iv, p in zip(dirs, ivs, plains)]
+    is_open = [i % 2 == 1 for i in range(n)]
+    srcs, dsts = [], []
+    tags = torch.zeros((n, 16), dtype=torch.uint8, device="cuda")
+    status = torch.full((n,), 7, dtype=torch.int32, device="cuda")
+    descs = (_native.SpDesc * n)()
+    for i in range(n):
+        if is_open[i]:
+            c, t = refs[i]
+            if i == 5:
+                c = bytes([c[0] ^ 1]) + c[1:]  # tampered
+            src = _dev(torch, c)
+            tags[i] = torch.tensor(list(t), dtype=torch.uint8)
+        else:
+            src = _dev(torch, plains[i])
+        dst = torch.full_like(src, 0xAB)
+        srcs.append(src)
+        dsts.append(dst)
+        d = descs[i]
+        d.dir, d.reserved, d.iv, d.len = dirs[i], int(is_open[i]), ivs[i], sizes[i]
+        d.src, d.dst, d.tag = src.data_ptr(), dst.data_ptr(), tags[i].data_ptr()
+        d.status = status.data_ptr() + 4 * i
+    rc = lib.sp_crypt_batch(ctx._h, descs, n, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0, _native.last_error()
+    torch.cuda.synchronize()
+    st = status.cpu().tolist()
+    for i in range(n):
+        if is_open[i]:
+            if i == 5:
+                assert st[i] == 1 and _host(dsts[i]) == bytes(sizes[i])
+            else:
+                assert st[i] == 0 and _host(dsts[i]) == plains[i], i
+        else:
+            assert (_host(dsts[i]), _host(tags[i])) == refs[i], i
+            assert st[i] == 7  # seals leave status alone
