@@ -380,6 +380,7 @@ def run_gpu(args) -> None:
     offload = None
     if not args.no_offload:
         offload = offload_bench(args, dist, dev_sync, rank, world)
+        offload["other_configs"] = workloads_bench(args, dist, dev_sync, rank, world)
 
     if rank != 0:
         if dist is not None:
@@ -440,24 +441,13 @@ def run_gpu(args) -> None:
         dist.destroy_process_group()
 
 
-def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
-    """OPT-66B-shaped FlexGen weight offload (2 offloaded layers, 61 x 32 MiB
-    blocks each) through the B200 engine vs the same swaps as plain copies —
-    the north star's 'within 10% of unencrypted swap throughput'.  Every rank
-    replays its own trace on its own channel (seed = rank); a run's time is
-    the max over ranks, its bytes the sum.  Runs alternate plain / encrypted;
-    best of `reps` each (pinned-memory copy variance on a shared host)."""
-    from paper_2411_03357_b200 import workload
-    from paper_2411_03357_b200.replay import ReplayConfig, run_engine, run_plain
-
-    # The whole trace is timed (speculation runs ahead across iteration
-    # boundaries, so a mid-trace clock start would credit the encrypted run
-    # with copies issued before it); timed repetitions follow one untimed
-    # run of each arm and the best of each is reported.
-    iters = args.offload_iters
-    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=iters, seed=rank)
-    start = 0
-    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank)
+def trace_compare(tr, cfg, dist, dev_sync, world: int, reps: int) -> dict:
+    """One synthetic trace through the native engine (libsppipe: encrypted,
+    speculative) and as plain pinned cudaMemcpyAsync swaps from the same C++
+    dispatch loop (sp_pipe_plain_replay): one untimed run of each, then
+    `reps` timed runs of each alternating; best of each.  A run's time is the
+    max over ranks, its bytes the sum (whole job)."""
+    from paper_2411_03357_b200.replay import prepare_memory, run_engine, run_plain_native
 
     def timed(fn):
         barrier(dist, dev_sync)
@@ -465,31 +455,66 @@ def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1)
         wall = reduce_max(dist, r.wall_s, dev_sync)
         return r, world * r.swap_bytes / wall / 1e9
 
-    from paper_2411_03357_b200.replay import prepare_memory
-
     memory = prepare_memory(tr, cfg)  # one set of pinned host blocks for every run
-    # untimed warm-up of both arms: staging and device blocks come from the
-    # caching allocator on the long-lived data-plane streams afterwards
-    run_plain(tr, fill="fast", memory=memory)
+    run_plain_native(tr, cfg, memory=memory)
     run_engine(tr, cfg, memory=memory)
     plain, enc, rep = [], [], None
-    for _ in range(args.offload_reps):
-        _, g = timed(lambda: run_plain(tr, fill="fast", measure_from=start, memory=memory))
-        plain.append(g)
-        r, g = timed(lambda: run_engine(tr, cfg, measure_from=start, memory=memory))
+    for _ in range(reps):
+        plain.append(timed(lambda: run_plain_native(tr, cfg, memory=memory))[1])
+        r, g = timed(lambda: run_engine(tr, cfg, memory=memory))
         enc.append(g)
         rep = r.engine.report()
         del r
-    return {"model": "opt-66b", "layers_offloaded_per_gpu": 2, "iterations": args.offload_iters,
-            "layer_bytes": workload.opt_layer_bytes("opt-66b"),
-            "swap_bytes_timed_per_gpu": tr.swap_bytes(), "timed": "whole trace, best of reps",
-            "n_gpus": world, "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
+    return {"swap_bytes_per_gpu": tr.swap_bytes(), "events": len(tr.events),
+            "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
             "encrypted_runs": [round(x, 2) for x in enc], "plain_runs": [round(x, 2) for x in plain],
             "throughput_ratio": round(max(enc) / max(plain), 4),
-            "note": "whole-job swap GB/s (sum over ranks / max time); tokens/s ratio == swap throughput ratio "
-                    "(same trace, same batch); random payload",
-            "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "nops": rep["nops"],
-            "sequence_hit_rate": rep["sequence_hit_rate"]}
+            "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "misses": rep["miss"], "nops": rep["nops"],
+            "relinquishes": rep["relinquishes"] + rep["replans"], "sequence_hit_rate": rep["sequence_hit_rate"]}
+
+
+def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
+    """OPT-66B-shaped FlexGen weight offload (2 offloaded layers, 61 x 32 MiB
+    blocks each) through the native engine vs the same swaps as plain
+    copies — the north star's 'within 10% of unencrypted swap throughput'.
+    Every rank replays its own trace on its own channel (seed = rank).  The
+    whole trace is timed (speculation runs ahead across iteration
+    boundaries, so a mid-trace clock start would credit the encrypted run
+    with copies issued before it)."""
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import ReplayConfig
+
+    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank, engine="native")
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=args.offload_iters, seed=rank)
+    out = {"model": "opt-66b", "layers_offloaded_per_gpu": 2, "iterations": args.offload_iters,
+           "layer_bytes": workload.opt_layer_bytes("opt-66b"), "timed": "whole trace, best of reps", "n_gpus": world,
+           "engine": "libsppipe (native control plane + B200 data plane), sp_pipe_replay",
+           "plain": "sp_pipe_plain_replay: the same swaps as pinned cudaMemcpyAsync, no crypto",
+           "note": "whole-job swap GB/s (sum over ranks / max time); tokens/s ratio == swap throughput ratio "
+                   "(same trace, same batch); random payload"}
+    out.update(trace_compare(tr, cfg, dist, dev_sync, world, args.offload_reps))
+    return out
+
+
+def workloads_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
+    """BASELINE configs 3 and 4 at full shape through the same comparison:
+    OPT-30B vLLM KV-block swapping (229,376 B blocks, adversarial 25%
+    mispredictions, relinquish path) and OPT-30B LoRA activation offload
+    (48 x 28 MiB activations, encrypt-on-D2H / decrypt-on-H2D)."""
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import ReplayConfig
+
+    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank, engine="native",
+                       reference_compat=False)
+    kv = workload.gen_adversarial_trace(
+        workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=rank), 0.25, seed=8)
+    act = workload.gen_activation_trace(48, 29_360_128, 2, seed=rank)
+    return {
+        "kv_swap_opt30b": {"trace": "gen_kvswap_trace(48, lifo, 229,376 B blocks, parallel 4) + 25% adversarial",
+                           **trace_compare(kv, cfg, dist, dev_sync, world, 5)},
+        "activation_opt30b": {"trace": "gen_activation_trace(48 layers, 29,360,128 B, 2 steps)",
+                              **trace_compare(act, cfg, dist, dev_sync, world, 2)},
+    }
 
 
 def main() -> None:
@@ -503,7 +528,7 @@ def main() -> None:
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (flow check on a 1-GPU box)")
     ap.add_argument("--cpu-reps", type=int, default=8, help="layers sealed+opened by the 1-core CPU baseline")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
-    ap.add_argument("--offload-iters", type=int, default=3)
+    ap.add_argument("--offload-iters", type=int, default=8)
     ap.add_argument("--offload-reps", type=int, default=4)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -219,6 +219,10 @@ int sp_pipe_app_read(sp_pipe *p, int64_t block, uint64_t offset, uint64_t n, voi
 /* Whole trace in one call (the replay driver of simulator.py:404-426 minus
  * its cost model); payloads holds small-I/O and app-write bytes. */
 int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done);
+/* The unencrypted baseline of the same trace (NoCc): each swap one plain
+ * cudaMemcpyAsync between the registered pinned block and HBM on the pipe's
+ * copy streams, same ordering rules, no crypto; returns when the device is idle. */
+int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads);
 int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done);
 
 /* report(): counters in the order of sp_pipe_counter_name(i); n = count. */
@@ -236,6 +240,9 @@ int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which);
 int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, void *bytes);
 /* Data-plane statistics: bytes over PCIe per direction, kernel launches. */
 int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches);
+/* Device memory: bytes the stream-ordered pool holds from the driver, bytes
+ * handed out, bytes parked in this pipe's buffer cache. */
+int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t *cached);
 const char *sp_pipe_last_error(void);
 
 #ifdef __cplusplus

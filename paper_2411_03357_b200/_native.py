@@ -97,10 +97,10 @@ SPPIPE_SYMBOLS = (
     "sp_pred_outstanding", "sp_pred_in_batch_count", "sp_pred_decision_count", "sp_pred_decision",
     "sp_pipe_create", "sp_pipe_destroy", "sp_pipe_register_block", "sp_pipe_seed_device", "sp_pipe_submit_h2d",
     "sp_pipe_submit_d2h", "sp_pipe_small_io", "sp_pipe_sync", "sp_pipe_speculate", "sp_pipe_relinquish",
-    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay",
+    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
     "sp_pipe_handle_done", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv", "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
-    "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_last_error",
+    "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
 )
 
 
@@ -195,12 +195,14 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_app_write": [vp, i64, u64, vp, u64, P(i64)],
             "sp_pipe_app_read": [vp, i64, u64, u64, vp],
             "sp_pipe_replay": [vp, P(SpEvent), u64, vp, P(u64)],
+            "sp_pipe_plain_replay": [vp, P(SpEvent), u64, vp],
             "sp_pipe_handle_done": [vp, u64, P(i32)],
             "sp_pipe_report": [vp, P(i64), i32, P(i32)],
             "sp_pipe_actions": [vp, i64, P(SpAction), i64, P(i64)],
             "sp_pipe_sent_log": [vp, i32, i64, P(SpSent), i64, P(i64)],
             "sp_pipe_delivered": [vp, i32, i64, P(SpDelivery), vp],
             "sp_pipe_stats": [vp, P(u64), P(u64), P(u64)],
+            "sp_pipe_pool_stats": [vp, P(u64), P(u64), P(u64)],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)

@@ -78,6 +78,7 @@ struct Fence {
     cudaEvent_t ev = nullptr;
     cudaStream_t stream = nullptr;
     bool recorded = false;
+    bool complete = false;  // observed complete once (never re-recorded after that)
     Plane *plane = nullptr;
     ~Fence();
 };
@@ -87,6 +88,7 @@ struct Buf {
     Plane *plane = nullptr;
     uint8_t *ptr = nullptr;
     uint64_t size = 0;
+    uint64_t alloc_size = 0;
     std::vector<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
     uint64_t last_use = 0;
     cudaStream_t last_stream = nullptr;
@@ -335,7 +337,7 @@ std::mutex g_dev_mu;
 std::map<int, Streams> g_streams;
 std::map<int, DevicePool> g_pools;
 std::map<std::pair<int, std::string>, sp_ctx *> g_ctx;  // key setup once per (device, key)
-std::vector<std::pair<uint8_t *, uint64_t>> g_pinned;   // idle pinned arenas (process-wide)
+std::vector<std::pair<uint8_t *, uint64_t>> g_rings;    // idle pinned staging rings (process-wide)
 
 sp_ctx *ctx_for(int dev, const uint8_t key[32]) {
     std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -425,6 +427,10 @@ class Plane {
     };
     std::vector<Garbage> garbage;
     bool collecting = false;
+    std::unordered_map<uint64_t, std::vector<Garbage>> cache;  // size class -> retired buffers
+    uint64_t cached_bytes = 0;
+    bool closing = false;
+    static constexpr uint64_t kCacheBytes = 8ull << 30;
 
     // compute queue
     std::vector<Op> ops;
@@ -434,12 +440,15 @@ class Plane {
     std::vector<uint8_t> arena_host;
     BufP arena_dev;
     uint64_t arena_off = 0;
-    struct PinnedArena {
-        uint8_t *ptr;
-        uint64_t cap;
-        FenceP done;
-    };
-    std::vector<PinnedArena> pinned_free, pinned_busy;
+    // Pinned host staging ring for small payloads (arena flushes, token
+    // copies): slots are taken in order and handed back when the fence of
+    // the copy that read/wrote them has passed; one cudaHostAlloc per process.
+    struct Ring {
+        uint8_t *ptr = nullptr;
+        uint64_t cap = 0, head = 0;
+        std::deque<std::tuple<uint64_t, uint64_t, FenceP>> busy;  // [begin, end), fence
+    } ring;
+    static constexpr uint64_t kRingBytes = 32ull << 20;
     static constexpr uint64_t kArenaBytes = 1 << 20;
     // landings
     std::vector<Landing> landings;
@@ -468,6 +477,7 @@ class Plane {
             finish_streams();
         } catch (...) {
         }
+        closing = true;
         ops.clear();
         landings.clear();
         host_ready.clear();
@@ -475,16 +485,16 @@ class Plane {
         arena_dev.reset();
         zero_scratch.reset();
         window.reset();
+        for (auto &kv : cache)
+            for (auto &g : kv.second) garbage.push_back(std::move(g));
+        cache.clear();
         collect();
         cudaStreamSynchronize(s.comp);
-        {
-            // every copy out of the arenas is done (streams drained): hand them on
+        if (ring.ptr) {
+            // every copy through the ring is done (streams drained): hand it on
+            ring.busy.clear();
             std::lock_guard<std::mutex> lk(g_dev_mu);
-            for (auto &a : pinned_free) g_pinned.push_back({a.ptr, a.cap});
-            for (auto &a : pinned_busy) {
-                a.done.reset();
-                g_pinned.push_back({a.ptr, a.cap});
-            }
+            g_rings.push_back({ring.ptr, ring.cap});
         }
         for (cudaEvent_t e : free_events) cudaEventDestroy(e);
         if (status) cudaFree(status);
@@ -518,14 +528,50 @@ class Plane {
         if (f->stream == st) return;  // stream order covers it
         ck(cudaStreamWaitEvent(st, f->ev, 0), "cudaStreamWaitEvent");
     }
+    // Size classes of the plane's buffer cache: 4 KiB steps up to 1 MiB,
+    // then 1 MiB steps (staging sizes repeat: chunks, KV blocks, arenas).
+    static uint64_t size_class(uint64_t n) {
+        n = std::max<uint64_t>(n, 16);
+        return n <= (1u << 20) ? (n + 4095u) & ~uint64_t(4095) : (n + (1u << 20) - 1) & ~uint64_t((1u << 20) - 1);
+    }
+    static bool passed(Fence &f) {
+        if (!f.complete && cudaEventQuery(f.ev) == cudaSuccess) f.complete = true;
+        return f.complete;
+    }
+    // A retired buffer is reusable on stream st without any wait when every
+    // other stream that touched it has passed its fence.
+    bool reusable(const Garbage &g, cudaStream_t st) {
+        for (auto &u : g.uses) {
+            if (u.first == st) continue;
+            if (!u.second || !u.second->recorded) return false;
+            if (!passed(*u.second)) return false;
+        }
+        return true;
+    }
     BufP alloc(uint64_t n, cudaStream_t st) {
         auto b = std::make_shared<Buf>();
         b->plane = this;
         b->size = n;
         if (!dry) {
-            void *p = nullptr;
-            ck(cudaMallocFromPoolAsync(&p, std::max<uint64_t>(n, 16), pool, st), "cudaMallocFromPoolAsync");
-            b->ptr = static_cast<uint8_t *>(p);
+            const uint64_t cls = size_class(n);
+            auto it = cache.find(cls);
+            if (it != cache.end()) {
+                auto &v = it->second;
+                const size_t lim = v.size() > 4 ? v.size() - 4 : 0;
+                for (size_t k = v.size(); k-- > lim;) {
+                    if (!reusable(v[k], st)) continue;
+                    b->ptr = v[k].ptr;
+                    v.erase(v.begin() + (long)k);
+                    cached_bytes -= cls;
+                    break;
+                }
+            }
+            if (!b->ptr) {
+                void *p = nullptr;
+                ck(cudaMallocFromPoolAsync(&p, cls, pool, st), "cudaMallocFromPoolAsync");
+                b->ptr = static_cast<uint8_t *>(p);
+            }
+            b->alloc_size = cls;
             b->last_stream = st;
             b->uses.emplace_back(st, FenceP());
         }
@@ -533,7 +579,13 @@ class Plane {
     }
     void retire(Buf *b) {
         if (dry || !b->ptr) return;
-        garbage.push_back({b->ptr, std::move(b->uses), b->last_stream});
+        Garbage g{b->ptr, std::move(b->uses), b->last_stream};
+        if (!closing && cached_bytes + b->alloc_size <= kCacheBytes) {
+            cache[b->alloc_size].push_back(std::move(g));
+            cached_bytes += b->alloc_size;
+            return;
+        }
+        garbage.push_back(std::move(g));
     }
     // Return retired buffers to the pool on the stream of their last use,
     // after every other stream that touched them has passed its fence.
@@ -609,15 +661,18 @@ class Plane {
 
     void flush() {
         if (dry) return;
-        if (!arena_host.empty()) {
-            PinnedArena pa = pinned_arena(arena_host.size());
-            memcpy(pa.ptr, arena_host.data(), arena_host.size());
-            ck(cudaMemcpyAsync(arena_dev->ptr, pa.ptr, arena_host.size(), cudaMemcpyHostToDevice, s.comp),
-               "arena H2D");
-            pa.done = record_new(s.comp);
-            arena_dev->use(s.comp, pa.done, ++tick);
-            pinned_busy.push_back(pa);
-            bytes_h2d += arena_host.size();
+        if (arena_dev && arena_off) {
+            // the window's arena is sealed/opened by this flush; the next one starts fresh
+            if (!arena_host.empty()) {
+                const uint64_t n = arena_host.size();
+                uint8_t *h = ring_reserve(n);
+                memcpy(h, arena_host.data(), n);
+                ck(cudaMemcpyAsync(arena_dev->ptr, h, n, cudaMemcpyHostToDevice, s.comp), "arena H2D");
+                FenceP f = record_new(s.comp);
+                ring_commit(h, n, f);
+                arena_dev->use(s.comp, f, ++tick);
+                bytes_h2d += n;
+            }
             arena_host.clear();
             arena_dev.reset();
             arena_off = 0;
@@ -679,34 +734,40 @@ class Plane {
         collect();
     }
 
-    PinnedArena pinned_arena(uint64_t need) {
-        for (size_t k = 0; k < pinned_busy.size();) {
-            if (cudaEventQuery(pinned_busy[k].done->ev) == cudaSuccess) {
-                pinned_busy[k].done.reset();
-                pinned_free.push_back(pinned_busy[k]);
-                pinned_busy.erase(pinned_busy.begin() + (long)k);
-            } else {
-                ++k;
-            }
-        }
-        for (size_t k = 0; k < pinned_free.size(); ++k)
-            if (pinned_free[k].cap >= need) {
-                PinnedArena a = pinned_free[k];
-                pinned_free.erase(pinned_free.begin() + (long)k);
-                return a;
-            }
-        {
-            std::lock_guard<std::mutex> lk(g_dev_mu);
-            for (size_t k = 0; k < g_pinned.size(); ++k)
-                if (g_pinned[k].second >= need) {
-                    PinnedArena a{g_pinned[k].first, g_pinned[k].second, nullptr};
-                    g_pinned.erase(g_pinned.begin() + (long)k);
-                    return a;
+    uint8_t *ring_reserve(uint64_t n) {
+        if (!ring.ptr) {
+            {
+                std::lock_guard<std::mutex> lk(g_dev_mu);
+                if (!g_rings.empty()) {
+                    ring.ptr = g_rings.back().first;
+                    ring.cap = g_rings.back().second;
+                    g_rings.pop_back();
                 }
+            }
+            if (!ring.ptr) {
+                ring.cap = kRingBytes;
+                ck(cudaHostAlloc(reinterpret_cast<void **>(&ring.ptr), ring.cap, cudaHostAllocDefault), "cudaHostAlloc(ring)");
+            }
         }
-        PinnedArena a{nullptr, std::max(need, kArenaBytes), nullptr};
-        ck(cudaHostAlloc(reinterpret_cast<void **>(&a.ptr), a.cap, cudaHostAllocDefault), "cudaHostAlloc(arena)");
-        return a;
+        if (n > ring.cap) throw ValueErr("small payload larger than the staging ring");
+        if (ring.head + n > ring.cap) ring.head = 0;
+        const uint64_t lo = ring.head, hi = lo + n;
+        while (!ring.busy.empty()) {
+            auto &b = ring.busy.front();
+            const bool overlap = std::get<0>(b) < hi && lo < std::get<1>(b);
+            if (overlap) {
+                ck(cudaEventSynchronize(std::get<2>(b)->ev), "ring slot wait");
+            } else if (!passed(*std::get<2>(b))) {
+                break;
+            }
+            ring.busy.pop_front();
+        }
+        ring.head = hi;
+        return ring.ptr + lo;
+    }
+    void ring_commit(uint8_t *p, uint64_t n, const FenceP &f) {
+        const uint64_t lo = (uint64_t)(p - ring.ptr);
+        ring.busy.emplace_back(lo, lo + n, f);
     }
 
     void flush_landings() {
@@ -762,13 +823,48 @@ class Plane {
                 if (it != h2d_done.end() && it->second) wait(s.d2h, it->second);
                 last = p.block;
             }
-            ck(cudaMemcpyAsync(p.block->host + p.boff, buf->ptr + p.off, p.n, cudaMemcpyDeviceToHost, s.d2h),
-               "landing D2H");
         }
+        copy_batch_d2h(places.size(), [&](size_t i, void *&dst, void *&src, size_t &n) {
+            dst = places[i].block->host + places[i].boff;
+            src = buf->ptr + places[i].off;
+            n = places[i].n;
+        });
         FenceP ev = record_new(s.d2h);
         buf->use(s.d2h, ev, ++tick);
         for (auto &l : ls) host_ready[l.block->id] = ev;
         bytes_d2h += total;
+    }
+
+    // Landing copies of one flush: one cudaMemcpyBatchAsync (CUDA 12.8+)
+    // instead of a call per block; plain cudaMemcpyAsync where unsupported.
+    template <class F>
+    void copy_batch_d2h(size_t count, F &&get) {
+        static bool batch_ok = true;
+        if (count > 1 && batch_ok) {
+            std::vector<void *> dsts(count), srcs(count);
+            std::vector<size_t> sizes(count);
+            for (size_t i = 0; i < count; ++i) get(i, dsts[i], srcs[i], sizes[i]);
+            cudaMemcpyAttributes attr;
+            memset(&attr, 0, sizeof attr);
+            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+            attr.srcLocHint.type = cudaMemLocationTypeDevice;
+            attr.srcLocHint.id = dev;
+            attr.dstLocHint.type = cudaMemLocationTypeHost;
+            size_t idx = 0, fail_idx = SIZE_MAX;
+            cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), count, &attr, &idx, 1,
+                                                 &fail_idx, s.d2h);
+            if (e == cudaSuccess) return;
+            if (fail_idx != SIZE_MAX || (e != cudaErrorNotSupported && e != cudaErrorInvalidValue))
+                ck(e, "cudaMemcpyBatchAsync(landing)");
+            cudaGetLastError();
+            batch_ok = false;  // driver without batch copies: per-copy path from now on
+        }
+        for (size_t i = 0; i < count; ++i) {
+            void *dst, *src;
+            size_t n;
+            get(i, dst, src, n);
+            ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s.d2h), "landing D2H");
+        }
     }
 
     void before_host_read_of(int64_t block_id) {
@@ -963,7 +1059,7 @@ class Plane {
         for (auto &j : jobs) {
             const MsgP &m = std::get<0>(j);
             View dst = std::get<2>(j);
-            if (!dst.buf) dst = View{alloc(m->len, s.comp), 0, m->len};
+            if (!dst.buf) dst = arena_scratch(m->len);
             int32_t *st = status_slot();
             Op op = make_op(SP_OP_OPEN, (uint32_t)dir, std::get<1>(j), m->len, View{m->buf, m->off, m->len}, dst,
                             m->buf, m->tag_off, st);
@@ -986,6 +1082,22 @@ class Plane {
     }
 
     View new_device_buffer(uint64_t n) { return View{alloc(n, s.comp), 0, n}; }
+
+    // Device-only bytes carved from the current small-payload arena (open
+    // destinations of NOPs and token messages): no allocation per message.
+    View arena_scratch(uint64_t n) {
+        uint64_t need = round16(n);
+        if (need > kArenaBytes / 4) return new_device_buffer(n);
+        if (!arena_dev || arena_off + need > arena_dev->size) {
+            if (arena_off) flush();
+            arena_dev = alloc(kArenaBytes, s.comp);
+            arena_off = 0;
+            arena_host.clear();
+        }
+        View v{arena_dev, arena_off, n};
+        arena_off += need;
+        return v;
+    }
 
     void host_sync(int64_t block_id) {
         if (dry) return;
@@ -1219,7 +1331,7 @@ class Engine {
                 View whole = device_buffer(meta.block_id);
                 dst = View{whole.buf, whole.off + inner, meta.nbytes};
             } else if (!plane.dry) {
-                dst = plane.new_device_buffer(meta.nbytes);
+                dst = plane.arena_scratch(meta.nbytes);
             }
             jobs.emplace_back(mi.first, mi.second, dst);
             if (cfg.record_stream) delivered.push_back({meta.seq, meta.base + meta.offset, meta.nbytes, dst});
@@ -1373,7 +1485,7 @@ class Engine {
             auto msgs = plane.seal_bytes({{payload, size}}, D2H, send_iv[D2H], false);
             send(D2H, msgs[0]);
             auto mi = take(D2H);
-            View dst = plane.dry ? View{} : plane.new_device_buffer(size);
+            View dst = plane.dry ? View{} : plane.arena_scratch(size);
             std::vector<std::tuple<MsgP, uint64_t, View>> jobs{{mi.first, mi.second, dst}};
             plane.open_into(jobs, D2H);
             if (cfg.record_stream) d2h_stream.push_back({sq, 0, size, dst});
@@ -1627,6 +1739,59 @@ class Engine {
         device_mem[block_id] = v;
     }
 
+    // The unencrypted baseline of the same trace (the simulator's NoCc
+    // system, simulator.py SystemKind): every swap is one plain
+    // cudaMemcpyAsync between the pinned host block and HBM on the same
+    // copy streams, same ordering rules (a block's swap-in waits for its
+    // last swap-out to land; swap-outs follow earlier swap-ins), no crypto,
+    // no control plane.  Token I/O crosses PCIe from the pinned arena.
+    void plain_replay(const sp_event *ev, uint64_t n, const uint8_t *payloads) {
+        if (plane.dry) return;
+        Plane &pl = plane;
+        std::unordered_map<int64_t, View> dev;
+        std::unordered_map<int64_t, FenceP> landed;
+        std::vector<uint8_t *> pinned;
+        FenceP last_in;
+        for (uint64_t k = 0; k < n; ++k) {
+            const sp_event &e = ev[k];
+            if (e.kind == SP_EV_SWAP_IN) {
+                Block &b = mem.block(e.block);
+                auto it = landed.find(e.block);
+                if (it != landed.end()) pl.wait(pl.s.h2d, it->second);
+                View v{pl.alloc(b.len, pl.s.h2d), 0, b.len};
+                ck(cudaMemcpyAsync(v.ptr(), b.host, b.len, cudaMemcpyHostToDevice, pl.s.h2d), "plain H2D");
+                last_in = pl.record_new(pl.s.h2d);
+                v.buf->use(pl.s.h2d, last_in, ++pl.tick);
+                dev[e.block] = v;
+            } else if (e.kind == SP_EV_SWAP_OUT) {
+                Block &b = mem.block(e.block);
+                auto it = dev.find(e.block);
+                View v = it != dev.end() ? it->second : View{pl.alloc(b.len, pl.s.d2h), 0, b.len};
+                if (last_in) pl.wait(pl.s.d2h, last_in);
+                ck(cudaMemcpyAsync(b.host, v.ptr(), b.len, cudaMemcpyDeviceToHost, pl.s.d2h), "plain D2H");
+                FenceP f = pl.record_new(pl.s.d2h);
+                v.buf->use(pl.s.d2h, f, ++pl.tick);
+                landed[e.block] = f;
+                dev.erase(e.block);
+            } else if (e.kind == SP_EV_SMALL_IO_H2D || e.kind == SP_EV_SMALL_IO_D2H) {
+                const bool h2d = e.kind == SP_EV_SMALL_IO_H2D;
+                cudaStream_t st = h2d ? pl.s.h2d : pl.s.d2h;
+                View v{pl.alloc(e.len, st), 0, e.len};
+                uint8_t *h = pl.ring_reserve(e.len);
+                if (h2d && payloads) memcpy(h, payloads + e.payload, e.len);
+                ck(cudaMemcpyAsync(h2d ? (void *)v.ptr() : (void *)h, h2d ? (const void *)h : (const void *)v.ptr(),
+                                   e.len, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+                   "plain token copy");
+                FenceP f = pl.record_new(st);
+                pl.ring_commit(h, e.len, f);
+                v.buf->use(st, f, ++pl.tick);
+            }
+        }
+        dev.clear();
+        pl.collect();
+        pl.finish_streams();
+    }
+
     // Replay driver (simulator.py:404-426 dispatch, workload event kinds).
     void replay(const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
         for (uint64_t k = 0; k < n; ++k) {
@@ -1870,6 +2035,9 @@ int sp_pipe_app_write(sp_pipe *p, int64_t block, uint64_t offset, const void *da
 int sp_pipe_app_read(sp_pipe *p, int64_t block, uint64_t offset, uint64_t n, void *out) {
     return guarded([&] { p->e->app_read(block, offset, n, static_cast<uint8_t *>(out)); });
 }
+int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads) {
+    return guarded([&] { p->e->plain_replay(ev, n, payloads); });
+}
 int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
     if (done) *done = 0;
     return guarded([&] { p->e->replay(ev, n, payloads, done); });
@@ -1928,6 +2096,19 @@ int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, vo
         if (p->e->pending(H2D)) p->e->drain_gpu();
         p->e->plane.copy_to_host(r.view, bytes);
     });
+}
+int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t *cached) {
+    Plane &pl = p->e->plane;
+    uint64_t r = 0, u = 0;
+    if (!pl.dry) {
+        unsigned long long v = 0;
+        if (cudaMemPoolGetAttribute(pl.pool, cudaMemPoolAttrReservedMemCurrent, &v) == cudaSuccess) r = v;
+        if (cudaMemPoolGetAttribute(pl.pool, cudaMemPoolAttrUsedMemCurrent, &v) == cudaSuccess) u = v;
+    }
+    if (reserved) *reserved = r;
+    if (used) *used = u;
+    if (cached) *cached = pl.cached_bytes;
+    return SP_OK;
 }
 int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches) {
     if (bytes_h2d) *bytes_h2d = p->e->plane.bytes_h2d;

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import weakref
 from typing import Iterable
 
 from . import _native
@@ -226,8 +227,11 @@ class NativeEngine:
         h = ctypes.c_void_p()
         _check(self._lib.sp_pipe_create(ctypes.byref(cfg), bytes(cpu.key.key_bytes), predictor._h, ctypes.byref(h)))
         self._h = h
-        self.cpu = _Endpoint(self, Direction.HOST_TO_DEVICE, cpu.key)
-        self.gpu = _Endpoint(self, Direction.DEVICE_TO_HOST, gpu.key)
+        # views hold a weak reference: no cycle, so the pipe (and its device
+        # memory) is released as soon as the last user drops the engine
+        me = weakref.proxy(self)
+        self.cpu = _Endpoint(me, Direction.HOST_TO_DEVICE, cpu.key)
+        self.gpu = _Endpoint(me, Direction.DEVICE_TO_HOST, gpu.key)
         self._registered = 0
         self._actions: list[Action] = []
         self._delivered: list = []
@@ -329,15 +333,40 @@ class NativeEngine:
         return out.raw[:length]
 
     # -- whole traces in one native call ------------------------------------------------
-    def replay_events(self, events, payloads: bytes = b"") -> int:
+    @staticmethod
+    def encode(events, payloads: bytes = b"") -> tuple:
         """events: sequence of (kind, cls, block, base, len, payload_offset)
-        tuples (SP_EV_* kinds); returns the number of events dispatched."""
+        tuples (SP_EV_* kinds) -> an sp_event array ready for replay_encoded."""
+        import numpy as np
+
+        dt = np.dtype({"names": ["kind", "cls", "block", "base", "len", "payload"],
+                       "formats": [np.int32, np.int32, np.int64, np.uint64, np.uint64, np.uint64],
+                       "offsets": [f[1].offset for f in [(n, getattr(SpEvent, n)) for n, _ in SpEvent._fields_]],
+                       "itemsize": ctypes.sizeof(SpEvent)})
+        arr = np.array(events, dtype=dt) if events else np.zeros(0, dtype=dt)
+        return arr, bytes(payloads)
+
+    def replay_encoded(self, encoded: tuple) -> int:
+        """Dispatch a whole encoded trace segment in one sp_pipe_replay call;
+        returns the number of events dispatched."""
+        arr, payloads = encoded
         self._sync_blocks()
-        arr = (SpEvent * max(1, len(events)))(*[SpEvent(*e) for e in events])
         done = ctypes.c_uint64()
-        rc = self._lib.sp_pipe_replay(self._h, arr, len(events), payloads or None, ctypes.byref(done))
+        rc = self._lib.sp_pipe_replay(self._h, arr.ctypes.data_as(ctypes.POINTER(SpEvent)), len(arr),
+                                      payloads or None, ctypes.byref(done))
         _check(rc)
         return done.value
+
+    def plain_replay_encoded(self, encoded: tuple) -> None:
+        """The same trace segment as plain copies (no crypto, no control
+        plane): the unencrypted-swap baseline on the same streams."""
+        arr, payloads = encoded
+        self._sync_blocks()
+        _check(self._lib.sp_pipe_plain_replay(self._h, arr.ctypes.data_as(ctypes.POINTER(SpEvent)), len(arr),
+                                              payloads or None))
+
+    def replay_events(self, events, payloads: bytes = b"") -> int:
+        return self.replay_encoded(self.encode(events, payloads))
 
     # -- reporting -------------------------------------------------------------------------
     def report(self) -> dict:
@@ -406,4 +435,7 @@ class NativeEngine:
     def plane_stats(self) -> dict:
         a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         self._lib.sp_pipe_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
-        return {"bytes_h2d": a.value, "bytes_d2h": b.value, "launches": c.value}
+        r, u, k = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self._lib.sp_pipe_pool_stats(self._h, ctypes.byref(r), ctypes.byref(u), ctypes.byref(k))
+        return {"bytes_h2d": a.value, "bytes_d2h": b.value, "launches": c.value, "pool_reserved": r.value,
+                "pool_used": u.value, "cached": k.value}

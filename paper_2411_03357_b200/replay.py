@@ -223,9 +223,20 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
         _drain(engine, config)
         mark["t0"] = time.perf_counter()
 
+    segments = None
+    if config.engine == "native" and config.native_dispatch == "replay":
+        # trace -> sp_event arrays before the clock starts (trace loading, not engine work)
+        cut = measure_from if measure_from else 0
+        segments = [engine.encode(*encode_events(trace, blocks, config, 0, cut))] if cut else []
+        segments.append(engine.encode(*encode_events(trace, blocks, config, cut)))
+        mark["t0"] = time.perf_counter()
     try:
-        if config.engine == "native" and config.native_dispatch == "replay":
-            _replay_native(engine, blocks, trace, config, measure_from, at_mark)
+        if segments is not None:
+            for i, seg in enumerate(segments):
+                if i:
+                    at_mark()
+                engine.replay_encoded(seg)
+            engine.finish()
         else:
             _dispatch_all(engine, blocks, trace, config, measure_from, at_mark)
     except Exception as exc:
@@ -235,19 +246,6 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
                             f"{type(exc).__name__}: {exc}")
     wall = time.perf_counter() - mark["t0"]
     return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
-
-
-def _replay_native(engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,
-                   at_mark=None) -> None:
-    """The whole trace through sp_pipe_replay (one native call per segment)."""
-    cut = measure_from if measure_from and at_mark is not None else 0
-    if cut:
-        events, payload = encode_events(trace, blocks, config, 0, cut)
-        engine.replay_events(events, payload)
-        at_mark()
-    events, payload = encode_events(trace, blocks, config, cut)
-    engine.replay_events(events, payload)
-    engine.finish()
 
 
 def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,
@@ -273,6 +271,27 @@ def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConf
         elif isinstance(ev, ComputeEvent):
             pass
     engine.finish()
+
+
+def run_plain_native(trace: Trace, config: ReplayConfig = ReplayConfig(), memory: HostMemory | None = None,
+                     measure_from: int = 0) -> ReplayResult:
+    """NoCc through libsppipe (sp_pipe_plain_replay): the same swaps as plain
+    pinned cudaMemcpyAsync from C++, on the pipe's copy streams — the
+    unencrypted baseline with the same (native) dispatch cost as the
+    encrypted native engine."""
+    from dataclasses import replace
+
+    cfg = replace(config, engine="native", plane="gpu")
+    engine, blocks = build_engine(trace, cfg, memory)
+    pre = engine.encode(*encode_events(trace, blocks, cfg, 0, measure_from)) if measure_from else None
+    seg = engine.encode(*encode_events(trace, blocks, cfg, measure_from))
+    _drain(engine, cfg)
+    if pre is not None:
+        engine.plain_replay_encoded(pre)
+    t0 = time.perf_counter()
+    engine.plain_replay_encoded(seg)
+    wall = time.perf_counter() - t0
+    return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
 
 
 def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: int = 0,

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2411_03357_b200 import workload  # noqa: E402
-from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engine, run_plain  # noqa: E402
+from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engine, run_plain, run_plain_native  # noqa: E402
 
 
 def main() -> None:
@@ -32,7 +32,7 @@ def main() -> None:
     memory = prepare_memory(tr, cfg)
     print(f"prepare_memory {time.perf_counter() - t:.2f}s", flush=True)
     ncfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=0, engine="native")
-    res = {"plain": [], "enc": [], "enc_host_s": [], "native": [], "native_host_s": []}
+    res = {"plain": [], "enc": [], "enc_host_s": [], "native": [], "native_host_s": [], "plain_native": []}
     for _ in range(args.reps):
         r = run_plain(tr, fill="fast", memory=memory)
         res["plain"].append(round(r.swap_gbs, 2))
@@ -48,10 +48,11 @@ def main() -> None:
         res["native"].append(round(r.swap_gbs, 2))
         assert r.engine.report() == rep
         del r
+        res["plain_native"].append(round(run_plain_native(tr, ncfg, memory=memory).swap_gbs, 2))
         if args.empty_cache:
             torch.cuda.empty_cache()
         print(res["plain"][-1], res["enc"][-1], res["enc_host_s"][-1], res["native"][-1], res["native_host_s"][-1],
-              flush=True)
+              res["plain_native"][-1], flush=True)
     res["report"] = {k: rep[k] for k in ("hit", "iv_ahead", "nops", "miss") if k in rep}
     print(json.dumps(res), flush=True)
     if args.no_trace:
