@@ -446,7 +446,10 @@ void key_expand(const uint8_t key[32], uint32_t rk[60]) {
     memcpy(rk, w, 240);  // little-endian words == AES state column words
 }
 
-constexpr int kPinSlots = 4;
+// Pinned descriptor-staging slots per stream: a slot is reused only after the
+// copy that read it completed, so the host can run this many large batches
+// ahead of the device before it blocks.
+constexpr int kPinSlots = 32;
 
 struct Workspace {
     std::mutex mu;  // calls on one stream from several host threads serialise here
@@ -456,9 +459,9 @@ struct Workspace {
     size_t cap_acc = 0;
     std::vector<MsgDev> h_msgs;
     // pinned staging ring for descriptor arrays larger than kInline
-    MsgDev *h_pin[kPinSlots] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t ev_pin[kPinSlots] = {nullptr, nullptr, nullptr, nullptr};
-    bool ev_live[kPinSlots] = {false, false, false, false};
+    MsgDev *h_pin[kPinSlots] = {};
+    cudaEvent_t ev_pin[kPinSlots] = {};
+    bool ev_live[kPinSlots] = {};
     size_t cap_pin = 0;
     int slot = 0;
 };
@@ -513,13 +516,25 @@ uint32_t rows_of(uint64_t len) { return (uint32_t)((((len + 15u) >> 4) + 31u) >>
 // (1,024 L2 requests per warp): fine for big batches (one combine per ~260
 // rows), but for small batches it is the whole cost if 16 warps of one SM do
 // it at once.  So small batches spread few working warps over many SMs
-// (>= 8 rows per warp); big ones use all 16 warps of every SM.
+// (>= 4 rows per warp, measured best on 224 KiB KV batches); big ones use all 16 warps of every SM.
 // Tiny messages (NOP pads, tokens) are latency-bound in their epilogue, so a
 // batch also gets at least one warp per message.
+// Minimum rows per working warp of a small batch (SPGCM_ROWS_PER_WARP
+// overrides, for launch-shape sweeps).
+uint64_t rows_per_warp() {
+    static const uint64_t v = [] {
+        const char *e = getenv("SPGCM_ROWS_PER_WARP");
+        const long x = e ? atol(e) : 0;
+        return x > 0 ? (uint64_t)x : (uint64_t)4;
+    }();
+    return v;
+}
+
 void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
     const uint64_t sms = (uint64_t)ctx->num_sms;
     const uint64_t want_warps =
-        std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / 8u, std::min(nmsgs, rows)), sms * kWarpsPerCta));
+        std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rows_per_warp(), std::min(nmsgs, rows)),
+                                                 sms * kWarpsPerCta));
     warps_used = (uint32_t)((want_warps + sms - 1) / sms);
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }

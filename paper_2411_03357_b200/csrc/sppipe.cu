@@ -404,6 +404,18 @@ struct Op {
     int nr = 0, nw = 0;
 };
 
+// Host->device staging copies gathered and issued as one batch (one
+// cudaMemcpyBatchAsync) with one shared fence, recorded at issue.
+struct CopyBatch {
+    std::vector<void *> dst;
+    std::vector<void *> src;
+    std::vector<size_t> n;
+    std::vector<BufP> keep;     // staging buffers, alive until issued
+    std::vector<FenceP> waits;  // host blocks' landings that must precede the reads
+    FenceP fence;
+    bool empty() const { return n.empty(); }
+};
+
 struct Landing {
     Block *block;
     std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;  // msg, iv, offset in block
@@ -455,6 +467,8 @@ class Plane {
     std::unordered_set<int64_t> landing_blocks;
     std::unordered_map<int64_t, FenceP> host_ready;  // block -> fence after last D2H into it
     std::unordered_map<int64_t, FenceP> h2d_done;    // block -> fence after last H2D from it
+    CopyBatch otf_copies;                             // on-the-fly staging copies (issued at flush)
+    CopyBatch *spec_copies = nullptr;                 // copies of the SpecBatch being built
     // status words of opens
     int32_t *status = nullptr;
     uint64_t status_cap = 1 << 16, status_used = 0;
@@ -661,6 +675,7 @@ class Plane {
 
     void flush() {
         if (dry) return;
+        issue_pending_copies();
         if (arena_dev && arena_off) {
             // the window's arena is sealed/opened by this flush; the next one starts fresh
             if (!arena_host.empty()) {
@@ -835,10 +850,40 @@ class Plane {
         bytes_d2h += total;
     }
 
-    // Landing copies of one flush: one cudaMemcpyBatchAsync (CUDA 12.8+)
-    // instead of a call per block; plain cudaMemcpyAsync where unsupported.
+    // Issue a gathered batch of H2D staging copies on the copy stream.
+    void issue(CopyBatch &cb) {
+        if (cb.empty()) return;
+        std::unordered_set<Fence *> seen;
+        for (auto &f : cb.waits)
+            if (f && seen.insert(f.get()).second) wait(s.h2d, f);
+        copy_batch(s.h2d, true, cb.n.size(), [&](size_t i, void *&dst, void *&src, size_t &n) {
+            dst = cb.dst[i];
+            src = cb.src[i];
+            n = cb.n[i];
+        });
+        record(cb.fence, s.h2d);
+        ++tick;
+        for (auto &b : cb.keep) b->use(s.h2d, cb.fence, tick);
+        cb.dst.clear();
+        cb.src.clear();
+        cb.n.clear();
+        cb.keep.clear();
+        cb.waits.clear();
+        cb.fence.reset();
+    }
+    void issue_pending_copies() {
+        issue(otf_copies);
+        if (spec_copies) issue(*spec_copies);
+    }
+
     template <class F>
     void copy_batch_d2h(size_t count, F &&get) {
+        copy_batch(s.d2h, false, count, get);
+    }
+    // Copies of one flush / batch: one cudaMemcpyBatchAsync (CUDA 12.8+)
+    // instead of a call per copy; plain cudaMemcpyAsync where unsupported.
+    template <class F>
+    void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
         static bool batch_ok = true;
         if (count > 1 && batch_ok) {
             std::vector<void *> dsts(count), srcs(count);
@@ -847,15 +892,16 @@ class Plane {
             cudaMemcpyAttributes attr;
             memset(&attr, 0, sizeof attr);
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.srcLocHint.type = cudaMemLocationTypeDevice;
-            attr.srcLocHint.id = dev;
-            attr.dstLocHint.type = cudaMemLocationTypeHost;
+            attr.srcLocHint.type = h2d ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
+            attr.srcLocHint.id = h2d ? 0 : dev;
+            attr.dstLocHint.type = h2d ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
+            attr.dstLocHint.id = h2d ? dev : 0;
             size_t idx = 0, fail_idx = SIZE_MAX;
             cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), count, &attr, &idx, 1,
-                                                 &fail_idx, s.d2h);
+                                                 &fail_idx, st);
             if (e == cudaSuccess) return;
             if (fail_idx != SIZE_MAX || (e != cudaErrorNotSupported && e != cudaErrorInvalidValue))
-                ck(e, "cudaMemcpyBatchAsync(landing)");
+                ck(e, "cudaMemcpyBatchAsync");
             cudaGetLastError();
             batch_ok = false;  // driver without batch copies: per-copy path from now on
         }
@@ -863,7 +909,7 @@ class Plane {
             void *dst, *src;
             size_t n;
             get(i, dst, src, n);
-            ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s.d2h), "landing D2H");
+            ck(cudaMemcpyAsync(dst, src, n, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st), "batched copy");
         }
     }
 
@@ -874,17 +920,22 @@ class Plane {
     // -- seals ----------------------------------------------------------------------------
     // H2D the plaintext of `block` [inner+off, +n) per span into one staging
     // buffer; returns the staging buffer (payload views at off-first, tags after).
-    BufP stage_h2d(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, FenceP &done) {
+    // The copy joins `cb` (issued with its batch); `done` is the batch fence.
+    BufP stage_h2d(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, FenceP &done,
+                   CopyBatch &cb) {
         before_host_read_of(b.id);
         uint64_t total = 0;
         for (auto &sp : spans) total += sp.second;
         uint64_t first = spans[0].first;
         auto it = host_ready.find(b.id);
-        if (it != host_ready.end() && it->second) wait(s.h2d, it->second);
+        if (it != host_ready.end() && it->second) cb.waits.push_back(it->second);
         BufP buf = alloc(round16(total) + kTag * spans.size(), s.h2d);
-        ck(cudaMemcpyAsync(buf->ptr, b.host + inner + first, total, cudaMemcpyHostToDevice, s.h2d), "swap-in H2D");
-        done = record_new(s.h2d);
-        buf->use(s.h2d, done, ++tick);
+        if (!cb.fence) cb.fence = new_fence();
+        cb.dst.push_back(buf->ptr);
+        cb.src.push_back(b.host + inner + first);
+        cb.n.push_back(total);
+        cb.keep.push_back(buf);
+        done = cb.fence;
         h2d_done[b.id] = done;
         bytes_h2d += total;
         return buf;
@@ -903,7 +954,7 @@ class Plane {
             return msgs;
         }
         FenceP done;
-        BufP buf = stage_h2d(b, inner, spans, done);
+        BufP buf = stage_h2d(b, inner, spans, done, otf_copies);
         uint64_t first = spans[0].first, total = 0;
         for (auto &sp : spans) total += sp.second;
         for (size_t i = 0; i < spans.size(); ++i) {
@@ -930,8 +981,12 @@ class Plane {
         uint64_t bytes = 0;
         FenceP ready;
         FenceP last_copy;
+        CopyBatch copies;
         explicit SpecBatch(Plane *pl) : p(pl) {
             if (!p->dry) ready = p->new_fence();
+        }
+        ~SpecBatch() {
+            if (p->spec_copies == &copies) p->spec_copies = nullptr;
         }
         std::vector<MsgP> add(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
                               uint64_t iv0) {
@@ -946,7 +1001,8 @@ class Plane {
                 return msgs;
             }
             FenceP done;
-            BufP buf = p->stage_h2d(b, inner, spans, done);
+            p->spec_copies = &copies;  // a flush while this batch is built issues its copies first
+            BufP buf = p->stage_h2d(b, inner, spans, done, copies);
             last_copy = done;
             uint64_t first = spans[0].first, total = 0;
             for (auto &sp : spans) total += sp.second;
@@ -974,6 +1030,7 @@ class Plane {
         }
         void launch() {
             if (p->dry || items.empty()) return;
+            p->issue(copies);
             p->wait(p->s.spec, last_copy);
             ck_sp(sp_seal_batch(p->ctx, items.data(), (int)items.size(), p->s.spec), "sp_seal_batch(spec)");
             ++p->launches;
