@@ -412,7 +412,14 @@ def run_gpu(args) -> None:
                      "unit": "GB/s", "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 4),
                      "traffic": ncu_traffic_per_launch(), "peak_kind": peaks_kind,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "note": "k_gcm is bound by the shared-memory LSU pipe, not HBM: see int_roofline"},
+                     "note": "k_gcm is bound by the shared-memory LSU pipe, not HBM: see int_roofline",
+                     "north_star": {
+                         "definition": "BASELINE north star: the slower of the integer-op bound and read+write "
+                                       "bytes at the HBM peak, in payload GB/s",
+                         "bound_gbs": round(min(lsu_bound, alu_bound, peaks.get("hbm_gbs", 6650.0) / 2), 1),
+                         "achieved_gbs": round(per_gpu_payload, 2),
+                         "frac": round(per_gpu_payload / min(lsu_bound, alu_bound,
+                                                             peaks.get("hbm_gbs", 6650.0) / 2), 4)}},
         "int_roofline": {"bound": "lsu (T-table + GHASH lookups)", "payload_gbs": round(per_gpu_payload, 2),
                          "lsu_bound_gbs": round(lsu_bound, 1), "alu_bound_gbs": round(alu_bound, 1),
                          "frac_of_lsu_bound": round(per_gpu_payload / lsu_bound, 4),

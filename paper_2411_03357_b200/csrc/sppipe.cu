@@ -451,7 +451,8 @@ class Plane {
     // small-payload arena
     std::vector<uint8_t> arena_host;
     BufP arena_dev;
-    uint64_t arena_off = 0;
+    uint64_t arena_off = 0;      // payloads (copied from the host) grow up from 0
+    uint64_t arena_low = 0;      // device-only scratch grows down from the end
     // Pinned host staging ring for small payloads (arena flushes, token
     // copies): slots are taken in order and handed back when the fence of
     // the copy that read/wrote them has passed; one cudaHostAlloc per process.
@@ -676,7 +677,7 @@ class Plane {
     void flush() {
         if (dry) return;
         issue_pending_copies();
-        if (arena_dev && arena_off) {
+        if (arena_dev && (arena_off || arena_low < arena_dev->size)) {
             // the window's arena is sealed/opened by this flush; the next one starts fresh
             if (!arena_host.empty()) {
                 const uint64_t n = arena_host.size();
@@ -691,6 +692,7 @@ class Plane {
             arena_host.clear();
             arena_dev.reset();
             arena_off = 0;
+            arena_low = 0;
         }
         if (!ops.empty()) {
             std::vector<Op> q;
@@ -1085,12 +1087,7 @@ class Plane {
             m->nop = nop;
             if (!dry) {
                 uint64_t need = round16(n) + kTag;
-                if (!arena_dev || arena_off + need > arena_dev->size) {
-                    if (arena_off) flush();
-                    arena_dev = alloc(std::max(kArenaBytes, need), s.comp);
-                    arena_off = 0;
-                    arena_host.clear();
-                }
+                if (!arena_dev || arena_off + need > arena_low) new_arena(need);
                 uint64_t o = arena_off;
                 arena_off += need;
                 if (arena_host.size() < o + n) arena_host.resize(o + n, 0);
@@ -1145,15 +1142,17 @@ class Plane {
     View arena_scratch(uint64_t n) {
         uint64_t need = round16(n);
         if (need > kArenaBytes / 4) return new_device_buffer(n);
-        if (!arena_dev || arena_off + need > arena_dev->size) {
-            if (arena_off) flush();
-            arena_dev = alloc(kArenaBytes, s.comp);
-            arena_off = 0;
-            arena_host.clear();
-        }
-        View v{arena_dev, arena_off, n};
-        arena_off += need;
-        return v;
+        if (!arena_dev || arena_off + need > arena_low) new_arena(need);
+        arena_low -= need;
+        return View{arena_dev, arena_low, n};
+    }
+    // Seal the current arena's window (flush) and start a fresh arena.
+    void new_arena(uint64_t need) {
+        if (arena_dev) flush();
+        arena_dev = alloc(std::max(kArenaBytes, need), s.comp);
+        arena_off = 0;
+        arena_low = arena_dev->size;
+        arena_host.clear();
     }
 
     void host_sync(int64_t block_id) {

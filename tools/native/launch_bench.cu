@@ -4,6 +4,8 @@
 #include <vector>
 #include "spgcm.h"
 
+__global__ void k_empty() {}
+
 int main() {
     uint8_t key[32];
     for (int i = 0; i < 32; ++i) key[i] = (uint8_t)i;
@@ -17,6 +19,17 @@ int main() {
     cudaMalloc(&out, 64u << 20);
     cudaMalloc(&tags, 16 * 64);
     cudaMemset(buf, 7, 64u << 20);
+    {
+        for (int w = 0; w < 20; ++w) k_empty<<<148, 512, 0, s>>>();
+        cudaEvent_t a, b;
+        cudaEventCreate(&a); cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        for (int r = 0; r < 200; ++r) k_empty<<<148, 512, 0, s>>>();
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        printf("empty kernel 148x512: %8.2f us/launch\n", ms * 1000 / 200);
+    }
     for (size_t n : sizes) {
         for (int nmsg : {1, 8, 32}) {
             if (n * nmsg > (64u << 20)) continue;

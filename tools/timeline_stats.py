@@ -68,6 +68,12 @@ def main(path: str) -> None:
             r[2] = max(r[2], e["dur"])
     for name, (n, dur, mx) in sorted(rt.items(), key=lambda x: -x[1][1])[:10]:
         print(f"runtime {name}: n={n} total {dur / 1e3:.1f} ms max {mx / 1e3:.2f} ms")
+    api = [(e["ts"], e["ts"] + e["dur"]) for e in ev if e.get("ph") == "X" and e.get("cat") == "cuda_runtime"]
+    if api:
+        a0 = min(a for a, _ in api)
+        a1 = max(b for _, b in api)
+        print(f"host API span {(a1 - a0) / 1e3:.2f} ms, API busy {union(api) / 1e3:.2f} ms, "
+              f"GPU tail after last API call {(t1 - a1) / 1e3:.2f} ms")
     long = sorted(((e["ts"] - t0) / 1e3, e["dur"] / 1e3, e["name"]) for e in ev
                   if e.get("ph") == "X" and e.get("cat") == "cuda_runtime" and e["dur"] > 1000)
     print("runtime calls > 1 ms (at ms, ms, name):", [(round(a, 1), round(b, 1), c) for a, b, c in long[:40]])
