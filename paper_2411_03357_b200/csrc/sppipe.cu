@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "spgcm.h"
+#include "spguard.h"
 #include "sppipe.h"
 #include "sppred.hpp"
 
@@ -159,6 +160,8 @@ class HostMem {
     }
     static bool overlaps(uint64_t ab, uint64_t al, uint64_t bb, uint64_t bl) { return ab < bb + bl && bb < ab + al; }
 
+    bool hw = false;  // mirror write guards with mprotect'ed pages (libspguard)
+
     void install_write_guard(uint64_t base, uint64_t len, int64_t owner) {
         for (auto &kv : write_guards) {
             const WriteGuard &g = kv.second;
@@ -167,8 +170,16 @@ class HostMem {
                                std::to_string(g.owner));
         }
         write_guards[owner] = WriteGuard{base, len, owner, true};
+        if (hw) {
+            auto bi = block_at(base, len);
+            if (bi.first->host && spg_protect(bi.first->host + bi.second, len, owner) != SPG_OK)
+                throw std::runtime_error("spg_protect failed (errno " + std::to_string(spg_errno()) + ")");
+        }
     }
-    void release_write_guard(int64_t owner) { write_guards.erase(owner); }
+    void release_write_guard(int64_t owner) {
+        write_guards.erase(owner);
+        if (hw) spg_release(owner);
+    }
     void install_read_guard(uint64_t base, uint64_t len, int64_t task) {
         for (auto &kv : read_guards)
             if (overlaps(base, len, kv.second.first, kv.second.second))
@@ -1290,6 +1301,10 @@ class Engine {
     Engine(const sp_pipe_config &c, const uint8_t key[32], Predictor *p)
         : cfg(c), plane(c.dry != 0, key, c.batch_bytes ? c.batch_bytes : (64ull << 20), c.reserve_bytes), pred(p),
           val(mem, c.window) {
+        if (c.hw_guards) {
+            if (spg_init() != SPG_OK) throw std::runtime_error("spg_init failed");
+            mem.hw = true;
+        }
         send_iv[H2D] = c.initial_h2d_iv;
         send_iv[D2H] = c.initial_d2h_iv;
         recv_iv[H2D] = c.initial_h2d_iv;
@@ -1564,7 +1579,7 @@ class Engine {
         for (auto &kv : mem.write_guards)
             if (kv.second.active && HostMem::overlaps(base, n, kv.second.base, kv.second.len)) owners.push_back(kv.first);
         for (int64_t o : owners) {
-            mem.write_guards.erase(o);
+            mem.release_write_guard(o);
             val.on_write_fault(o);
         }
         if (b.host) memcpy(b.host + offset, data, n);
@@ -1636,7 +1651,26 @@ class Engine {
         }
     }
 
+    // Stores that bypassed app_write into mprotect'ed guarded pages: the
+    // SIGSEGV handler queued their owners; turn them into write faults
+    // (memory.poll_hw_faults -> validator invalidation) before any verdict.
+    void poll_hw_faults() {
+        int64_t owners[256];
+        for (;;) {
+            int n = spg_drain(owners, 256);
+            for (int i = 0; i < n; ++i) {
+                auto it = mem.write_guards.find(owners[i]);
+                if (it == mem.write_guards.end() || !it->second.active) continue;
+                mem.release_write_guard(owners[i]);
+                counters[C_WRITE_FAULTS]++;
+                val.on_write_fault(owners[i]);
+            }
+            if (n < 256) break;
+        }
+    }
+
     void complete_spec_tasks() {
+        if (mem.hw) poll_hw_faults();
         if (spec_queue.empty()) return;
         Plane::SpecBatch batch(&plane);
         try {

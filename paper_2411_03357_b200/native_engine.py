@@ -221,6 +221,7 @@ class NativeEngine:
         cfg.speculate, cfg.defer_swap_decrypt, cfg.record_stream = c.speculate, c.defer_swap_decrypt, c.record_stream
         cfg.strict_auth, cfg.reference_compat = c.strict_auth, c.reference_compat
         cfg.dry = c.plane == "dry"
+        cfg.hw_guards = bool(getattr(memory, "hw_guards", False))
         cfg.initial_h2d_iv, cfg.initial_d2h_iv = cpu.send_iv, gpu.send_iv
         cfg.batch_bytes = 64 << 20
         cfg.reserve_bytes = reserve_bytes

@@ -85,3 +85,57 @@ def test_hw_guard_on_pinned_memory_gpu():
     out = subprocess.run([sys.executable, "-c", GPU_SCRIPT], capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "hw guards ok 1" in out.stdout
+
+
+NATIVE_SCRIPT = textwrap.dedent('''
+    import sys
+    sys.path.insert(0, %r)
+    from paper_2411_03357_b200 import guards
+    from paper_2411_03357_b200.channel import new_channel
+    from paper_2411_03357_b200.engine import CopyRequest, EngineConfig
+    from paper_2411_03357_b200.memory import HostMemory, ModelLayer, prng_fill
+    from paper_2411_03357_b200.native_engine import NativeEngine, NativePredictor
+    from paper_2411_03357_b200.predictor import ModelProfile, TransferClass
+
+    W = TransferClass.MODEL_WEIGHTS
+    mem = HostMemory(pinned=PINNED, hw_guards=True)
+    cpu, gpu = new_channel(seed=1)
+    pred = NativePredictor(ModelProfile("m", 256 * 1024, 4096))
+    eng = NativeEngine(mem, cpu, gpu, pred, EngineConfig(leeway=0, plane=PLANE))
+    blocks = [mem.alloc(ModelLayer(i), 256 * 1024, prng_fill(i)) for i in range(4)]
+    for b in blocks:
+        pred.observe_swap_out(b.id)
+    req = lambda b: CopyRequest("h2d", b.base, b.len, W, block_id=b.id)
+    # two FIFO batches lock the pattern; the sync after the second queues
+    # encrypt-ahead of block 3, labeled (and guarded) at the next entry
+    for b in blocks[:2]:
+        eng.copy_h2d(req(b))
+        eng.sync()
+        eng.copy_d2h(CopyRequest("d2h", b.base, b.len, W, block_id=b.id))
+    assert guards.active() >= 1, guards.active()
+    target = blocks[2]
+    target.data[100000] ^= 0xFF          # a direct store: no app_write, no HostMemory.write
+    assert guards.faults() == 1
+    h = eng.copy_h2d(req(target))        # the entry point turns the trap into an invalidation
+    assert h.verdict.value == "stale", h.verdict
+    assert eng.report()["write_faults"] == 1
+    eng.sync()
+    eng.finish()
+    assert guards.active() == 0
+    print("native hw guards ok", guards.faults())
+''' % ROOT)
+
+
+def test_native_hw_guard_invalidates_on_direct_store():
+    script = NATIVE_SCRIPT.replace("PINNED", "False").replace("PLANE", '"dry"')
+    out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "native hw guards ok 1" in out.stdout
+
+
+@pytest.mark.gpu
+def test_native_hw_guard_gpu():
+    script = NATIVE_SCRIPT.replace("PINNED", "True").replace("PLANE", '"gpu"')
+    out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "native hw guards ok 1" in out.stdout
