@@ -66,6 +66,12 @@ __device__ __forceinline__ void fill_tables(uint8_t *sm, const KParams &p) {
     }
 }
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ uint4 len_block(uint64_t len) {
     const uint64_t bits = len * 8u;
     return make_uint4(0u, 0u, bswap32((uint32_t)(bits >> 32)), bswap32((uint32_t)bits));
@@ -116,8 +122,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
     if (warp >= p.warps_used) return;
     const uint64_t gw = (uint64_t)blockIdx.x * p.warps_used + warp;
     const uint64_t nw = (uint64_t)gridDim.x * p.warps_used;
-    uint64_t g = p.row_begin + (total * gw) / nw;
-    const uint64_t g_end = p.row_begin + (total * (gw + 1)) / nw;
+    uint64_t g, g_end;
+    if (total * nw <= 0xffffffffull) {  // 32-bit division (the common case; 64-bit is a long software routine)
+        const uint32_t t32 = (uint32_t)total, w32 = (uint32_t)gw, n32 = (uint32_t)nw;
+        g = p.row_begin + (t32 * w32) / n32;
+        g_end = p.row_begin + (t32 * (w32 + 1u)) / n32;
+    } else {
+        g = p.row_begin + (total * gw) / nw;
+        g_end = p.row_begin + (total * (gw + 1)) / nw;
+    }
     if (g >= g_end) return;
 
     const MsgDev *msgs = p.nmsgs <= kInline ? p.inl : p.msgs;
@@ -206,14 +219,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
         } else {
             uint32_t *acc = p.acc + (size_t)m * 8u;
+            // XOR-accumulate (order-free, so deterministic) and count rows:
+            // the count is a release/acquire RMW, no full fence.
             if (lane < 4) atomicXor(acc + lane, word_of(w, lane));
-            __threadfence();
             __syncwarp();
             uint32_t old = 0;
-            if (lane == 0) old = atomicAdd(acc + 4, (uint32_t)(t_b - t_a));
+            if (lane == 0) old = atom_add_acq_rel_gpu(acc + 4, (uint32_t)(t_b - t_a));
             old = __shfl_sync(0xffffffffu, old, 0);
             if (old + (uint32_t)(t_b - t_a) == md.rows) {
-                __threadfence();
+                __syncwarp();
                 uint32_t v = 0;
                 if (lane < 4) v = atomicExch(acc + lane, 0u);
                 if (lane == 0) atomicExch(acc + 4, 0u);
