@@ -336,7 +336,7 @@ class Validator {
 
 // ---- data plane -----------------------------------------------------------------------
 struct Streams {
-    cudaStream_t comp, spec, h2d, d2h, land;
+    cudaStream_t comp, spec, h2d, d2h, land, host;  // host: ordered application writes (host functions)
 };
 
 struct DevicePool {
@@ -367,7 +367,7 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[5] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land};
+    cudaStream_t *all[6] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host};
     for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
     g_streams[dev] = s;
     return s;
@@ -849,6 +849,8 @@ class Plane {
             if (p.block != last) {
                 auto it = h2d_done.find(p.block->id);
                 if (it != h2d_done.end() && it->second) wait(s.d2h, it->second);
+                auto hr = host_ready.find(p.block->id);  // an ordered app write (same stream: no-op otherwise)
+                if (hr != host_ready.end() && hr->second) wait(s.d2h, hr->second);
                 last = p.block;
             }
         }
@@ -1176,17 +1178,41 @@ class Plane {
         auto it = host_ready.find(block_id);
         if (it != host_ready.end() && it->second) ck(cudaEventSynchronize(it->second->ev), "host_ready sync");
     }
-    void before_host_write(int64_t block_id) {
-        if (dry) return;
-        flush();
-        for (auto *t : {&h2d_done, &host_ready}) {
-            auto it = t->find(block_id);
-            if (it != t->end() && it->second) ck(cudaEventSynchronize(it->second->ev), "host write sync");
+    // An application write into a host block, ordered on the device
+    // timeline instead of by a host wait: stream-ordered copies from the
+    // pinned staging ring into the block run after every issued landing
+    // into the block and every issued H2D read of it, and later H2D reads /
+    // landings / app reads order after it through host_ready.
+    void ordered_host_write(Block &b, uint64_t offset, const uint8_t *data, uint64_t n) {
+        if (!b.host) return;
+        if (dry) {
+            memcpy(b.host + offset, data, n);
+            return;
         }
+        flush();  // issue pending landings and staging copies first
+        enqueue_host_write(b, offset, data, n, h2d_done[b.id]);
+    }
+    // On its own stream, so only work on this block waits for the callback.
+    void enqueue_host_write(Block &b, uint64_t offset, const uint8_t *data, uint64_t n, const FenceP &reads) {
+        if (reads) wait(s.host, reads);
+        auto lr = host_ready.find(b.id);  // the block's last landing (or earlier app write)
+        if (lr != host_ready.end() && lr->second) wait(s.host, lr->second);
+        // staged in the pinned ring and bounced through HBM by two async DMA
+        // copies (host-to-host cudaMemcpyAsync would block the caller until
+        // the stream drains; host functions stall on the callback thread)
+        uint8_t *h = ring_reserve(n);
+        memcpy(h, data, n);
+        BufP tmp = alloc(n, s.host);
+        ck(cudaMemcpyAsync(tmp->ptr, h, n, cudaMemcpyHostToDevice, s.host), "app write H2D");
+        ck(cudaMemcpyAsync(b.host + offset, tmp->ptr, n, cudaMemcpyDeviceToHost, s.host), "app write D2H");
+        FenceP f = record_new(s.host);
+        ring_commit(h, n, f);
+        tmp->use(s.host, f, ++tick);
+        host_ready[b.id] = f;
     }
     void finish_streams() {
         flush();
-        cudaStream_t all[5] = {s.comp, s.spec, s.land, s.h2d, s.d2h};
+        cudaStream_t all[6] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
     void finish() {
@@ -1570,7 +1596,6 @@ class Engine {
         complete_spec_tasks();
         Block &b = mem.block(block_id);
         resolve_decrypts_over(b.base + offset, n, true);
-        plane.before_host_write(block_id);
         if (offset + n > b.len)
             throw BoundsErr("access (" + std::to_string(offset) + ", " + std::to_string(n) + ") outside block " +
                             std::to_string(b.id) + " of " + std::to_string(b.len) + " bytes");
@@ -1582,7 +1607,10 @@ class Engine {
             mem.release_write_guard(o);
             val.on_write_fault(o);
         }
-        if (b.host) memcpy(b.host + offset, data, n);
+        plane.ordered_host_write(b, offset, data, n);
+        // with page guards, a record labeled after this call must not see the
+        // deferred store land on its freshly protected pages: complete it now
+        if (mem.hw) plane.host_sync(block_id);
         counters[C_WRITE_FAULTS] += (int64_t)owners.size();
         return (int64_t)owners.size();
     }
@@ -1858,11 +1886,20 @@ class Engine {
                 auto it = dev.find(e.block);
                 View v = it != dev.end() ? it->second : View{pl.alloc(b.len, pl.s.d2h), 0, b.len};
                 if (last_in) pl.wait(pl.s.d2h, last_in);
+                auto lt = landed.find(e.block);  // an earlier app write into the block
+                if (lt != landed.end()) pl.wait(pl.s.d2h, lt->second);
                 ck(cudaMemcpyAsync(b.host, v.ptr(), b.len, cudaMemcpyDeviceToHost, pl.s.d2h), "plain D2H");
                 FenceP f = pl.record_new(pl.s.d2h);
                 v.buf->use(pl.s.d2h, f, ++pl.tick);
                 landed[e.block] = f;
                 dev.erase(e.block);
+            } else if (e.kind == SP_EV_APP_WRITE) {
+                // the same ordered host write the engine performs (after the block's pending DMA)
+                Block &b = mem.block(e.block);
+                auto lt = landed.find(e.block);
+                if (lt != landed.end()) pl.host_ready[e.block] = lt->second;
+                pl.enqueue_host_write(b, e.base, payloads + e.payload, e.len, last_in);
+                landed[e.block] = pl.host_ready[e.block];
             } else if (e.kind == SP_EV_SMALL_IO_H2D || e.kind == SP_EV_SMALL_IO_D2H) {
                 const bool h2d = e.kind == SP_EV_SMALL_IO_H2D;
                 cudaStream_t st = h2d ? pl.s.h2d : pl.s.d2h;
