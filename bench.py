@@ -500,6 +500,14 @@ def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1)
            "note": "whole-job swap GB/s (sum over ranks / max time); tokens/s ratio == swap throughput ratio "
                    "(same trace, same batch); random payload"}
     out.update(trace_compare(tr, cfg, dist, dev_sync, world, args.offload_reps))
+    # the no-speculation system on the same trace (the simulator's SyncCc):
+    # every swap sealed and opened on the fly, synchronous host decrypts
+    from dataclasses import replace
+
+    sync_cfg = replace(cfg, system="synccc")
+    sync = trace_compare(tr, sync_cfg, dist, dev_sync, world, max(1, args.offload_reps // 2))
+    out["synccc_gbs"] = sync["encrypted_gbs"]
+    out["synccc_ratio"] = round(sync["encrypted_gbs"] / out["plain_gbs"], 4)
     return out
 
 
