@@ -225,6 +225,11 @@ int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *pa
  * copy streams, same ordering rules, no crypto; returns when the device is idle. */
 int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads);
 int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done);
+/* Test hook (the reference's Channel(test_hooks=True).hook_corrupt_in_flight,
+ * channel.py:263-273): XOR `mask` into byte `byte_index` of the index-th
+ * message still in flight on the `dir` lane (sent, not yet received),
+ * stream-ordered after its seal.  The receiver's open must then fail. */
+int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_index, uint8_t mask);
 
 /* report(): counters in the order of sp_pipe_counter_name(i); n = count. */
 int sp_pipe_report(sp_pipe *p, int64_t *out, int32_t cap, int32_t *n);

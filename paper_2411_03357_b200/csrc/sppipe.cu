@@ -1942,6 +1942,8 @@ class Engine {
 
 using namespace sppipe;
 
+__global__ void k_xor_byte(uint8_t *p, uint8_t mask) { *p ^= mask; }
+
 struct sp_pred {
     Predictor p;
     explicit sp_pred(const PredConfig &c) : p(c) {}
@@ -2168,6 +2170,21 @@ int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8
 int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
     if (done) *done = 0;
     return guarded([&] { p->e->replay(ev, n, payloads, done); });
+}
+int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_index, uint8_t mask) {
+    return guarded([&] {
+        Engine &e = *p->e;
+        auto &q = e.lanes[dir & 1].queue;
+        if (index >= q.size()) throw KeyErr("no in-flight message " + std::to_string(index));
+        const MsgP &m = q[(size_t)index];
+        if (byte_index >= m->len) throw ValueErr("byte index outside the message");
+        if (e.plane.dry || !m->buf) return;
+        e.plane.flush();  // its seal is issued; the flip is ordered after it on its producer stream
+        cudaStream_t st = m->ready && m->ready->recorded ? m->ready->stream : e.plane.s.comp;
+        k_xor_byte<<<1, 1, 0, st>>>(m->buf->ptr + m->off + byte_index, mask);
+        ck(cudaGetLastError(), "k_xor_byte");
+        ck(cudaStreamSynchronize(st), "test corrupt");
+    });
 }
 int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done) {
     *done = (seq >= 1 && seq <= p->e->next_seq && !p->e->suspended_seqs.count(seq)) ? 1 : 0;

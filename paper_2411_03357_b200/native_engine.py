@@ -318,6 +318,11 @@ class NativeEngine:
     def finish(self) -> None:
         _check(self._lib.sp_pipe_finish(self._h))
 
+    def test_corrupt_in_flight(self, direction: Direction, index: int, byte_index: int = 0, bit: int = 0) -> None:
+        """hook_corrupt_in_flight (channel.py:263-273): flip one bit of an
+        in-flight (sent, not yet received) message."""
+        _check(self._lib.sp_pipe_test_corrupt(self._h, direction.value, index, byte_index, 1 << bit))
+
     def flush(self, wait: bool = False) -> None:
         """Issue queued launches now (and with `wait`, drain the device)."""
         _check(self._lib.sp_pipe_flush(self._h, 1 if wait else 0))

@@ -274,3 +274,49 @@ def test_native_app_read_sees_swapped_out_bytes_gpu():
     assert got == dev.cpu().numpy().tobytes()
     assert eng.report()["read_faults"] == 1
     eng.finish()
+
+
+def _one_block_engine(plane: str, strict: bool = False):
+    from paper_2411_03357_b200.channel import new_channel
+    from paper_2411_03357_b200.engine import EngineConfig
+    from paper_2411_03357_b200.memory import HostMemory, ModelLayer, prng_fill
+    from paper_2411_03357_b200.native_engine import NativeEngine, NativePredictor
+
+    mem = HostMemory(pinned=None if plane == "gpu" else False)
+    cpu, gpu = new_channel(seed=9)
+    pred = NativePredictor(ModelProfile("m", 70_000, 64))
+    eng = NativeEngine(mem, cpu, gpu, pred, EngineConfig(plane=plane, strict_auth=strict))
+    b = mem.alloc(ModelLayer(1), 70_000, prng_fill(4))
+    pred.observe_swap_out(b.id)
+    return eng, b
+
+
+def test_native_test_hook_bounds():
+    from paper_2411_03357_b200.channel import Direction
+
+    eng, _ = _one_block_engine("dry")
+    with pytest.raises(KeyError):
+        eng.test_corrupt_in_flight(Direction.HOST_TO_DEVICE, 0)
+
+
+@pytest.mark.gpu
+def test_native_tamper_detected_gpu():
+    """A bit flipped in an in-flight H2D message (after its seal, before the
+    receiver's open) fails authentication: finish raises AuthError
+    (GcmAuthError) and the schedule is otherwise untouched."""
+    from paper_2411_03357_b200.channel import Direction
+    from paper_2411_03357_b200.engine import CopyRequest
+    from paper_2411_03357_b200.gcm import GcmAuthError
+    from paper_2411_03357_b200.predictor import TransferClass
+
+    eng, b = _one_block_engine("gpu")
+    eng.copy_h2d(CopyRequest("h2d", b.base, b.len, TransferClass.MODEL_WEIGHTS, block_id=b.id))
+    eng.test_corrupt_in_flight(Direction.HOST_TO_DEVICE, 0, byte_index=1234, bit=3)
+    eng.sync()
+    with pytest.raises(GcmAuthError):
+        eng.finish()
+    # an untouched run of the same request authenticates
+    eng2, b2 = _one_block_engine("gpu")
+    eng2.copy_h2d(CopyRequest("h2d", b2.base, b2.len, TransferClass.MODEL_WEIGHTS, block_id=b2.id))
+    eng2.sync()
+    eng2.finish()
