@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import random
 import weakref
 from typing import Iterable
 
@@ -234,6 +235,7 @@ class NativeEngine:
         self.cpu = _Endpoint(me, Direction.HOST_TO_DEVICE, cpu.key)
         self.gpu = _Endpoint(me, Direction.DEVICE_TO_HOST, gpu.key)
         self._registered = 0
+        self._rng = random.Random(0xC0DE)
         self._actions: list[Action] = []
         self._delivered: list = []
         self._d2h: list = []
@@ -296,9 +298,7 @@ class NativeEngine:
         if direction not in ("h2d", "d2h"):
             raise ValueError(f"unknown direction {direction!r}")
         if payload is None:
-            import random
-
-            payload = random.Random(0xC0DE).randbytes(size)
+            payload = self._rng.randbytes(size)  # engine.py:401, one generator per engine
         _check(self._lib.sp_pipe_small_io(self._h, 0 if direction == "h2d" else 1, bytes(payload), size))
 
     def sync(self) -> None:
