@@ -108,8 +108,15 @@ __device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams 
 __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParams p) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
-    fill_tables(sm, p);
+    // let a dependent launch on this stream be scheduled now: its CTAs take
+    // idle SMs and fill their tables while this grid runs (they read no data
+    // before their own griddepcontrol.wait, which waits for this grid to end)
+    asm volatile("griddepcontrol.launch_dependents;");
+    fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
     __syncthreads();
+    // programmatic dependent launch: everything below may read what the
+    // previous kernel on this stream wrote (messages, accumulators)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     const int lane = threadIdx.x & 31;
     const uint32_t lct = (uint32_t)lane * 4u;                  // T tables
@@ -576,7 +583,25 @@ int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_e
     p.row_end = row_end;
     int grid = 1;
     launch_shape(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
-    k_gcm<<<grid, kThreads, kSmemBytes, s>>>(p);
+    // Programmatic dependent launch: a launch that directly follows another
+    // kernel on the stream starts (and fills its shared-memory tables)
+    // while that kernel's last CTAs drain; it waits in griddepcontrol.wait
+    // before touching any data.  SPGCM_PDL=0 disables.
+    static const bool pdl = [] {
+        const char *e = getenv("SPGCM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm, p), "k_gcm launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     SP_CUDA(cudaGetLastError(), "k_gcm launch");
     return SP_OK;
