@@ -180,19 +180,36 @@ class HostMem {
         write_guards.erase(owner);
         if (hw) spg_release(owner);
     }
-    void install_read_guard(uint64_t base, uint64_t len, int64_t task) {
-        for (auto &kv : read_guards)
-            if (overlaps(base, len, kv.second.first, kv.second.second))
-                throw GuardErr("read guard (" + hex(base) + ", " + std::to_string(len) + ") overlaps task " +
-                               std::to_string(kv.first));
-        read_guards[task] = {base, len};
-    }
-    void release_read_guard(int64_t task) { read_guards.erase(task); }
+    // Read guards are disjoint (install rejects overlaps), so an index by
+    // base answers overlap queries in O(log n + k); results come back in task
+    // id order = the reference's dict insertion order (memory.py:244-259).
+    std::map<uint64_t, std::pair<uint64_t, int64_t>> rg_by_base;  // base -> (len, task)
+
     std::vector<int64_t> read_guards_over(uint64_t base, uint64_t len) const {
         std::vector<int64_t> out;
-        for (auto &kv : read_guards)
-            if (overlaps(base, len, kv.second.first, kv.second.second)) out.push_back(kv.first);
+        if (!len) return out;
+        auto it = rg_by_base.lower_bound(base);
+        if (it != rg_by_base.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second.first > base) out.push_back(pv->second.second);
+        }
+        for (; it != rg_by_base.end() && it->first < base + len; ++it) out.push_back(it->second.second);
+        std::sort(out.begin(), out.end());
         return out;
+    }
+    void install_read_guard(uint64_t base, uint64_t len, int64_t task) {
+        auto hits = read_guards_over(base, len);
+        if (!hits.empty())
+            throw GuardErr("read guard (" + hex(base) + ", " + std::to_string(len) + ") overlaps task " +
+                           std::to_string(hits.front()));
+        read_guards[task] = {base, len};
+        rg_by_base[base] = {len, task};
+    }
+    void release_read_guard(int64_t task) {
+        auto it = read_guards.find(task);
+        if (it == read_guards.end()) return;
+        rg_by_base.erase(it->second.first);
+        read_guards.erase(it);
     }
 };
 

@@ -320,3 +320,22 @@ def test_native_tamper_detected_gpu():
     eng2.copy_h2d(CopyRequest("h2d", b2.base, b2.len, TransferClass.MODEL_WEIGHTS, block_id=b2.id))
     eng2.sync()
     eng2.finish()
+
+
+@pytest.mark.parametrize("chunk_mib", [4, 16])
+def test_layer_larger_than_window_hits_c2_in_both_engines(chunk_mib):
+    """A FIFO weight-offload layer split into more chunks than the validator
+    window (64) triggers the reference's defect C2 without
+    any adversarial mutation; the native and the Python engine raise the same
+    EngineError at the same point, and both complete with the fix on."""
+    chunk = chunk_mib << 20
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=chunk)
+    for compat in (True, False):
+        runs = [run_engine(tr, ReplayConfig(plane="dry", engine=e, chunk_bytes=chunk, predictor_chunk_bytes=chunk,
+                                            reference_compat=compat), catch=True) for e in ("python", "native")]
+        assert runs[0].error == runs[1].error
+        assert _schedule(runs[0].engine) == _schedule(runs[1].engine)
+        if compat:
+            assert runs[0].error.startswith("EngineError: commit at counter")
+        else:
+            assert runs[0].error is None and runs[0].engine.report()["otf_burned_records"] > 0
