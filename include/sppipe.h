@@ -220,9 +220,11 @@ int sp_pipe_app_read(sp_pipe *p, int64_t block, uint64_t offset, uint64_t n, voi
 /* Whole trace in one call (the replay driver of simulator.py:404-426 minus
  * its cost model); payloads holds small-I/O and app-write bytes. */
 int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done);
-/* The unencrypted baseline of the same trace (NoCc): each swap one plain
- * cudaMemcpyAsync between the registered pinned block and HBM on the pipe's
- * copy streams, same ordering rules, no crypto; returns when the device is idle. */
+/* The unencrypted baseline of the same trace (NoCc): the swaps as plain
+ * copies between the registered pinned blocks and HBM on the pipe's copy
+ * streams, gathered per batch boundary into batched copies like the
+ * engine's flushes, same ordering rules, no crypto; returns when the device
+ * is idle. */
 int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads);
 int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done);
 /* Test hook (the reference's Channel(test_hooks=True).hook_corrupt_in_flight,

@@ -1884,34 +1884,78 @@ class Engine {
         if (plane.dry) return;
         Plane &pl = plane;
         std::unordered_map<int64_t, View> dev;
-        std::unordered_map<int64_t, FenceP> landed;
-        std::vector<uint8_t *> pinned;
+        std::unordered_map<int64_t, FenceP> landed;  // block -> its last D2H / app write
         FenceP last_in;
+        // Copies gathered per batch boundary (sync) like the engine's flushes,
+        // so the baseline gets the same batched-copy advantage.
+        struct Pend {
+            std::vector<void *> dst, src;
+            std::vector<size_t> n;
+            std::vector<BufP> keep;
+            std::unordered_set<int64_t> blocks;
+            uint64_t bytes = 0;
+            void add(void *d, void *s, size_t k, const BufP &b, int64_t blk) {
+                dst.push_back(d);
+                src.push_back(s);
+                n.push_back(k);
+                keep.push_back(b);
+                blocks.insert(blk);
+                bytes += k;
+            }
+        };
+        Pend pin, pout;
+        auto issue = [&](Pend &q, cudaStream_t st, bool h2d) {
+            pl.copy_batch(st, h2d, q.n.size(), [&](size_t i, void *&d, void *&src, size_t &k) {
+                d = q.dst[i];
+                src = q.src[i];
+                k = q.n[i];
+            });
+            FenceP f = pl.record_new(st);
+            ++pl.tick;
+            for (auto &b : q.keep) b->use(st, f, pl.tick);
+            return f;
+        };
+        auto flush_in = [&] {
+            if (pin.n.empty()) return;
+            last_in = issue(pin, pl.s.h2d, true);
+            pin = Pend{};
+        };
+        auto flush_out = [&] {
+            if (pout.n.empty()) return;
+            if (last_in) pl.wait(pl.s.d2h, last_in);  // swap-outs follow the swap-ins issued before them
+            FenceP f = issue(pout, pl.s.d2h, false);
+            for (int64_t b : pout.blocks) landed[b] = f;
+            pout = Pend{};
+        };
+        const uint64_t kBatch = 64ull << 20;
         for (uint64_t k = 0; k < n; ++k) {
             const sp_event &e = ev[k];
             if (e.kind == SP_EV_SWAP_IN) {
                 Block &b = mem.block(e.block);
+                if (pout.blocks.count(e.block)) flush_out();  // its last swap-out lands first
                 auto it = landed.find(e.block);
                 if (it != landed.end()) pl.wait(pl.s.h2d, it->second);
                 View v{pl.alloc(b.len, pl.s.h2d), 0, b.len};
-                ck(cudaMemcpyAsync(v.ptr(), b.host, b.len, cudaMemcpyHostToDevice, pl.s.h2d), "plain H2D");
-                last_in = pl.record_new(pl.s.h2d);
-                v.buf->use(pl.s.h2d, last_in, ++pl.tick);
+                pin.add(v.ptr(), b.host, b.len, v.buf, e.block);
                 dev[e.block] = v;
+                if (pin.bytes >= kBatch) flush_in();
             } else if (e.kind == SP_EV_SWAP_OUT) {
                 Block &b = mem.block(e.block);
+                if (pin.blocks.count(e.block)) flush_in();  // its swap-in reaches the device first
                 auto it = dev.find(e.block);
                 View v = it != dev.end() ? it->second : View{pl.alloc(b.len, pl.s.d2h), 0, b.len};
-                if (last_in) pl.wait(pl.s.d2h, last_in);
                 auto lt = landed.find(e.block);  // an earlier app write into the block
                 if (lt != landed.end()) pl.wait(pl.s.d2h, lt->second);
-                ck(cudaMemcpyAsync(b.host, v.ptr(), b.len, cudaMemcpyDeviceToHost, pl.s.d2h), "plain D2H");
-                FenceP f = pl.record_new(pl.s.d2h);
-                v.buf->use(pl.s.d2h, f, ++pl.tick);
-                landed[e.block] = f;
+                pout.add(b.host, v.ptr(), b.len, v.buf, e.block);
                 dev.erase(e.block);
+                if (pout.bytes >= kBatch) flush_out();
+            } else if (e.kind == SP_EV_SYNC) {
+                flush_in();
+                flush_out();
             } else if (e.kind == SP_EV_APP_WRITE) {
                 // the same ordered host write the engine performs (after the block's pending DMA)
+                flush_in();
+                flush_out();
                 Block &b = mem.block(e.block);
                 auto lt = landed.find(e.block);
                 if (lt != landed.end()) pl.host_ready[e.block] = lt->second;
@@ -1931,6 +1975,8 @@ class Engine {
                 v.buf->use(st, f, ++pl.tick);
             }
         }
+        flush_in();
+        flush_out();
         dev.clear();
         pl.collect();
         pl.finish_streams();
