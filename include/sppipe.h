@@ -244,6 +244,20 @@ int64_t sp_pipe_sent_count(sp_pipe *p, int32_t dir);
 int sp_pipe_sent_log(sp_pipe *p, int32_t dir, int64_t from, sp_sent *out, int64_t cap, int64_t *n);
 /* Recorded streams (record_stream): which 0 = delivered H2D plaintext,
  * 1 = D2H small-I/O stream.  bytes (host, size bytes) may be NULL. */
+/* Validator records (validator.CiphertextRecord, validator.py:44-63): ids
+ * are 1 .. sp_pipe_record_count; state 0 pending, 1 committed, 2 invalidated. */
+typedef struct sp_record {
+    int64_t id;
+    uint64_t base;
+    uint64_t len;
+    uint64_t iv;
+    uint64_t span;     /* consecutive counters (chunks) */
+    int64_t block_id;  /* INT64_MIN = None */
+    int32_t state;
+    int32_t reserved;
+} sp_record;
+int64_t sp_pipe_record_count(sp_pipe *p);
+int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out);
 int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which);
 int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, void *bytes);
 /* Data-plane statistics: bytes over PCIe per direction, kernel launches. */

@@ -101,7 +101,7 @@ SPPIPE_SYMBOLS = (
     "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
-    "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
+    "sp_pipe_record_count", "sp_pipe_record", "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
 )
 
 
@@ -146,6 +146,12 @@ class SpAction(ctypes.Structure):
 
 class SpSent(ctypes.Structure):
     _fields_ = [("iv", ctypes.c_uint64), ("size", ctypes.c_uint64), ("nop", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class SpRecord(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int64), ("base", ctypes.c_uint64), ("len", ctypes.c_uint64), ("iv", ctypes.c_uint64),
+                ("span", ctypes.c_uint64), ("block_id", ctypes.c_int64), ("state", ctypes.c_int32),
                 ("reserved", ctypes.c_int32)]
 
 
@@ -203,6 +209,7 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_actions": [vp, i64, P(SpAction), i64, P(i64)],
             "sp_pipe_sent_log": [vp, i32, i64, P(SpSent), i64, P(i64)],
             "sp_pipe_delivered": [vp, i32, i64, P(SpDelivery), vp],
+            "sp_pipe_record": [vp, i64, P(SpRecord)],
             "sp_pipe_stats": [vp, P(u64), P(u64), P(u64)],
             "sp_pipe_pool_stats": [vp, P(u64), P(u64), P(u64)],
         }
@@ -221,6 +228,8 @@ def load_sppipe() -> ctypes.CDLL:
             getattr(lib, name).restype = i64
         lib.sp_pipe_sent_count.argtypes = [vp, i32]
         lib.sp_pipe_sent_count.restype = i64
+        lib.sp_pipe_record_count.argtypes = [vp]
+        lib.sp_pipe_record_count.restype = i64
         lib.sp_pipe_delivered_count.argtypes = [vp, i32]
         lib.sp_pipe_delivered_count.restype = i64
         for name in ("sp_pipe_send_iv", "sp_pipe_recv_iv"):

@@ -2289,6 +2289,17 @@ int sp_pipe_sent_log(sp_pipe *p, int32_t dir, int64_t from, sp_sent *out, int64_
     *n = k;
     return SP_OK;
 }
+int64_t sp_pipe_record_count(sp_pipe *p) { return (int64_t)p->e->val.records.size(); }
+int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out) {
+    Validator &v = p->e->val;
+    if (id < 1 || id > (int64_t)v.records.size()) {
+        g_err = "no record " + std::to_string(id);
+        return SP_EKEY;
+    }
+    const Record &r = v.rec(id);
+    *out = sp_record{r.id, r.base, r.len, r.iv, r.span(), r.block_id, (int32_t)r.state, 0};
+    return SP_OK;
+}
 int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which) {
     return (int64_t)(which ? p->e->d2h_stream.size() : p->e->delivered.size());
 }

@@ -17,18 +17,19 @@ import ctypes
 import hashlib
 import random
 import weakref
+from dataclasses import dataclass
 from typing import Iterable
 
 from . import _native
 from ._native import (SpAction, SpDecision, SpDelivery, SpEvent, SpPipeConfig, SpPrediction, SpPredConfig,
-                      SpSent)
+                      SpRecord, SpSent)
 from .channel import Direction
 from .engine import Action, ActionKind, CopyRequest, EngineConfig, EngineError, HandleState
 from .gcm import GcmAuthError
 from .memory import BoundsError, GuardOverlapError, HostMemory, KvCache, ModelLayer
 from .predictor import (DEFAULT_CONFIG, AmbiguousProfile, ModelProfile, PatternHypothesis, PatternKind, Prediction,
                         PredictorConfig, TransferClass, UnknownBlock)
-from .validator import OverlapError, StateError, VerdictKind
+from .validator import OverlapError, RecordState, StateError, VerdictKind
 
 _CLASS = {TransferClass.MODEL_WEIGHTS: 0, TransferClass.KV_CACHE: 1, TransferClass.SMALL_IO: 2}
 _CLASS_BACK = {v: k for k, v in _CLASS.items()}
@@ -171,6 +172,52 @@ class _Handle:
         return HandleState.DONE if self.done else HandleState.PENDING
 
 
+@dataclass(frozen=True)
+class RecordView:
+    """A validator record as the pipe holds it (validator.CiphertextRecord
+    without the device payloads)."""
+
+    id: int
+    base: int
+    len: int
+    iv: int
+    iv_span: int
+    state: RecordState
+    block_id: int | None
+
+    @property
+    def last_iv(self) -> int:
+        return self.iv + self.iv_span - 1
+
+
+class _ValidatorView:
+    """Read-only view of the native validator (validator.Validator's
+    queries: records, pending_records, pending_count)."""
+
+    _STATES = (RecordState.PENDING, RecordState.COMMITTED, RecordState.INVALIDATED)
+
+    def __init__(self, engine: "NativeEngine") -> None:
+        self._engine = engine
+
+    def _get(self, rid: int) -> RecordView:
+        e = self._engine
+        r = SpRecord()
+        _check(e._lib.sp_pipe_record(e._h, rid, ctypes.byref(r)))
+        return RecordView(r.id, r.base, r.len, r.iv, r.span, self._STATES[r.state],
+                          None if r.block_id == -(1 << 63) else r.block_id)
+
+    @property
+    def records(self) -> dict:
+        n = self._engine._lib.sp_pipe_record_count(self._engine._h)
+        return {i: self._get(i) for i in range(1, n + 1)}
+
+    def pending_records(self) -> list:
+        return [r for r in self.records.values() if r.state is RecordState.PENDING]
+
+    def pending_count(self) -> int:
+        return len(self.pending_records())
+
+
 class _Channel:
     def __init__(self, engine: "NativeEngine") -> None:
         self._engine = engine
@@ -234,6 +281,7 @@ class NativeEngine:
         me = weakref.proxy(self)
         self.cpu = _Endpoint(me, Direction.HOST_TO_DEVICE, cpu.key)
         self.gpu = _Endpoint(me, Direction.DEVICE_TO_HOST, gpu.key)
+        self.validator = _ValidatorView(me)
         self._registered = 0
         self._rng = random.Random(0xC0DE)
         self._actions: list[Action] = []

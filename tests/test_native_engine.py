@@ -339,3 +339,18 @@ def test_layer_larger_than_window_hits_c2_in_both_engines(chunk_mib):
             assert runs[0].error.startswith("EngineError: commit at counter")
         else:
             assert runs[0].error is None and runs[0].engine.report()["otf_burned_records"] > 0
+
+
+def test_native_validator_view_matches_python():
+    """engine.validator.records as the reference exposes it (cli.py nop-padding
+    scenario reads it): same ids, ranges, counters and states as the Python
+    engine's validator after a KV trace."""
+    tr = _adv("lifo", 0.25, 8)
+    a = run_engine(tr, ReplayConfig(plane="dry"), catch=True)
+    b = run_engine(tr, ReplayConfig(plane="dry", engine="native"), catch=True)
+    ra, rb = a.engine.validator.records, b.engine.validator.records
+    assert list(ra) == list(rb) and ra
+    for rid in ra:
+        x, y = ra[rid], rb[rid]
+        assert (x.id, x.base, x.len, x.iv, x.iv_span, x.state, x.block_id) == \
+               (y.id, y.base, y.len, y.iv, y.iv_span, y.state, y.block_id)
