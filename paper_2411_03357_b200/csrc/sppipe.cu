@@ -502,7 +502,6 @@ class Plane {
     int32_t *status = nullptr;
     uint64_t status_cap = 1 << 16, status_used = 0;
     uint64_t bytes_h2d = 0, bytes_d2h = 0, launches = 0;
-    BufP zero_scratch;
 
     Plane(bool dry_, const uint8_t key[32], uint64_t batch, uint64_t reserve) : dry(dry_), batch_bytes(batch) {
         if (dry) return;
@@ -526,7 +525,6 @@ class Plane {
         host_ready.clear();
         h2d_done.clear();
         arena_dev.reset();
-        zero_scratch.reset();
         window.reset();
         for (auto &kv : cache)
             for (auto &g : kv.second) garbage.push_back(std::move(g));
