@@ -357,3 +357,65 @@ def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: i
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
+
+
+def main(argv: list[str] | None = None) -> int:
+    """Replay reference-format JSONL traces (workload.py:188-260 schema v1)
+    on the B200: one JSON line per (trace, system) with measured swap GB/s,
+    the plain-copy baseline and the engine's report counters — the
+    measured counterpart of the reference's `specpipe sim` (cli.py:119-183)."""
+    import argparse
+    import json
+
+    from .workload import load_trace
+
+    ap = argparse.ArgumentParser(prog="python -m paper_2411_03357_b200.replay")
+    ap.add_argument("trace", nargs="+", help="JSONL trace file(s) in the reference schema")
+    ap.add_argument("--system", action="append", choices=["specpipe", "synccc", "nocc"],
+                    help="systems to run (default: all three)")
+    ap.add_argument("--engine", choices=["native", "python"], default="native")
+    ap.add_argument("--plane", choices=["gpu", "dry"], default="gpu")
+    ap.add_argument("--window", type=int, default=64)
+    ap.add_argument("--leeway", type=int, default=8)
+    ap.add_argument("--depth", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3, help="timed runs per system (best reported)")
+    ap.add_argument("--fix-c2", action="store_true", help="reference_compat=False (SURVEY App. C defect C2 fixed)")
+    args = ap.parse_args(argv)
+    systems = args.system or ["specpipe", "synccc", "nocc"]
+    for path in args.trace:
+        trace = load_trace(path)
+        for system in systems:
+            cfg = ReplayConfig(system="specpipe" if system == "nocc" else system, engine=args.engine,
+                               plane=args.plane, window=args.window, leeway=args.leeway, depth=args.depth,
+                               seed=args.seed, record_stream=False, fill="fast" if args.plane == "gpu" else "seeded",
+                               reference_compat=not args.fix_c2)
+            memory = prepare_memory(trace, cfg)
+            row = {"trace": str(path), "system": system, "engine": args.engine, "plane": args.plane,
+                   "swap_bytes": trace.swap_bytes(), "events": len(trace.events)}
+            if system == "nocc":
+                if args.plane != "gpu" or args.engine != "native":
+                    row["error"] = "nocc replays need --engine native --plane gpu"
+                else:
+                    runs = [run_plain_native(trace, cfg, memory=memory) for _ in range(args.reps + 1)][1:]
+                    row["swap_gbs"] = round(max(r.swap_gbs for r in runs), 3)
+                print(json.dumps(row), flush=True)
+                continue
+            res = None
+            best = 0.0
+            for _ in range(args.reps + (1 if args.plane == "gpu" else 0)):
+                res = run_engine(trace, cfg, catch=True, memory=memory)
+                if res.error:
+                    break
+                best = max(best, res.swap_gbs)
+            rep = res.engine.report()
+            row.update({"error": res.error, "swap_gbs": round(best, 3) if args.plane == "gpu" else None,
+                        "hit": rep["hit"], "iv_ahead": rep["iv_ahead"], "miss": rep["miss"], "nops": rep["nops"],
+                        "relinquishes": rep["relinquishes"] + rep["replans"],
+                        "sequence_hit_rate": rep["sequence_hit_rate"], "data_msgs": rep["data_msgs"]})
+            print(json.dumps(row), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

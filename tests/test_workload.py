@@ -57,3 +57,23 @@ def test_opt_shapes():
     tr = workload.gen_opt_offload_trace("opt-13b", [21], 1)
     sizes = sorted({b.nbytes for b in tr.header.blocks})
     assert sizes == [25_298_944, 32 * 1024 * 1024]
+
+
+def test_jsonl_replay_cli_dry(tmp_path, capsys):
+    """Reference-format JSONL traces replay through either engine from the
+    command line (python -m paper_2411_03357_b200.replay); both engines
+    report the same decisions."""
+    import json
+
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import main
+
+    tr = workload.gen_kvswap_trace(6, "lifo", kv_block_bytes=28672, parallel_size=2, seed=1)
+    path = tmp_path / "kv.jsonl"
+    workload.save_trace(tr, path)
+    rows = []
+    for engine in ("native", "python"):
+        assert main([str(path), "--plane", "dry", "--engine", engine, "--system", "specpipe"]) == 0
+        rows.append(json.loads(capsys.readouterr().out.strip().splitlines()[-1]))
+    strip = lambda r: {k: v for k, v in r.items() if k != "engine"}  # noqa: E731
+    assert strip(rows[0]) == strip(rows[1]) and rows[0]["error"] is None and rows[0]["data_msgs"] > 0
