@@ -138,22 +138,29 @@ struct WriteGuard {
 
 class HostMem {
   public:
-    std::map<int64_t, Block> blocks;            // id -> block
+    // id -> block (ids are small and dense, memory.py:117-166); stable addresses
+    std::vector<std::unique_ptr<Block>> blocks;
     std::map<uint64_t, int64_t> by_base;        // base -> id
     std::map<int64_t, WriteGuard> write_guards;  // owner (record id) -> guard (insertion order == id order)
     std::map<int64_t, std::pair<uint64_t, uint64_t>> read_guards;  // task id -> (base, len)
 
     Block &block(int64_t id) {
-        auto it = blocks.find(id);
-        if (it == blocks.end()) throw KeyErr(std::to_string(id));
-        return it->second;
+        if (id < 0 || id >= (int64_t)blocks.size() || !blocks[(size_t)id]) throw KeyErr(std::to_string(id));
+        return *blocks[(size_t)id];
+    }
+    void add_block(const Block &b) {
+        if (b.id < 0 || b.id > (int64_t)1 << 40) throw ValueErr("block id out of range");
+        if ((size_t)b.id >= blocks.size()) blocks.resize((size_t)b.id + 1);
+        if (blocks[(size_t)b.id]) by_base.erase(blocks[(size_t)b.id]->base);
+        blocks[(size_t)b.id].reset(new Block(b));
+        by_base[b.base] = b.id;
     }
     // memory.py block_at: the block containing [base, base+len)
     std::pair<Block *, uint64_t> block_at(uint64_t base, uint64_t len) {
         auto it = by_base.upper_bound(base);
         if (it != by_base.begin()) {
             --it;
-            Block &b = blocks.at(it->second);
+            Block &b = block(it->second);
             if (b.base <= base && base + len <= b.base + b.len) return {&b, base - b.base};
         }
         throw BoundsErr("range (" + hex(base) + ", " + std::to_string(len) + ") is not inside any block");
@@ -2161,9 +2168,7 @@ void sp_pipe_destroy(sp_pipe *p) { delete p; }
 
 int sp_pipe_register_block(sp_pipe *p, int64_t id, uint64_t base, uint64_t len, int32_t kind, void *host) {
     return guarded([&] {
-        auto &m = p->e->mem;
-        m.blocks[id] = Block{id, base, len, kind, static_cast<uint8_t *>(host)};
-        m.by_base[base] = id;
+        p->e->mem.add_block(Block{id, base, len, kind, static_cast<uint8_t *>(host)});
     });
 }
 int sp_pipe_seed_device(sp_pipe *p, int64_t block, const void *src, uint64_t len, int32_t src_is_device) {
