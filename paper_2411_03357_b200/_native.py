@@ -13,7 +13,7 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
 SPGCM_PATH = os.environ.get("SPGCM_LIB") or os.path.join(LIB_DIR, "libspgcm.so")  # env: A/B builds
-SPPIPE_PATH = os.path.join(LIB_DIR, "libsppipe.so")
+SPPIPE_PATH = os.environ.get("SPPIPE_LIB") or os.path.join(LIB_DIR, "libsppipe.so")  # env: A/B builds
 
 SP_OK, SP_EINVAL, SP_EAUTH, SP_ECUDA, SP_ENODEV = 0, 1, 2, 3, 4
 
@@ -214,6 +214,8 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_pool_stats": [vp, P(u64), P(u64), P(u64)],
         }
         for name, args in sig.items():
+            if not hasattr(lib, name):  # older A/B builds (SPPIPE_LIB); tests/test_native_engine.py checks the ABI
+                continue
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
@@ -228,8 +230,9 @@ def load_sppipe() -> ctypes.CDLL:
             getattr(lib, name).restype = i64
         lib.sp_pipe_sent_count.argtypes = [vp, i32]
         lib.sp_pipe_sent_count.restype = i64
-        lib.sp_pipe_record_count.argtypes = [vp]
-        lib.sp_pipe_record_count.restype = i64
+        if hasattr(lib, "sp_pipe_record_count"):
+            lib.sp_pipe_record_count.argtypes = [vp]
+            lib.sp_pipe_record_count.restype = i64
         lib.sp_pipe_delivered_count.argtypes = [vp, i32]
         lib.sp_pipe_delivered_count.restype = i64
         for name in ("sp_pipe_send_iv", "sp_pipe_recv_iv"):

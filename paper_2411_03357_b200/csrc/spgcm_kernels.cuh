@@ -59,9 +59,10 @@ struct MsgDev {
 };
 
 // Batches of up to kInline messages travel inside the kernel parameters (no
-// descriptor copy, no host staging on the launch path); larger batches use a
-// device array filled from a pinned staging ring.
-constexpr uint32_t kInline = 32;
+// descriptor copy, no host staging on the launch path; 16 KiB of the 32 KiB
+// sm_100 parameter space): measured host issue cost 3.5 us per launch vs
+// ~17 us through the pinned staging ring + copy + event of larger batches.
+constexpr uint32_t kInline = 256;
 
 // MsgDev.dir: low byte = channel direction (nonce word 0), this bit = open
 // (verify + decrypt) instead of seal, so one launch can mix both.

@@ -1,5 +1,6 @@
 // Per-launch cost of small seal batches from C (no Python in the loop).
 #include <cuda_runtime.h>
+#include <chrono>
 #include <cstdio>
 #include <vector>
 #include "spgcm.h"
@@ -29,6 +30,20 @@ int main() {
         cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         printf("empty kernel 148x512: %8.2f us/launch\n", ms * 1000 / 200);
+    }
+    {
+        // host-side issue cost per launch: inline descriptors (<= 32) vs the pinned ring
+        std::vector<sp_desc> d(256);
+        for (int i = 0; i < 256; ++i) d[i] = sp_desc{0, 0, (uint64_t)i, 16, buf + 16 * i, out + 16 * i, tags + 16 * (i % 64), nullptr};
+        for (int nmsg : {1, 32, 33, 64, 256}) {
+            for (int w = 0; w < 50; ++w) sp_seal_batch(ctx, d.data(), nmsg, s);
+            cudaStreamSynchronize(s);
+            auto t0 = std::chrono::steady_clock::now();
+            for (int r = 0; r < 200; ++r) sp_seal_batch(ctx, d.data(), nmsg, s);
+            double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / 200;
+            cudaStreamSynchronize(s);
+            printf("host issue cost, %3d msgs: %6.2f us/launch\n", nmsg, us);
+        }
     }
     for (size_t n : sizes) {
         for (int nmsg : {1, 8, 32}) {
