@@ -212,6 +212,12 @@ int sp_pipe_speculate(sp_pipe *p);
 int sp_pipe_relinquish(sp_pipe *p, int64_t *count);
 int sp_pipe_drain_decrypts(sp_pipe *p);
 int sp_pipe_finish(sp_pipe *p);
+/* finish() that returns once every observable result is final (all
+ * committed transfers opened and verified, all landings and app writes on
+ * the host) without waiting for encrypt-ahead work of records discarded at
+ * finish, which gates nothing (the reference simulator's makespan excludes
+ * it, simulator.py:441-443); sp_pipe_flush(p, 1) or destroy drains it. */
+int sp_pipe_finish_observable(sp_pipe *p);
 /* Issue every queued launch/landing now; with wait != 0 also block until all
  * device work of the pipe's streams is done (no counter or tag checks). */
 int sp_pipe_flush(sp_pipe *p, int32_t wait);

@@ -97,7 +97,7 @@ SPPIPE_SYMBOLS = (
     "sp_pred_outstanding", "sp_pred_in_batch_count", "sp_pred_decision_count", "sp_pred_decision",
     "sp_pipe_create", "sp_pipe_destroy", "sp_pipe_register_block", "sp_pipe_seed_device", "sp_pipe_submit_h2d",
     "sp_pipe_submit_d2h", "sp_pipe_small_io", "sp_pipe_sync", "sp_pipe_speculate", "sp_pipe_relinquish",
-    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
+    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_finish_observable", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
     "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
@@ -198,7 +198,8 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_submit_d2h": [vp, u64, u64, i32, i64, P(u64)],
             "sp_pipe_small_io": [vp, i32, vp, u64],
             "sp_pipe_sync": [vp], "sp_pipe_speculate": [vp], "sp_pipe_relinquish": [vp, P(i64)],
-            "sp_pipe_drain_decrypts": [vp], "sp_pipe_finish": [vp], "sp_pipe_flush": [vp, i32],
+            "sp_pipe_drain_decrypts": [vp], "sp_pipe_finish": [vp], "sp_pipe_finish_observable": [vp],
+            "sp_pipe_flush": [vp, i32],
             "sp_pipe_app_write": [vp, i64, u64, vp, u64, P(i64)],
             "sp_pipe_app_read": [vp, i64, u64, u64, vp],
             "sp_pipe_replay": [vp, P(SpEvent), u64, vp, P(u64)],

@@ -26,7 +26,8 @@ using namespace spgcm;
 // Device: the batched seal/open kernel
 // =============================================================================
 
-__device__ __forceinline__ void fill_tables(uint8_t *sm, const KParams &p) {
+template <class P>
+__device__ __forceinline__ void fill_tables(uint8_t *sm, const P &p) {
     // 8192 AES stores + 4096 GHASH stores of 16 B = 24 per thread.  All global
     // loads are issued before any store so their latencies overlap (the tables
     // are usually evicted from L2 by the payload stream: one DRAM round trip
@@ -78,7 +79,8 @@ __device__ __forceinline__ uint4 len_block(uint64_t len) {
 }
 
 // Tag finalisation for one message; S = GHASH without E_K(J0).  Warp-uniform.
-__device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams &p, const MsgDev &md,
+template <class P>
+__device__ __forceinline__ void finish_message(const uint8_t *sm, const P &p, const MsgDev &md,
                                                uint4 S, uint32_t x0, uint32_t x1, uint32_t x2,
                                                uint32_t lct, int lane) {
     const uint4 ek = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
@@ -105,7 +107,8 @@ __device__ __forceinline__ void finish_message(const uint8_t *sm, const KParams 
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParams p) {
+template <uint32_t INL>
+__global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParamsT<INL> p) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
     // let a dependent launch on this stream be scheduled now: its CTAs take
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
     }
     if (g >= g_end) return;
 
-    const MsgDev *msgs = p.nmsgs <= kInline ? p.inl : p.msgs;
+    const MsgDev *msgs = p.nmsgs <= INL ? p.inl : p.msgs;
     // first message containing row g (binary search on row_begin)
     uint32_t lo = 0, hi = p.nmsgs - 1;
     while (lo < hi) {
@@ -577,7 +580,8 @@ int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
     return SP_OK;
 }
 
-int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_end, cudaStream_t s) {
+template <uint32_t INL>
+int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t row_end, cudaStream_t s) {
     if (row_end <= row_begin) return SP_OK;
     p.row_begin = row_begin;
     p.row_end = row_end;
@@ -601,16 +605,17 @@ int launch_rows(const sp_ctx *ctx, KParams p, uint64_t row_begin, uint64_t row_e
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm, p), "k_gcm launch");
+    SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL>, p), "k_gcm launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    SP_CUDA(cudaGetLastError(), "k_gcm launch");
     return SP_OK;
 }
 
 // Build device message table for a batch; returns total rows.  mode: 0 all
 // seal, 1 all open, 2 per message (desc.reserved = SP_OP_SEAL / SP_OP_OPEN).
+// With `big` non-null, a batch of kInline+1 .. kInlineBig messages goes
+// inline in *big (and *use_big is set) instead of through the staging ring.
 int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Workspace *ws, KParams &p,
-                uint64_t &rows, int mode) {
+                uint64_t &rows, int mode, KParamsBig *big = nullptr, bool *use_big = nullptr) {
     ws->h_msgs.resize((size_t)n);
     rows = 0;
     for (int i = 0; i < n; ++i) {
@@ -634,8 +639,22 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
     int rc = ensure_ws(ws, (size_t)n, s);
     if (rc) return rc;
     p = base_params(ctx);
+    if (use_big) *use_big = false;
     if ((uint32_t)n <= kInline) {
         memcpy(p.inl, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev));
+    } else if (big && (uint32_t)n <= kInlineBig) {
+        memcpy(big->rk, p.rk, sizeof(p.rk));
+        big->ttab = p.ttab;
+        big->mg = p.mg;
+        big->nt = p.nt;
+        big->msgs = ws->d_msgs;
+        big->acc = ws->d_acc;
+        big->nmsgs = (uint32_t)n;
+        big->reserved = 0;
+        big->row_begin = big->row_end = 0;
+        big->warps_used = 0;
+        memcpy(big->inl, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev));
+        *use_big = true;
     } else {
         // pinned ring slot: wait only for the copy that last used this slot
         const int k = ws->slot;
@@ -677,10 +696,12 @@ int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, int mode) {
     Workspace *ws = workspace_for(ctx->device, s);
     std::lock_guard<std::mutex> lk(ws->mu);
     KParams p;
+    static thread_local KParamsBig big;  // 16.6 KiB: off the stack
+    bool use_big = false;
     uint64_t rows = 0;
-    int rc = stage_batch(ctx, d, n, s, ws, p, rows, mode);
+    int rc = stage_batch(ctx, d, n, s, ws, p, rows, mode, &big, &use_big);
     if (rc) return rc;
-    return launch_rows(ctx, p, 0, rows, s);
+    return use_big ? launch_rows(ctx, big, 0, rows, s) : launch_rows(ctx, p, 0, rows, s);
 }
 
 // ---- host-buffer pipeline ----------------------------------------------------
@@ -918,8 +939,10 @@ int sp_ctx_create(const uint8_t key[SP_KEY_BYTES], sp_ctx **out) {
     cudaDeviceProp prop;
     SP_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
     if (prop.major != 10) return fail(SP_ENODEV, "libspgcm is built for sm_100a (B200) only");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
             "cudaFuncSetAttribute(k_gcm)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
+            "cudaFuncSetAttribute(k_gcm big)");
     sp_ctx *c = new sp_ctx();
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;

@@ -59,17 +59,22 @@ struct MsgDev {
 };
 
 // Batches of up to kInline messages travel inside the kernel parameters (no
-// descriptor copy, no host staging on the launch path; 16 KiB of the 32 KiB
-// sm_100 parameter space): measured host issue cost 3.5 us per launch vs
-// ~17 us through the pinned staging ring + copy + event of larger batches.
-constexpr uint32_t kInline = 256;
+// descriptor copy, no host staging on the launch path).  Two parameter
+// blocks: 32 inline descriptors (2.4 KiB) for the common case, 256 (16.6
+// KiB) for 33-256 message batches (host issue 3.5 us vs ~17 us through the
+// pinned staging ring + copy + event).  Keeping most launches small matters:
+// the driver's ring of pending launch parameters is finite, and with 16 KiB
+// blocks a deep queue of pending launches blocks the issuing thread.
+constexpr uint32_t kInline = 32;
+constexpr uint32_t kInlineBig = 256;
 
 // MsgDev.dir: low byte = channel direction (nonce word 0), this bit = open
 // (verify + decrypt) instead of seal, so one launch can mix both.
 constexpr uint32_t kOpenBit = 0x100u;
 
-struct KParams {
-    MsgDev inl[kInline];
+template <uint32_t INL>
+struct KParamsT {
+    MsgDev inl[INL];
     uint32_t rk[60];
     const uint32_t *ttab;  // T0..T3 [4][256] then R8[256]
     const uint4 *mg;       // M_G[256], G = H^32
@@ -82,6 +87,8 @@ struct KParams {
     uint32_t reserved;
     uint32_t warps_used;   // warps per CTA that own rows (<= kWarpsPerCta)
 };
+using KParams = KParamsT<kInline>;
+using KParamsBig = KParamsT<kInlineBig>;
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 

@@ -360,7 +360,7 @@ class Validator {
 
 // ---- data plane -----------------------------------------------------------------------
 struct Streams {
-    cudaStream_t comp, spec, h2d, d2h, land, host;  // host: ordered application writes (host functions)
+    cudaStream_t comp, spec, h2d, d2h, land, host, out;  // host: ordered app writes; out: swap-out seals
 };
 
 struct DevicePool {
@@ -391,7 +391,7 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[6] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host};
+    cudaStream_t *all[7] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out};
     for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
     g_streams[dev] = s;
     return s;
@@ -484,7 +484,6 @@ class Plane {
     uint64_t ops_bytes = 0;
     FenceP window;
     // small-payload arena
-    std::vector<uint8_t> arena_host;
     BufP arena_dev;
     uint64_t arena_off = 0;      // payloads (copied from the host) grow up from 0
     uint64_t arena_low = 0;      // device-only scratch grows down from the end
@@ -498,12 +497,30 @@ class Plane {
     } ring;
     static constexpr uint64_t kRingBytes = 32ull << 20;
     static constexpr uint64_t kArenaBytes = 1 << 20;
+    // NOP pads seal zeros: read from a device zero page instead of crossing PCIe
+    static constexpr uint64_t kZeroBytes = 1 << 20;
+    uint8_t *zero_dev = nullptr;
+    // ring slots read by queued (not yet issued) seals: committed with the
+    // fence of the flush that issues them
+    std::vector<std::pair<uint8_t *, uint64_t>> ring_pending;
+    uint64_t ring_pending_bytes = 0;
     // landings
     std::vector<Landing> landings;
     std::unordered_set<int64_t> landing_blocks;
     std::unordered_map<int64_t, FenceP> host_ready;  // block -> fence after last D2H into it
     std::unordered_map<int64_t, FenceP> h2d_done;    // block -> fence after last H2D from it
     CopyBatch otf_copies;                             // on-the-fly staging copies (issued at flush)
+    // Swap-out seals, on their own stream: each waits only for the launch
+    // that last wrote its source block, so a layer's swap-out seals (and its
+    // landings and D2H copies) start while the receiver's opens of later
+    // chunks still run on the compute stream.
+    struct OutBatch {
+        std::vector<sp_desc> items;
+        std::vector<BufP> bufs;
+        std::vector<FenceP> waits;
+        uint64_t bytes = 0;
+        FenceP ready;
+    } outb;
     CopyBatch *spec_copies = nullptr;                 // copies of the SpecBatch being built
     // status words of opens
     int32_t *status = nullptr;
@@ -517,6 +534,8 @@ class Plane {
         pool = pool_for(dev, reserve, s.comp);
         ctx = ctx_for(dev, key);
         ck(cudaMalloc(&status, status_cap * sizeof(int32_t)), "cudaMalloc(status)");
+        ck(cudaMalloc(&zero_dev, kZeroBytes), "cudaMalloc(zero page)");
+        ck(cudaMemset(zero_dev, 0, kZeroBytes), "cudaMemset(zero page)");
         ck(cudaMemset(status, 0, status_cap * sizeof(int32_t)), "cudaMemset(status)");
         window = new_fence();
     }
@@ -546,6 +565,7 @@ class Plane {
         }
         for (cudaEvent_t e : free_events) cudaEventDestroy(e);
         if (status) cudaFree(status);
+        if (zero_dev) cudaFree(zero_dev);
     }
 
     // -- events / buffers --------------------------------------------------------------
@@ -683,6 +703,18 @@ class Plane {
     // -- compute queue ------------------------------------------------------------------
     void queue(Op &&op, uint64_t nbytes) {
         if (op.wait == window) op.wait.reset();  // queue order covers the current window
+        // write-after-read against swap-out seals still reading the buffer on
+        // the out stream (partial swap-outs keep the block buffer alive)
+        for (int k = 0; k < op.nw; ++k) {
+            const Buf *b = op.w[k].buf;
+            for (auto &x : outb.bufs)
+                if (x.get() == b) {
+                    launch_out();
+                    break;
+                }
+            for (auto &u : b->uses)
+                if (u.first == s.out && u.second && u.second->recorded) wait(s.comp, u.second);
+        }
         ops.push_back(std::move(op));
         ops_bytes += nbytes;
         if (ops_bytes >= batch_bytes) flush();
@@ -712,17 +744,6 @@ class Plane {
         issue_pending_copies();
         if (arena_dev && (arena_off || arena_low < arena_dev->size)) {
             // the window's arena is sealed/opened by this flush; the next one starts fresh
-            if (!arena_host.empty()) {
-                const uint64_t n = arena_host.size();
-                uint8_t *h = ring_reserve(n);
-                memcpy(h, arena_host.data(), n);
-                ck(cudaMemcpyAsync(arena_dev->ptr, h, n, cudaMemcpyHostToDevice, s.comp), "arena H2D");
-                FenceP f = record_new(s.comp);
-                ring_commit(h, n, f);
-                arena_dev->use(s.comp, f, ++tick);
-                bytes_h2d += n;
-            }
-            arena_host.clear();
             arena_dev.reset();
             arena_off = 0;
             arena_low = 0;
@@ -778,8 +799,12 @@ class Plane {
                 if (op.a) op.a->use(s.comp, window, tick);
                 if (op.b) op.b->use(s.comp, window, tick);
             }
+            for (auto &r : ring_pending) ring_commit(r.first, r.second, window);
+            ring_pending.clear();
+            ring_pending_bytes = 0;
             window = new_fence();
         }
+        launch_out();
         if (!landings.empty()) flush_landings();
         collect();
     }
@@ -796,10 +821,14 @@ class Plane {
             }
             if (!ring.ptr) {
                 ring.cap = kRingBytes;
-                ck(cudaHostAlloc(reinterpret_cast<void **>(&ring.ptr), ring.cap, cudaHostAllocDefault), "cudaHostAlloc(ring)");
+                // mapped: the sealing kernel reads small payloads straight from here
+                // (no copy-engine transfer queued behind bulk swap copies)
+                ck(cudaHostAlloc(reinterpret_cast<void **>(&ring.ptr), ring.cap,
+                                 cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc(ring)");
             }
         }
         if (n > ring.cap) throw ValueErr("small payload larger than the staging ring");
+        n = (n + 63u) & ~uint64_t(63);  // 64-byte slots: vectorised kernel reads straight from the ring
         if (ring.head + n > ring.cap) ring.head = 0;
         const uint64_t lo = ring.head, hi = lo + n;
         while (!ring.busy.empty()) {
@@ -921,7 +950,10 @@ class Plane {
     // instead of a call per copy; plain cudaMemcpyAsync where unsupported.
     template <class F>
     void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
-        static bool batch_ok = true;
+        static bool batch_ok = [] {  // SPPIPE_BATCH_COPY=0: per-copy calls (profilers show each copy)
+            const char *e = getenv("SPPIPE_BATCH_COPY");
+            return !(e && e[0] == '0');
+        }();
         if (count > 1 && batch_ok) {
             std::vector<void *> dsts(count), srcs(count);
             std::vector<size_t> sizes(count);
@@ -1094,21 +1126,52 @@ class Plane {
         }
         uint64_t total = 0, first = spans[0].first;
         for (auto &sp : spans) total += sp.second;
-        BufP buf = alloc(round16(total) + kTag * spans.size(), s.comp);
+        // the source's writer (a receiver open) must be issued before we can wait for it
+        for (const Op &op : ops)
+            if (op.a.get() == src.buf.get() || op.b.get() == src.buf.get()) {
+                flush();
+                break;
+            }
+        for (auto &u : src.buf->uses)
+            if (u.first != s.out && u.second && u.second->recorded) outb.waits.push_back(u.second);
+        if (!outb.ready) outb.ready = new_fence();
+        BufP buf = alloc(round16(total) + kTag * spans.size(), s.out);
         for (size_t i = 0; i < spans.size(); ++i) {
             auto m = std::make_shared<Msg>();
             m->buf = buf;
             m->off = spans[i].first - first;
             m->len = spans[i].second;
             m->tag_off = round16(total) + kTag * i;
-            Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, m->len,
-                            View{src.buf, src.off + spans[i].first, m->len}, View{buf, m->off, m->len}, buf,
-                            m->tag_off, nullptr);
-            m->ready = window;
-            queue(std::move(op), m->len);
+            sp_desc d{};
+            d.dir = (uint32_t)dir;
+            d.reserved = SP_OP_SEAL;
+            d.iv = iv0 + i;
+            d.len = m->len;
+            d.src = src.buf->ptr + src.off + spans[i].first;
+            d.dst = buf->ptr + m->off;
+            d.tag = buf->ptr + m->tag_off;
+            outb.items.push_back(d);
+            m->ready = outb.ready;
             msgs.push_back(m);
         }
+        outb.bufs.push_back(buf);
+        outb.bufs.push_back(src.buf);
+        outb.bytes += total;
+        if (outb.bytes >= batch_bytes) launch_out();
         return msgs;
+    }
+
+    void launch_out() {
+        if (outb.items.empty()) return;
+        std::unordered_set<Fence *> seen;
+        for (auto &f : outb.waits)
+            if (seen.insert(f.get()).second) wait(s.out, f);
+        ck_sp(sp_seal_batch(ctx, outb.items.data(), (int)outb.items.size(), s.out), "sp_seal_batch(swap-out)");
+        ++launches;
+        record(outb.ready, s.out);
+        ++tick;
+        for (auto &b : outb.bufs) b->use(s.out, outb.ready, tick);
+        outb = OutBatch{};
     }
 
     // NOP pads and token I/O: staged in the byte arena (one PCIe copy per flush).
@@ -1121,18 +1184,39 @@ class Plane {
             m->len = n;
             m->nop = nop;
             if (!dry) {
+                // source: the device zero page (NOPs) or the payload in the
+                // mapped pinned ring, read by the kernel over PCIe; the sealed
+                // message lands in the window's device arena
+                const bool zeros = !payloads[i].first && n <= kZeroBytes;
+                const uint8_t *src = zero_dev;
+                if (!zeros) {
+                    if (ring_pending_bytes + n > kRingBytes / 2) flush();  // keep unissued slots clear of wrap-around
+                    uint8_t *h = ring_reserve(n);
+                    if (payloads[i].first) memcpy(h, payloads[i].first, n);
+                    else memset(h, 0, n);
+                    ring_pending.push_back({h, n});
+                    ring_pending_bytes += n;
+                    src = h;
+                    bytes_h2d += n;
+                }
                 uint64_t need = round16(n) + kTag;
                 if (!arena_dev || arena_off + need > arena_low) new_arena(need);
                 uint64_t o = arena_off;
                 arena_off += need;
-                if (arena_host.size() < o + n) arena_host.resize(o + n, 0);
-                if (payloads[i].first) memcpy(arena_host.data() + o, payloads[i].first, n);
-                else memset(arena_host.data() + o, 0, n);
                 m->buf = arena_dev;
                 m->off = o;
                 m->tag_off = o + need - kTag;
-                View v{arena_dev, o, n};
-                Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, n, v, v, arena_dev, m->tag_off, nullptr);
+                Op op;
+                op.d.dir = (uint32_t)dir;
+                op.d.reserved = SP_OP_SEAL;
+                op.d.iv = iv0 + i;
+                op.d.len = n;
+                op.d.src = src;
+                op.d.dst = arena_dev->ptr + o;
+                op.d.tag = arena_dev->ptr + m->tag_off;
+                op.b = arena_dev;
+                op.w[op.nw++] = Region{arena_dev.get(), o, o + n};
+                op.w[op.nw++] = Region{arena_dev.get(), m->tag_off, m->tag_off + kTag};
                 m->ready = window;
                 queue(std::move(op), n);
             }
@@ -1187,7 +1271,6 @@ class Plane {
         arena_dev = alloc(std::max(kArenaBytes, need), s.comp);
         arena_off = 0;
         arena_low = arena_dev->size;
-        arena_host.clear();
     }
 
     void host_sync(int64_t block_id) {
@@ -1234,12 +1317,25 @@ class Plane {
     }
     void finish_streams() {
         flush();
-        cudaStream_t all[6] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host};
+        cudaStream_t all[7] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
-    void finish() {
+    // drain_all = false: wait only for work whose results can be observed —
+    // every receiver open and verdict (comp; it waited for the encrypt-ahead
+    // seals and copies it consumed), swap-out seals, landings and D2H copies,
+    // app writes.  What can still run then on the h2d/spec streams is
+    // encrypt-ahead of records discarded at finish (engine.py:583-592), which
+    // gates nothing (the reference simulator leaves it out of its makespan,
+    // simulator.py:441-443); the pipe's destructor drains it.
+    void finish(bool drain_all = true) {
         if (dry) return;
-        finish_streams();
+        if (drain_all) {
+            finish_streams();
+        } else {
+            flush();
+            cudaStream_t obs[5] = {s.comp, s.out, s.land, s.d2h, s.host};
+            for (auto st : obs) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        }
         check_auth();
     }
     void copy_to_host(const View &v, void *out) {
@@ -1845,7 +1941,7 @@ class Engine {
         for (int64_t id : ids) apply_decrypt(id, false);
     }
 
-    void finish() {
+    void finish(bool drain_all = true) {
         if (!suspended.empty() || !batch_ins.empty()) sync();
         drain_decrypts();
         for (int64_t id : val.pending_ids()) {
@@ -1854,7 +1950,7 @@ class Engine {
         }
         spec_queue.clear();
         if (pending(H2D)) drain_gpu();
-        plane.finish();
+        plane.finish(drain_all);
         audit();
     }
 
@@ -2213,6 +2309,9 @@ int sp_pipe_drain_decrypts(sp_pipe *p) {
 }
 int sp_pipe_finish(sp_pipe *p) {
     return guarded([&] { p->e->finish(); });
+}
+int sp_pipe_finish_observable(sp_pipe *p) {
+    return guarded([&] { p->e->finish(false); });
 }
 int sp_pipe_flush(sp_pipe *p, int32_t wait) {
     return guarded([&] {

@@ -363,8 +363,15 @@ class NativeEngine:
     def drain_decrypts(self) -> None:
         _check(self._lib.sp_pipe_drain_decrypts(self._h))
 
-    def finish(self) -> None:
-        _check(self._lib.sp_pipe_finish(self._h))
+    def finish(self, drain_discarded: bool = True) -> None:
+        """engine.finish (engine.py:583-607).  drain_discarded=False returns
+        once every observable result is final, leaving encrypt-ahead work of
+        records discarded here to drain in the background (see
+        sp_pipe_finish_observable)."""
+        if drain_discarded:
+            _check(self._lib.sp_pipe_finish(self._h))
+        else:
+            _check(self._lib.sp_pipe_finish_observable(self._h))
 
     def test_corrupt_in_flight(self, direction: Direction, index: int, byte_index: int = 0, bit: int = 0) -> None:
         """hook_corrupt_in_flight (channel.py:263-273): flip one bit of an

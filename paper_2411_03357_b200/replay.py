@@ -56,10 +56,19 @@ class ReplayResult:
     swap_bytes: int
     payload_bytes: int
     error: str | None = None
+    # native engine on the GPU: time until every observable result was final
+    # (finish without draining encrypt-ahead of records discarded at finish);
+    # wall_s additionally waits for that discarded work (the conservative number)
+    observable_s: float | None = None
 
     @property
     def swap_gbs(self) -> float:
         return self.swap_bytes / self.wall_s / 1e9 if self.wall_s > 0 else 0.0
+
+    @property
+    def observable_gbs(self) -> float:
+        t = self.observable_s if self.observable_s else self.wall_s
+        return self.swap_bytes / t / 1e9 if t > 0 else 0.0
 
 
 def prepare_memory(trace: Trace, config: ReplayConfig) -> HostMemory:
@@ -224,6 +233,7 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
         mark["t0"] = time.perf_counter()
 
     segments = None
+    observable = None
     if config.engine == "native" and config.native_dispatch == "replay":
         # trace -> sp_event arrays before the clock starts (trace loading, not engine work)
         cut = measure_from if measure_from else 0
@@ -236,7 +246,12 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
                 if i:
                     at_mark()
                 engine.replay_encoded(seg)
-            engine.finish()
+            if config.plane == "gpu":
+                engine.finish(drain_discarded=False)
+                observable = time.perf_counter() - mark["t0"]
+                engine.flush(wait=True)  # ... then the discarded encrypt-ahead drains too
+            else:
+                engine.finish()
         else:
             _dispatch_all(engine, blocks, trace, config, measure_from, at_mark)
     except Exception as exc:
@@ -245,7 +260,8 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
         return ReplayResult(engine, time.perf_counter() - mark["t0"], trace.swap_bytes(), trace.payload_bytes(),
                             f"{type(exc).__name__}: {exc}")
     wall = time.perf_counter() - mark["t0"]
-    return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
+    return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes(),
+                        observable_s=observable if segments is not None and config.plane == "gpu" else None)
 
 
 def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConfig, measure_from: int = 0,
