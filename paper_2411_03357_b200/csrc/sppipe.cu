@@ -93,6 +93,8 @@ struct Buf {
     std::vector<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
     uint64_t last_use = 0;
     cudaStream_t last_stream = nullptr;
+    uint32_t queued = 0;       // ops in the compute queue that touch this buffer (not yet issued)
+    uint32_t out_pending = 0;  // swap-out seals reading it, not yet launched
     void use(cudaStream_t s, const FenceP &f, uint64_t tick) {
         last_use = tick;
         last_stream = s;
@@ -707,14 +709,12 @@ class Plane {
         // the out stream (partial swap-outs keep the block buffer alive)
         for (int k = 0; k < op.nw; ++k) {
             const Buf *b = op.w[k].buf;
-            for (auto &x : outb.bufs)
-                if (x.get() == b) {
-                    launch_out();
-                    break;
-                }
+            if (b->out_pending) launch_out();
             for (auto &u : b->uses)
                 if (u.first == s.out && u.second && u.second->recorded) wait(s.comp, u.second);
         }
+        if (op.a) op.a->queued++;
+        if (op.b) op.b->queued++;
         ops.push_back(std::move(op));
         ops_bytes += nbytes;
         if (ops_bytes >= batch_bytes) flush();
@@ -796,8 +796,14 @@ class Plane {
             record(window, s.comp);
             ++tick;
             for (auto &op : q) {
-                if (op.a) op.a->use(s.comp, window, tick);
-                if (op.b) op.b->use(s.comp, window, tick);
+                if (op.a) {
+                    op.a->use(s.comp, window, tick);
+                    op.a->queued--;
+                }
+                if (op.b) {
+                    op.b->use(s.comp, window, tick);
+                    op.b->queued--;
+                }
             }
             for (auto &r : ring_pending) ring_commit(r.first, r.second, window);
             ring_pending.clear();
@@ -1127,11 +1133,7 @@ class Plane {
         uint64_t total = 0, first = spans[0].first;
         for (auto &sp : spans) total += sp.second;
         // the source's writer (a receiver open) must be issued before we can wait for it
-        for (const Op &op : ops)
-            if (op.a.get() == src.buf.get() || op.b.get() == src.buf.get()) {
-                flush();
-                break;
-            }
+        if (src.buf->queued) flush();
         for (auto &u : src.buf->uses)
             if (u.first != s.out && u.second && u.second->recorded) outb.waits.push_back(u.second);
         if (!outb.ready) outb.ready = new_fence();
@@ -1156,6 +1158,7 @@ class Plane {
         }
         outb.bufs.push_back(buf);
         outb.bufs.push_back(src.buf);
+        src.buf->out_pending++;
         outb.bytes += total;
         if (outb.bytes >= batch_bytes) launch_out();
         return msgs;
@@ -1170,7 +1173,10 @@ class Plane {
         ++launches;
         record(outb.ready, s.out);
         ++tick;
-        for (auto &b : outb.bufs) b->use(s.out, outb.ready, tick);
+        for (auto &b : outb.bufs) {
+            b->use(s.out, outb.ready, tick);
+            b->out_pending = 0;
+        }
         outb = OutBatch{};
     }
 
