@@ -612,6 +612,15 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
 
 // Build device message table for a batch; returns total rows.  mode: 0 all
 // seal, 1 all open, 2 per message (desc.reserved = SP_OP_SEAL / SP_OP_OPEN).
+// SPGCM_INLINE_BIG=0: batches above kInline always use the staging ring (A/B).
+bool inline_big_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("SPGCM_INLINE_BIG");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // With `big` non-null, a batch of kInline+1 .. kInlineBig messages goes
 // inline in *big (and *use_big is set) instead of through the staging ring.
 int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Workspace *ws, KParams &p,
@@ -642,7 +651,7 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
     if (use_big) *use_big = false;
     if ((uint32_t)n <= kInline) {
         memcpy(p.inl, ws->h_msgs.data(), (size_t)n * sizeof(MsgDev));
-    } else if (big && (uint32_t)n <= kInlineBig) {
+    } else if (big && (uint32_t)n <= kInlineBig && inline_big_enabled()) {
         memcpy(big->rk, p.rk, sizeof(p.rk));
         big->ttab = p.ttab;
         big->mg = p.mg;

@@ -368,7 +368,7 @@ class NativeEngine:
         once every observable result is final, leaving encrypt-ahead work of
         records discarded here to drain in the background (see
         sp_pipe_finish_observable)."""
-        if drain_discarded:
+        if drain_discarded or not hasattr(self._lib, "sp_pipe_finish_observable"):  # (older A/B builds)
             _check(self._lib.sp_pipe_finish(self._h))
         else:
             _check(self._lib.sp_pipe_finish_observable(self._h))

@@ -27,9 +27,11 @@ def best(fn, reps):
     return max(fn().swap_gbs for _ in range(reps))
 
 
-def main(out: str) -> None:
+def main(out: str, sizes_kib: list[int] | None = None) -> None:
     rows = []
-    for block in (64 * KIB, 256 * KIB, 1 * MIB, 4 * MIB, 16 * MIB, 32 * MIB, 64 * MIB, 128 * MIB, 256 * MIB):
+    sizes = [k * KIB for k in sizes_kib] if sizes_kib else \
+        (64 * KIB, 256 * KIB, 1 * MIB, 4 * MIB, 16 * MIB, 32 * MIB, 64 * MIB, 128 * MIB, 256 * MIB)
+    for block in sizes:
         t0 = time.time()
         tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=block)
         msg = min(block, 32 * MIB)
@@ -63,4 +65,5 @@ def main(out: str) -> None:
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/chunk_sweep.json")
+    main(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/chunk_sweep.json",
+         [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else None)
