@@ -41,6 +41,13 @@
 
 namespace sppipe {
 
+// Byte copy between UVA-mapped (pinned host or device) buffers, for small
+// ordered writes that must not use a copy engine.
+__global__ void k_bytes(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+
 // ---- error classes (Python exception names) -----------------------------------
 struct EngineErr : std::runtime_error { using std::runtime_error::runtime_error; };
 struct OverlapErr : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -130,6 +137,7 @@ struct Block {
     uint64_t base, len;
     int kind;
     uint8_t *host;
+    uint8_t *host_dev = nullptr;  // device-accessible alias of a pinned host block (UVA), else null
 };
 
 struct WriteGuard {
@@ -1336,17 +1344,28 @@ class Plane {
         if (reads) wait(s.host, reads);
         auto lr = host_ready.find(b.id);  // the block's last landing (or earlier app write)
         if (lr != host_ready.end() && lr->second) wait(s.host, lr->second);
-        // staged in the pinned ring and bounced through HBM by two async DMA
-        // copies (host-to-host cudaMemcpyAsync would block the caller until
-        // the stream drains; host functions stall on the callback thread)
+        // Staged in the mapped pinned ring; a small kernel then copies it into
+        // the (pinned, UVA-mapped) block over PCIe — no copy-engine transfer
+        // that could queue behind bulk swap copies.  Pageable blocks bounce
+        // through HBM with two DMA copies.  (A host-to-host cudaMemcpyAsync
+        // would block the caller until the stream drains; host functions
+        // stall on the callback thread.)
         uint8_t *h = ring_reserve(n);
         memcpy(h, data, n);
-        BufP tmp = alloc(n, s.host);
-        ck(cudaMemcpyAsync(tmp->ptr, h, n, cudaMemcpyHostToDevice, s.host), "app write H2D");
-        ck(cudaMemcpyAsync(b.host + offset, tmp->ptr, n, cudaMemcpyDeviceToHost, s.host), "app write D2H");
-        FenceP f = record_new(s.host);
+        FenceP f;
+        if (b.host_dev) {
+            const unsigned blocks = (unsigned)std::min<uint64_t>(148, (n + 4095) / 4096);
+            k_bytes<<<blocks, 256, 0, s.host>>>(b.host_dev + offset, h, n);
+            ck(cudaGetLastError(), "k_bytes(app write)");
+            f = record_new(s.host);
+        } else {
+            BufP tmp = alloc(n, s.host);
+            ck(cudaMemcpyAsync(tmp->ptr, h, n, cudaMemcpyHostToDevice, s.host), "app write H2D");
+            ck(cudaMemcpyAsync(b.host + offset, tmp->ptr, n, cudaMemcpyDeviceToHost, s.host), "app write D2H");
+            f = record_new(s.host);
+            tmp->use(s.host, f, ++tick);
+        }
         ring_commit(h, n, f);
-        tmp->use(s.host, f, ++tick);
         host_ready[b.id] = f;
     }
     void finish_streams() {
@@ -2298,7 +2317,14 @@ void sp_pipe_destroy(sp_pipe *p) { delete p; }
 
 int sp_pipe_register_block(sp_pipe *p, int64_t id, uint64_t base, uint64_t len, int32_t kind, void *host) {
     return guarded([&] {
-        p->e->mem.add_block(Block{id, base, len, kind, static_cast<uint8_t *>(host)});
+        Block b{id, base, len, kind, static_cast<uint8_t *>(host)};
+        if (host && !p->e->plane.dry) {
+            cudaPointerAttributes a;
+            if (cudaPointerGetAttributes(&a, host) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
+                b.host_dev = static_cast<uint8_t *>(a.devicePointer);
+            cudaGetLastError();  // pageable memory: clear the sticky query error
+        }
+        p->e->mem.add_block(b);
     });
 }
 int sp_pipe_seed_device(sp_pipe *p, int64_t block, const void *src, uint64_t len, int32_t src_is_device) {
