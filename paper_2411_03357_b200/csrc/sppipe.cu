@@ -481,13 +481,24 @@ class Plane {
         uint8_t *ptr;
         std::vector<std::pair<cudaStream_t, FenceP>> uses;
         cudaStream_t last;
+        uint64_t size;
     };
     std::vector<Garbage> garbage;
     bool collecting = false;
-    std::unordered_map<uint64_t, std::vector<Garbage>> cache;  // size class -> retired buffers
+    std::unordered_map<uint64_t, std::deque<Garbage>> cache;  // size class -> retired buffers, oldest first
     uint64_t cached_bytes = 0;
     bool closing = false;
     static constexpr uint64_t kCacheBytes = 8ull << 30;
+    uint64_t pool_bytes = 0;  // bytes this plane holds from the pool (in use or cached)
+    // SPPIPE_POOL_BUDGET_GB (default 16): past this, allocations wait for retired buffers
+    static uint64_t pool_budget() {
+        static const uint64_t b = [] {
+            const char *e = getenv("SPPIPE_POOL_BUDGET_GB");
+            const double gb = e ? atof(e) : 16.0;
+            return (uint64_t)(gb > 0 ? gb * (double)(1ull << 30) : 16.0 * (double)(1ull << 30));
+        }();
+        return b;
+    }
 
     // compute queue
     std::vector<Op> ops;
@@ -633,20 +644,40 @@ class Plane {
             const uint64_t cls = size_class(n);
             auto it = cache.find(cls);
             if (it != cache.end()) {
+                // oldest first: the likeliest to have every fence passed
                 auto &v = it->second;
-                const size_t lim = v.size() > 4 ? v.size() - 4 : 0;
-                for (size_t k = v.size(); k-- > lim;) {
+                const size_t lim = std::min<size_t>(v.size(), 8);
+                for (size_t k = 0; k < lim; ++k) {
                     if (!reusable(v[k], st)) continue;
                     b->ptr = v[k].ptr;
                     v.erase(v.begin() + (long)k);
                     cached_bytes -= cls;
                     break;
                 }
+                // Backpressure: past the pool budget, wait for the oldest
+                // retired buffer of this class instead of growing the pool
+                // (the host can run a whole trace ahead of the device; an
+                // unbounded lead turns into slow pool growth and HBM use).
+                if (!b->ptr && pool_bytes + cls > pool_budget()) trim_cache();
+                if (!b->ptr && !v.empty() && pool_bytes + cls > pool_budget()) {
+                    for (auto &u : v.front().uses) {
+                        if (u.second && u.second->recorded) {
+                            ck(cudaEventSynchronize(u.second->ev), "pool backpressure");
+                        } else if (u.first != st) {
+                            FenceP f = record_new(u.first);
+                            ck(cudaEventSynchronize(f->ev), "pool backpressure");
+                        }
+                    }
+                    b->ptr = v.front().ptr;
+                    v.erase(v.begin());
+                    cached_bytes -= cls;
+                }
             }
             if (!b->ptr) {
                 void *p = nullptr;
                 ck(cudaMallocFromPoolAsync(&p, cls, pool, st), "cudaMallocFromPoolAsync");
                 b->ptr = static_cast<uint8_t *>(p);
+                pool_bytes += cls;
             }
             b->alloc_size = cls;
             b->last_stream = st;
@@ -654,9 +685,34 @@ class Plane {
         }
         return b;
     }
+    // Return every cached buffer whose fences have all passed (idle) to the
+    // pool: frees budget for other size classes without waiting.
+    void trim_cache() {
+        for (auto &kv : cache) {
+            auto &v = kv.second;
+            size_t w = 0;
+            for (size_t k = 0; k < v.size(); ++k) {
+                bool idle = true;
+                for (auto &u : v[k].uses)
+                    if (u.second && (!u.second->recorded || !passed(*u.second))) {
+                        idle = false;
+                        break;
+                    }
+                if (idle) {
+                    ck(cudaFreeAsync(v[k].ptr, s.comp), "cudaFreeAsync(trim)");
+                    pool_bytes -= std::min(pool_bytes, kv.first);
+                    cached_bytes -= kv.first;
+                } else {
+                    if (w != k) v[w] = std::move(v[k]);
+                    ++w;
+                }
+            }
+            v.resize(w);
+        }
+    }
     void retire(Buf *b) {
         if (dry || !b->ptr) return;
-        Garbage g{b->ptr, std::move(b->uses), b->last_stream};
+        Garbage g{b->ptr, std::move(b->uses), b->last_stream, b->alloc_size};
         if (!closing && cached_bytes + b->alloc_size <= kCacheBytes) {
             cache[b->alloc_size].push_back(std::move(g));
             cached_bytes += b->alloc_size;
@@ -684,6 +740,7 @@ class Plane {
             }
             x.uses.clear();
             ck(cudaFreeAsync(x.ptr, fs), "cudaFreeAsync");
+            pool_bytes -= std::min(pool_bytes, x.size);
         }
         collecting = false;
     }
