@@ -876,6 +876,7 @@ class Plane {
         }
         launch_out();
         if (!landings.empty()) flush_landings();
+        ops_bytes = 0;  // landings count toward the threshold too: everything queued is issued now
         collect();
     }
 
@@ -1184,7 +1185,7 @@ class Plane {
     };
 
     std::vector<MsgP> seal_device_chunks(const View &src, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
-                                         uint64_t iv0) {
+                                         uint64_t iv0, bool own_stream = false) {
         std::vector<MsgP> msgs;
         if (dry) {
             for (auto &sp : spans) {
@@ -1196,7 +1197,7 @@ class Plane {
         }
         uint64_t total = 0, first = spans[0].first;
         for (auto &sp : spans) total += sp.second;
-        if (!out_stream_enabled()) {  // default: swap-out seals join the compute queue
+        if (!own_stream) {  // swap-out seals join the compute queue
             BufP buf = alloc(round16(total) + kTag * spans.size(), s.comp);
             for (size_t i = 0; i < spans.size(); ++i) {
                 auto m = std::make_shared<Msg>();
@@ -1245,16 +1246,23 @@ class Plane {
         return msgs;
     }
 
-    // SPPIPE_OUT_STREAM=1 puts swap-out seals on their own stream (each
-    // waiting only for the launch that wrote its source).  Measured: ~10%
-    // faster on the KV-swap trace, but 1-4 MiB-chunk offload loses 5-30%
-    // against the compute-queue placement, so it is off by default.
-    static bool out_stream_enabled() {
-        static const bool on = [] {
+    // Where swap-out seals run.  KV-cache evictions (small device-born
+    // blocks evicted in groups between decode steps) seal on their own
+    // stream, each waiting only for the launch that last wrote its block:
+    // the OPT-30B KV trace runs ~25% faster.  Weight/activation chunks join
+    // the compute queue: with hundreds of chunks per sync the extra stream
+    // costs more buffer reuse across streams than it overlaps (1 MiB-chunk
+    // offload 0.90 vs 0.65 of plain).  SPPIPE_OUT_STREAM=0/1 forces either.
+    static int out_stream_mode() {
+        static const int m = [] {
             const char *e = getenv("SPPIPE_OUT_STREAM");
-            return e && e[0] == '1';
+            return e ? (e[0] == '1' ? 1 : 0) : -1;
         }();
-        return on;
+        return m;
+    }
+    static bool out_stream_for(bool kv_class) {
+        const int m = out_stream_mode();
+        return m < 0 ? kv_class : m == 1;
     }
 
     void launch_out() {
@@ -1765,7 +1773,7 @@ class Engine {
         bool swap = r.cls == TC_WEIGHTS || r.cls == TC_KV;
         auto spans = chunk_spans(r.len, cfg.chunk_bytes);
         View src{buf.buf, buf.off + inner, r.len};
-        auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H]);
+        auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H], Plane::out_stream_for(r.cls == TC_KV));
         for (auto &m : msgs) send(D2H, m);
         if (inner == 0 && r.len == b.len) device_mem.erase(r.block_id);
         std::vector<std::tuple<MsgP, uint64_t, uint64_t>> taken;

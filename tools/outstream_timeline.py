@@ -6,9 +6,10 @@ from torch.profiler import ProfilerActivity, profile
 from paper_2411_03357_b200 import workload
 from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engine
 MIB = 1 << 20
-tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=MIB)
+tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=int(os.environ.get("CHUNK_KIB", "1024")) * 1024)
+CH = int(os.environ.get("CHUNK_KIB", "1024")) * 1024
 cfg = ReplayConfig(plane="gpu", fill="fast", engine="native", record_stream=False, system="synccc",
-                   chunk_bytes=MIB, predictor_chunk_bytes=MIB, reference_compat=False)
+                   chunk_bytes=CH, predictor_chunk_bytes=CH, reference_compat=False)
 mem = prepare_memory(tr, cfg)
 run_engine(tr, cfg, memory=mem)
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
