@@ -87,13 +87,16 @@ struct Fence {
     cudaStream_t stream = nullptr;
     bool recorded = false;
     bool complete = false;  // observed complete once (never re-recorded after that)
+    uint64_t seq = 0;       // record order: on one stream a higher seq completes later
     Plane *plane = nullptr;
     ~Fence();
 };
 using FenceP = std::shared_ptr<Fence>;
 
+struct Slab;
 struct Buf {
     Plane *plane = nullptr;
+    std::shared_ptr<Slab> slab;  // sub-allocation of a slab (small buffers), else null
     uint8_t *ptr = nullptr;
     uint64_t size = 0;
     uint64_t alloc_size = 0;
@@ -115,6 +118,18 @@ struct Buf {
     ~Buf();
 };
 using BufP = std::shared_ptr<Buf>;
+
+// Small buffers (<= 1 MiB: staging of small chunks, KV blocks, arenas) are
+// bump-allocated from 32 MiB slabs, one open slab per (stream, lane): a
+// sub-buffer costs no driver call (a pool allocation is ~1.5 us, per chunk
+// at 64 KiB blocks).  A dying sub-buffer folds its stream fences into the
+// slab; the slab retires (buffer cache, same reuse rules) when the last of
+// its sub-buffers is gone.  Ranges inside a slab are never reused while it
+// lives, so sub-buffers need no ordering among themselves.
+struct Slab {
+    BufP big;
+    uint64_t off = 0;
+};
 
 // A sealed message on the wire (channel.CiphertextMsg / DeviceCiphertext).
 struct Msg {
@@ -572,6 +587,7 @@ class Plane {
         h2d_done.clear();
         arena_dev.reset();
         window.reset();
+        slabs.clear();
         for (auto &kv : cache)
             for (auto &g : kv.second) garbage.push_back(std::move(g));
         cache.clear();
@@ -600,10 +616,12 @@ class Plane {
         }
         return f;
     }
+    uint64_t record_seq = 0;
     void record(const FenceP &f, cudaStream_t st) {
         ck(cudaEventRecord(f->ev, st), "cudaEventRecord");
         f->stream = st;
         f->recorded = true;
+        f->seq = ++record_seq;
     }
     FenceP record_new(cudaStream_t st) {
         FenceP f = new_fence();
@@ -636,7 +654,37 @@ class Plane {
         }
         return true;
     }
-    BufP alloc(uint64_t n, cudaStream_t st) {
+    static constexpr uint64_t kSlabBytes = 32ull << 20, kSlabMax = 1ull << 20;
+    static bool slabs_enabled() {  // SPPIPE_SLAB=0: every buffer from the pool / cache
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_SLAB");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+    std::map<std::pair<cudaStream_t, int>, std::shared_ptr<Slab>> slabs;  // open slab per (stream, lane)
+    // lane separates lifetimes: 0 = transient staging, 1 = device copies of blocks
+    BufP alloc(uint64_t n, cudaStream_t st, int lane = 0) {
+        if (!dry && n <= kSlabMax && slabs_enabled()) {
+            auto &sl = slabs[{st, lane}];
+            const uint64_t need = (std::max<uint64_t>(n, 16) + 255u) & ~uint64_t(255);
+            if (!sl || sl->off + need > sl->big->size) {
+                sl = std::make_shared<Slab>();
+                sl->big = alloc_whole(kSlabBytes, st);
+            }
+            auto b = std::make_shared<Buf>();
+            b->plane = this;
+            b->size = n;
+            b->ptr = sl->big->ptr + sl->off;
+            sl->off += need;
+            b->slab = sl;
+            b->last_stream = st;
+            b->uses.emplace_back(st, FenceP());
+            return b;
+        }
+        return alloc_whole(n, st);
+    }
+    BufP alloc_whole(uint64_t n, cudaStream_t st) {
         auto b = std::make_shared<Buf>();
         b->plane = this;
         b->size = n;
@@ -1361,7 +1409,7 @@ class Plane {
         if (ops_bytes >= batch_bytes) flush();
     }
 
-    View new_device_buffer(uint64_t n) { return View{alloc(n, s.comp), 0, n}; }
+    View new_device_buffer(uint64_t n) { return View{alloc(n, s.comp, 1), 0, n}; }
 
     // Device-only bytes carved from the current small-payload arena (open
     // destinations of NOPs and token messages): no allocation per message.
@@ -1468,6 +1516,33 @@ Fence::~Fence() {
     if (plane && ev) plane->free_events.push_back(ev);
 }
 Buf::~Buf() {
+    if (slab) {
+        // fold this sub-buffer's uses into the slab (latest recorded fence
+        // per stream; unrecorded ones are kept alongside, as extra entries)
+        Buf &into = *slab->big;
+        for (auto &u : uses) {
+            bool merged = false;
+            for (auto &v : into.uses) {
+                if (v.first != u.first) continue;
+                if (!u.second || v.second == u.second) {
+                    merged = true;
+                } else if (!v.second) {
+                    v.second = u.second;
+                    merged = true;
+                } else if (v.second->recorded && u.second->recorded) {
+                    if (u.second->seq > v.second->seq) v.second = u.second;
+                    merged = true;
+                }
+                if (merged) break;
+            }
+            if (!merged) into.uses.push_back(u);
+        }
+        if (last_use >= into.last_use) {
+            into.last_use = last_use;
+            into.last_stream = last_stream;
+        }
+        return;  // the slab member releases the slab (and, last, the slab buffer)
+    }
     if (plane) plane->retire(this);
 }
 
@@ -2154,7 +2229,7 @@ class Engine {
                 if (pout.blocks.count(e.block)) flush_out();  // its last swap-out lands first
                 auto it = landed.find(e.block);
                 if (it != landed.end()) pl.wait(pl.s.h2d, it->second);
-                View v{pl.alloc(b.len, pl.s.h2d), 0, b.len};
+                View v{pl.alloc(b.len, pl.s.h2d, 1), 0, b.len};
                 pin.add(v.ptr(), b.host, b.len, v.buf, e.block);
                 dev[e.block] = v;
                 if (pin.bytes >= kBatch) flush_in();
