@@ -37,6 +37,7 @@
 #include "spgcm.h"
 #include "spguard.h"
 #include "sppipe.h"
+#include "sppool.hpp"
 #include "sppred.hpp"
 
 namespace sppipe {
@@ -88,6 +89,7 @@ struct Fence {
     bool recorded = false;
     bool complete = false;  // observed complete once (never re-recorded after that)
     uint64_t seq = 0;       // record order: on one stream a higher seq completes later
+    uint64_t mark = 0;      // de-duplicates waits within one issue pass
     Plane *plane = nullptr;
     ~Fence();
 };
@@ -100,10 +102,13 @@ struct Buf {
     uint8_t *ptr = nullptr;
     uint64_t size = 0;
     uint64_t alloc_size = 0;
-    std::vector<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
+    PVec<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
     uint64_t last_use = 0;
     cudaStream_t last_stream = nullptr;
     uint32_t queued = 0;       // ops in the compute queue that touch this buffer (not yet issued)
+    // flush-local list of the regions queued ops touch (Plane::flush)
+    mutable uint64_t touch_epoch = 0;
+    mutable int32_t touch_head = -1;
     uint32_t out_pending = 0;  // swap-out seals reading it, not yet launched
     void use(cudaStream_t s, const FenceP &f, uint64_t tick) {
         last_use = tick;
@@ -139,6 +144,7 @@ struct Msg {
     FenceP ready;  // producer's fence (recorded at its launch)
 };
 using MsgP = std::shared_ptr<Msg>;
+using Spans = PVec<std::pair<uint64_t, uint64_t>>;  // (offset, length) of the messages of one transfer
 
 struct View {
     BufP buf;
@@ -166,8 +172,8 @@ class HostMem {
     // id -> block (ids are small and dense, memory.py:117-166); stable addresses
     std::vector<std::unique_ptr<Block>> blocks;
     std::map<uint64_t, int64_t> by_base;        // base -> id
-    std::map<int64_t, WriteGuard> write_guards;  // owner (record id) -> guard (insertion order == id order)
-    std::map<int64_t, std::pair<uint64_t, uint64_t>> read_guards;  // task id -> (base, len)
+    PMap<int64_t, WriteGuard> write_guards;  // owner (record id) -> guard (insertion order == id order)
+    PMap<int64_t, std::pair<uint64_t, uint64_t>> read_guards;  // task id -> (base, len)
 
     Block &block(int64_t id) {
         if (id < 0 || id >= (int64_t)blocks.size() || !blocks[(size_t)id]) throw KeyErr(std::to_string(id));
@@ -215,10 +221,10 @@ class HostMem {
     // Read guards are disjoint (install rejects overlaps), so an index by
     // base answers overlap queries in O(log n + k); results come back in task
     // id order = the reference's dict insertion order (memory.py:244-259).
-    std::map<uint64_t, std::pair<uint64_t, int64_t>> rg_by_base;  // base -> (len, task)
+    PMap<uint64_t, std::pair<uint64_t, int64_t>> rg_by_base;  // base -> (len, task)
 
-    std::vector<int64_t> read_guards_over(uint64_t base, uint64_t len) const {
-        std::vector<int64_t> out;
+    PVec<int64_t> read_guards_over(uint64_t base, uint64_t len) const {
+        PVec<int64_t> out;
         if (!len) return out;
         auto it = rg_by_base.lower_bound(base);
         if (it != rg_by_base.begin()) {
@@ -252,8 +258,8 @@ enum Verdict { V_HIT = 0, V_AHEAD = 1, V_BEHIND = 2, V_STALE = 3, V_MISS = 4, V_
 struct Record {
     int64_t id;
     uint64_t base, len, iv;
-    std::vector<MsgP> chunks;  // released (emptied) once the record leaves the window
-    std::vector<uint64_t> chunk_lens;
+    PVec<MsgP> chunks;  // released (emptied) once the record leaves the window
+    PVec<uint64_t> chunk_lens;
     RecState state = PENDING;
     int64_t block_id;  // INT64_MIN = None
     uint64_t span() const { return chunk_lens.size(); }
@@ -275,16 +281,16 @@ class Validator {
     uint64_t window;
     std::deque<Record> records;  // id i at index i-1
     int64_t next_id = 1;
-    std::unordered_map<RangeKey, int64_t, RangeHash> by_range, stale;
-    std::unordered_map<uint64_t, int64_t> by_iv;
-    std::set<int64_t> order;                        // pending ids (label order == id order)
-    std::set<std::pair<uint64_t, int64_t>> bases;  // (base, id) of pending
+    PUMap<RangeKey, int64_t, RangeHash> by_range, stale;
+    PUMap<uint64_t, int64_t> by_iv;
+    PSet<int64_t> order;                        // pending ids (label order == id order)
+    PSet<std::pair<uint64_t, int64_t>> bases;  // (base, id) of pending
     int64_t counters[5] = {0, 0, 0, 0, 0};
     int64_t evicted = 0;
 
     Record &rec(int64_t id) { return records[(size_t)(id - 1)]; }
 
-    int64_t label(std::vector<MsgP> chunks, std::vector<uint64_t> lens, uint64_t base, uint64_t len, uint64_t iv,
+    int64_t label(PVec<MsgP> chunks, PVec<uint64_t> lens, uint64_t base, uint64_t len, uint64_t iv,
                   int64_t block_id) {
         // pending ranges are disjoint: only the last one starting below the end can intersect
         auto it = bases.lower_bound({base + len, INT64_MIN});
@@ -478,7 +484,7 @@ struct CopyBatch {
 
 struct Landing {
     Block *block;
-    std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;  // msg, iv, offset in block
+    PVec<std::tuple<MsgP, uint64_t, uint64_t>> jobs;  // msg, iv, offset in block
     int dir;
 };
 
@@ -494,7 +500,7 @@ class Plane {
     std::vector<cudaEvent_t> free_events;
     struct Garbage {
         uint8_t *ptr;
-        std::vector<std::pair<cudaStream_t, FenceP>> uses;
+        PVec<std::pair<cudaStream_t, FenceP>> uses;
         cudaStream_t last;
         uint64_t size;
     };
@@ -516,7 +522,18 @@ class Plane {
     }
 
     // compute queue
-    std::vector<Op> ops;
+    std::vector<Op> ops, ops_spare;
+    struct Touch {
+        uint64_t lo, hi;
+        int level;
+        bool write;
+        int32_t next;
+    };
+    std::vector<Touch> touches;
+    std::vector<int> op_level;
+    std::vector<uint32_t> level_start, by_level;
+    std::vector<sp_desc> descs_scratch;
+    uint64_t touch_epoch = 0, mark_seq = 0;
     uint64_t ops_bytes = 0;
     FenceP window;
     // small-payload arena
@@ -542,9 +559,9 @@ class Plane {
     uint64_t ring_pending_bytes = 0;
     // landings
     std::vector<Landing> landings;
-    std::unordered_set<int64_t> landing_blocks;
-    std::unordered_map<int64_t, FenceP> host_ready;  // block -> fence after last D2H into it
-    std::unordered_map<int64_t, FenceP> h2d_done;    // block -> fence after last H2D from it
+    PUSet<int64_t> landing_blocks;
+    PUMap<int64_t, FenceP> host_ready;  // block -> fence after last D2H into it
+    PUMap<int64_t, FenceP> h2d_done;    // block -> fence after last H2D from it
     CopyBatch otf_copies;                             // on-the-fly staging copies (issued at flush)
     // Swap-out seals on their own stream (SPPIPE_OUT_STREAM=1, see
     // out_stream_enabled): each waits only for the launch that last wrote
@@ -606,7 +623,7 @@ class Plane {
 
     // -- events / buffers --------------------------------------------------------------
     FenceP new_fence() {
-        auto f = std::make_shared<Fence>();
+        auto f = pmake<Fence>();
         f->plane = this;
         if (!free_events.empty()) {
             f->ev = free_events.back();
@@ -669,10 +686,10 @@ class Plane {
             auto &sl = slabs[{st, lane}];
             const uint64_t need = (std::max<uint64_t>(n, 16) + 255u) & ~uint64_t(255);
             if (!sl || sl->off + need > sl->big->size) {
-                sl = std::make_shared<Slab>();
+                sl = pmake<Slab>();
                 sl->big = alloc_whole(kSlabBytes, st);
             }
-            auto b = std::make_shared<Buf>();
+            auto b = pmake<Buf>();
             b->plane = this;
             b->size = n;
             b->ptr = sl->big->ptr + sl->off;
@@ -685,7 +702,7 @@ class Plane {
         return alloc_whole(n, st);
     }
     BufP alloc_whole(uint64_t n, cudaStream_t st) {
-        auto b = std::make_shared<Buf>();
+        auto b = pmake<Buf>();
         b->plane = this;
         b->size = n;
         if (!dry) {
@@ -863,43 +880,62 @@ class Plane {
         if (!ops.empty()) {
             std::vector<Op> q;
             q.swap(ops);
+            ops.swap(ops_spare);  // keep the queue's capacity across flushes
             ops_bytes = 0;
-            // level = 1 + max level of the earlier ops it conflicts with
-            struct Touch {
-                uint64_t lo, hi;
-                int level;
-                bool write;
+            // level = 1 + max level of the earlier ops it conflicts with;
+            // per-buffer touch lists live in `touches` (no per-flush maps)
+            ++touch_epoch;
+            touches.clear();
+            auto head = [&](const Buf *b) -> int32_t & {
+                if (b->touch_epoch != touch_epoch) {
+                    b->touch_epoch = touch_epoch;
+                    b->touch_head = -1;
+                }
+                return b->touch_head;
             };
-            std::unordered_map<const Buf *, std::vector<Touch>> touched;
-            std::vector<int> level(q.size(), 0);
+            op_level.assign(q.size(), 0);
             int top = 0;
             for (size_t i = 0; i < q.size(); ++i) {
                 const Op &op = q[i];
                 int lv = 0;
                 auto scan = [&](const Region &rg, bool write) {
-                    auto it = touched.find(rg.buf);
-                    if (it == touched.end()) return;
-                    for (const Touch &t : it->second)
-                        if ((write || t.write) && t.lo < rg.hi && rg.lo < t.hi) lv = std::max(lv, t.level + 1);
+                    for (int32_t t = head(rg.buf); t >= 0; t = touches[t].next) {
+                        const Touch &x = touches[t];
+                        if ((write || x.write) && x.lo < rg.hi && rg.lo < x.hi) lv = std::max(lv, x.level + 1);
+                    }
                 };
                 for (int k = 0; k < op.nr; ++k) scan(op.r[k], false);
                 for (int k = 0; k < op.nw; ++k) scan(op.w[k], true);
-                level[i] = lv;
+                op_level[i] = lv;
                 top = std::max(top, lv);
-                for (int k = 0; k < op.nr; ++k) touched[op.r[k].buf].push_back({op.r[k].lo, op.r[k].hi, lv, false});
-                for (int k = 0; k < op.nw; ++k) touched[op.w[k].buf].push_back({op.w[k].lo, op.w[k].hi, lv, true});
+                auto add = [&](const Region &rg, bool write) {
+                    int32_t &h = head(rg.buf);
+                    touches.push_back({rg.lo, rg.hi, lv, write, h});
+                    h = (int32_t)touches.size() - 1;
+                };
+                for (int k = 0; k < op.nr; ++k) add(op.r[k], false);
+                for (int k = 0; k < op.nw; ++k) add(op.w[k], true);
             }
-            std::vector<sp_desc> descs;
-            std::unordered_set<Fence *> waited;
+            // ops grouped by level, queue order kept inside a level
+            level_start.assign((size_t)top + 2, 0);
+            for (int lv : op_level) level_start[(size_t)lv + 1]++;
+            for (int lv = 0; lv <= top; ++lv) level_start[(size_t)lv + 1] += level_start[(size_t)lv];
+            by_level.resize(q.size());
+            {
+                std::vector<uint32_t> fill(level_start.begin(), level_start.end() - 1);
+                for (size_t i = 0; i < q.size(); ++i) by_level[fill[(size_t)op_level[i]]++] = (uint32_t)i;
+            }
+            const uint64_t mk = ++mark_seq;
+            auto &descs = descs_scratch;
             for (int lv = 0; lv <= top; ++lv) {
                 descs.clear();
-                for (size_t i = 0; i < q.size(); ++i) {
-                    if (level[i] != lv) continue;
-                    if (q[i].wait && !waited.count(q[i].wait.get())) {
-                        wait(s.comp, q[i].wait);
-                        waited.insert(q[i].wait.get());
+                for (uint32_t k = level_start[(size_t)lv]; k < level_start[(size_t)lv + 1]; ++k) {
+                    const Op &op = q[by_level[k]];
+                    if (op.wait && op.wait->mark != mk) {
+                        wait(s.comp, op.wait);
+                        op.wait->mark = mk;
                     }
-                    descs.push_back(q[i].d);
+                    descs.push_back(op.d);
                 }
                 if (descs.empty()) continue;
                 ck_sp(sp_crypt_batch(ctx, descs.data(), (int)descs.size(), s.comp), "sp_crypt_batch");
@@ -921,6 +957,8 @@ class Plane {
             ring_pending.clear();
             ring_pending_bytes = 0;
             window = new_fence();
+            q.clear();
+            if (q.capacity() > ops_spare.capacity()) ops_spare.swap(q);
         }
         launch_out();
         if (!landings.empty()) flush_landings();
@@ -1109,7 +1147,7 @@ class Plane {
     // H2D the plaintext of `block` [inner+off, +n) per span into one staging
     // buffer; returns the staging buffer (payload views at off-first, tags after).
     // The copy joins `cb` (issued with its batch); `done` is the batch fence.
-    BufP stage_h2d(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, FenceP &done,
+    BufP stage_h2d(Block &b, uint64_t inner, const Spans &spans, FenceP &done,
                    CopyBatch &cb) {
         before_host_read_of(b.id);
         uint64_t total = 0;
@@ -1129,12 +1167,12 @@ class Plane {
         return buf;
     }
 
-    std::vector<MsgP> seal_host_chunks(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans,
+    PVec<MsgP> seal_host_chunks(Block &b, uint64_t inner, const Spans &spans,
                                        int dir, uint64_t iv0) {
-        std::vector<MsgP> msgs;
+        PVec<MsgP> msgs;
         if (dry) {
             for (auto &sp : spans) {
-                auto m = std::make_shared<Msg>();
+                auto m = pmake<Msg>();
                 m->len = sp.second;
                 msgs.push_back(m);
                 bytes_h2d += sp.second;
@@ -1146,7 +1184,7 @@ class Plane {
         uint64_t first = spans[0].first, total = 0;
         for (auto &sp : spans) total += sp.second;
         for (size_t i = 0; i < spans.size(); ++i) {
-            auto m = std::make_shared<Msg>();
+            auto m = pmake<Msg>();
             m->buf = buf;
             m->off = spans[i].first - first;
             m->len = spans[i].second;
@@ -1176,12 +1214,12 @@ class Plane {
         ~SpecBatch() {
             if (p->spec_copies == &copies) p->spec_copies = nullptr;
         }
-        std::vector<MsgP> add(Block &b, uint64_t inner, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
+        PVec<MsgP> add(Block &b, uint64_t inner, const Spans &spans, int dir,
                               uint64_t iv0) {
-            std::vector<MsgP> msgs;
+            PVec<MsgP> msgs;
             if (p->dry) {
                 for (auto &sp : spans) {
-                    auto m = std::make_shared<Msg>();
+                    auto m = pmake<Msg>();
                     m->len = sp.second;
                     msgs.push_back(m);
                     p->bytes_h2d += sp.second;
@@ -1195,7 +1233,7 @@ class Plane {
             uint64_t first = spans[0].first, total = 0;
             for (auto &sp : spans) total += sp.second;
             for (size_t i = 0; i < spans.size(); ++i) {
-                auto m = std::make_shared<Msg>();
+                auto m = pmake<Msg>();
                 m->buf = buf;
                 m->off = spans[i].first - first;
                 m->len = spans[i].second;
@@ -1232,12 +1270,12 @@ class Plane {
         }
     };
 
-    std::vector<MsgP> seal_device_chunks(const View &src, const std::vector<std::pair<uint64_t, uint64_t>> &spans, int dir,
+    PVec<MsgP> seal_device_chunks(const View &src, const Spans &spans, int dir,
                                          uint64_t iv0, bool own_stream = false) {
-        std::vector<MsgP> msgs;
+        PVec<MsgP> msgs;
         if (dry) {
             for (auto &sp : spans) {
-                auto m = std::make_shared<Msg>();
+                auto m = pmake<Msg>();
                 m->len = sp.second;
                 msgs.push_back(m);
             }
@@ -1248,7 +1286,7 @@ class Plane {
         if (!own_stream) {  // swap-out seals join the compute queue
             BufP buf = alloc(round16(total) + kTag * spans.size(), s.comp);
             for (size_t i = 0; i < spans.size(); ++i) {
-                auto m = std::make_shared<Msg>();
+                auto m = pmake<Msg>();
                 m->buf = buf;
                 m->off = spans[i].first - first;
                 m->len = spans[i].second;
@@ -1269,7 +1307,7 @@ class Plane {
         if (!outb.ready) outb.ready = new_fence();
         BufP buf = alloc(round16(total) + kTag * spans.size(), s.out);
         for (size_t i = 0; i < spans.size(); ++i) {
-            auto m = std::make_shared<Msg>();
+            auto m = pmake<Msg>();
             m->buf = buf;
             m->off = spans[i].first - first;
             m->len = spans[i].second;
@@ -1330,12 +1368,12 @@ class Plane {
     }
 
     // NOP pads and token I/O: staged in the byte arena (one PCIe copy per flush).
-    std::vector<MsgP> seal_bytes(const std::vector<std::pair<const uint8_t *, uint64_t>> &payloads, int dir, uint64_t iv0,
+    PVec<MsgP> seal_bytes(const std::vector<std::pair<const uint8_t *, uint64_t>> &payloads, int dir, uint64_t iv0,
                                  bool nop) {
-        std::vector<MsgP> msgs;
+        PVec<MsgP> msgs;
         for (size_t i = 0; i < payloads.size(); ++i) {
             uint64_t n = payloads[i].second;
-            auto m = std::make_shared<Msg>();
+            auto m = pmake<Msg>();
             m->len = n;
             m->nop = nop;
             if (!dry) {
@@ -1382,7 +1420,7 @@ class Plane {
 
     // -- opens ----------------------------------------------------------------------------
     // jobs: (msg, iv, dst view or empty) -> queued receiver opens.
-    void open_into(std::vector<std::tuple<MsgP, uint64_t, View>> &jobs, int dir) {
+    void open_into(PVec<std::tuple<MsgP, uint64_t, View>> &jobs, int dir) {
         if (dry) return;
         for (auto &j : jobs) {
             const MsgP &m = std::get<0>(j);
@@ -1396,7 +1434,7 @@ class Plane {
         }
     }
 
-    void land_on_host(Block &b, std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs, int dir) {
+    void land_on_host(Block &b, PVec<std::tuple<MsgP, uint64_t, uint64_t>> jobs, int dir) {
         uint64_t n = 0;
         for (auto &j : jobs) n += std::get<0>(j)->len;
         if (dry) {
@@ -1584,7 +1622,7 @@ struct Suspended {
 struct Deferred {
     int64_t task_id, block_id;
     uint64_t base, len;
-    std::vector<std::tuple<MsgP, uint64_t, uint64_t>> chunks;  // msg, iv, offset
+    PVec<std::tuple<MsgP, uint64_t, uint64_t>> chunks;  // msg, iv, offset
     bool done = false, landing = false;
 };
 struct Meta {
@@ -1604,8 +1642,8 @@ struct Recorded {
 
 constexpr int64_t NONE = INT64_MIN;
 
-std::vector<std::pair<uint64_t, uint64_t>> chunk_spans(uint64_t length, uint64_t chunk) {
-    std::vector<std::pair<uint64_t, uint64_t>> out;
+Spans chunk_spans(uint64_t length, uint64_t chunk) {
+    Spans out;
     for (uint64_t off = 0; off < length; off += chunk) out.push_back({off, std::min(chunk, length - off)});
     return out;
 }
@@ -1625,13 +1663,13 @@ class Engine {
     uint64_t initial_send_iv;
     std::deque<SpecTask> spec_queue;
     std::vector<Suspended> suspended;
-    std::set<uint64_t> suspended_seqs;
+    PSet<uint64_t> suspended_seqs;
     std::vector<int64_t> batch_ins, predicted_queue;
-    std::map<int64_t, Deferred> deferred;
+    PMap<int64_t, Deferred> deferred;
     int64_t next_task_id = 1;
     uint64_t next_seq = 0, next_label_iv = 0;
     std::deque<Meta> h2d_meta;
-    std::unordered_map<int64_t, View> device_mem;
+    PUMap<int64_t, View> device_mem;
     std::vector<Recorded> delivered, d2h_stream;
     int64_t ring_occupied = 0, ring_high = 0, ring_insertions = 0, ring_violations = 0;
 
@@ -1703,7 +1741,7 @@ class Engine {
     void land(Deferred &t) {
         Block &b = mem.block(t.block_id);
         uint64_t inner = t.base - b.base;
-        std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
+        PVec<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
         for (auto &c : t.chunks) jobs.emplace_back(std::get<0>(c), std::get<1>(c), inner + std::get<2>(c));
         plane.land_on_host(b, std::move(jobs), D2H);
         t.landing = true;
@@ -1723,7 +1761,7 @@ class Engine {
 
     // GPU endpoint receives everything queued on the H2D lane: one batched open.
     void drain_gpu() {
-        std::vector<std::tuple<MsgP, uint64_t, View>> jobs;
+        PVec<std::tuple<MsgP, uint64_t, View>> jobs;
         while (pending(H2D)) {
             auto mi = take(H2D);
             Meta meta = h2d_meta.front();
@@ -1819,12 +1857,12 @@ class Engine {
             throw EngineErr("commit at counter " + std::to_string(send_iv[H2D]) + " for record at " + std::to_string(rec.iv));
         val.commit(rid);
         uint64_t off = 0;
-        std::vector<MsgP> chunks = val.rec(rid).chunks;
-        std::vector<uint64_t> lens = val.rec(rid).chunk_lens;
+        PVec<MsgP> chunks = val.rec(rid).chunks;
+        PVec<uint64_t> lens = val.rec(rid).chunk_lens;
         int64_t block_id = val.rec(rid).block_id;
         uint64_t base = val.rec(rid).base;
         for (size_t i = 0; i < lens.size(); ++i) {
-            MsgP m = plane.dry ? std::make_shared<Msg>() : chunks[i];
+            MsgP m = plane.dry ? pmake<Msg>() : chunks[i];
             if (plane.dry) m->len = lens[i];
             send_h2d(m, rid, Meta{0, sq, block_id, base, off, lens[i]}, sq);
             off += lens[i];
@@ -1851,7 +1889,7 @@ class Engine {
         auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H], Plane::out_stream_for(r.cls == TC_KV));
         for (auto &m : msgs) send(D2H, m);
         if (inner == 0 && r.len == b.len) device_mem.erase(r.block_id);
-        std::vector<std::tuple<MsgP, uint64_t, uint64_t>> taken;
+        PVec<std::tuple<MsgP, uint64_t, uint64_t>> taken;
         for (auto &sp : spans) {
             auto mi = take(D2H);
             taken.emplace_back(mi.first, mi.second, sp.first);
@@ -1870,7 +1908,7 @@ class Engine {
             counters[C_DEFERRED_DECRYPTS]++;
             act(SP_ACT_D2H_DATA, -1, r.len, -1, tid, false, false, 0, (int64_t)sq);
         } else {
-            std::vector<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
+            PVec<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
             for (auto &t : taken) jobs.emplace_back(std::get<0>(t), std::get<1>(t), inner + std::get<2>(t));
             plane.land_on_host(b, std::move(jobs), D2H);
             act(SP_ACT_D2H_DATA, -1, r.len, -1, -1, true, false, 0, (int64_t)sq);
@@ -1894,7 +1932,7 @@ class Engine {
             send(D2H, msgs[0]);
             auto mi = take(D2H);
             View dst = plane.dry ? View{} : plane.arena_scratch(size);
-            std::vector<std::tuple<MsgP, uint64_t, View>> jobs{{mi.first, mi.second, dst}};
+            PVec<std::tuple<MsgP, uint64_t, View>> jobs{{mi.first, mi.second, dst}};
             plane.open_into(jobs, D2H);
             if (cfg.record_stream) d2h_stream.push_back({sq, 0, size, dst});
             counters[C_SYNC_DECRYPTS]++;
@@ -2033,9 +2071,9 @@ class Engine {
             Block &b = mem.block(t.block_id);
             auto spans = chunk_spans(t.len, cfg.chunk_bytes);
             auto msgs = batch.add(b, t.base - b.base, spans, H2D, t.iv);
-            std::vector<uint64_t> lens;
+            PVec<uint64_t> lens;
             for (auto &sp : spans) lens.push_back(sp.second);
-            int64_t rid = val.label(plane.dry ? std::vector<MsgP>() : msgs, lens, t.base, t.len, t.iv, t.block_id);
+            int64_t rid = val.label(plane.dry ? PVec<MsgP>() : std::move(msgs), std::move(lens), t.base, t.len, t.iv, t.block_id);
             counters[C_SPEC_ENCRYPTS]++;
             act(SP_ACT_SPEC_ENCRYPT, (int64_t)t.iv, t.len, rid);
         }
@@ -2111,7 +2149,12 @@ class Engine {
             size_t k = batch.size();
             bool hit = false;
             if (predicted_queue.size() >= k) {
-                std::set<int64_t> a(predicted_queue.begin(), predicted_queue.begin() + (long)k), b(batch.begin(), batch.end());
+                // set equality (the reference compares sets, engine.py:566-571)
+                std::vector<int64_t> a(predicted_queue.begin(), predicted_queue.begin() + (long)k), b(batch);
+                std::sort(a.begin(), a.end());
+                a.erase(std::unique(a.begin(), a.end()), a.end());
+                std::sort(b.begin(), b.end());
+                b.erase(std::unique(b.begin(), b.end()), b.end());
                 hit = a == b;
             }
             if (hit) {
