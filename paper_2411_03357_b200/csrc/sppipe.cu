@@ -404,6 +404,15 @@ std::map<int, Streams> g_streams;
 std::map<int, DevicePool> g_pools;
 std::map<std::pair<int, std::string>, sp_ctx *> g_ctx;  // key setup once per (device, key)
 std::vector<std::pair<uint8_t *, uint64_t>> g_rings;    // idle pinned staging rings (process-wide)
+// Device buffers of destroyed pipes, idle (their streams were drained):
+// the next pipe on the device takes them without a pool call (a pipe per
+// replay / bench repetition would otherwise re-carve its whole working set).
+struct IdleBufs {
+    std::unordered_map<uint64_t, std::vector<uint8_t *>> by_size;
+    uint64_t bytes = 0;
+};
+std::map<int, IdleBufs> g_idle;
+constexpr uint64_t kIdleBytes = 16ull << 30;
 
 sp_ctx *ctx_for(int dev, const uint8_t key[32]) {
     std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -593,20 +602,33 @@ class Plane {
     }
     ~Plane() {
         if (dry) return;
+        bool idle = true;
         try {
             finish_streams();
         } catch (...) {
+            idle = false;
         }
-        closing = true;
         ops.clear();
         landings.clear();
         host_ready.clear();
         h2d_done.clear();
         arena_dev.reset();
         window.reset();
-        slabs.clear();
-        for (auto &kv : cache)
-            for (auto &g : kv.second) garbage.push_back(std::move(g));
+        slabs.clear();  // open slabs retire into the cache
+        closing = true;
+        {
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            IdleBufs &ib = g_idle[dev];
+            for (auto &kv : cache)
+                for (auto &g : kv.second) {
+                    if (idle && ib.bytes + kv.first <= kIdleBytes) {
+                        ib.by_size[kv.first].push_back(g.ptr);
+                        ib.bytes += kv.first;
+                    } else {
+                        garbage.push_back(std::move(g));
+                    }
+                }
+        }
         cache.clear();
         collect();
         cudaStreamSynchronize(s.comp);
@@ -736,6 +758,17 @@ class Plane {
                     b->ptr = v.front().ptr;
                     v.erase(v.begin());
                     cached_bytes -= cls;
+                }
+            }
+            if (!b->ptr) {
+                std::lock_guard<std::mutex> lk(g_dev_mu);
+                IdleBufs &ib = g_idle[dev];
+                auto it = ib.by_size.find(cls);
+                if (it != ib.by_size.end() && !it->second.empty()) {
+                    b->ptr = it->second.back();
+                    it->second.pop_back();
+                    ib.bytes -= cls;
+                    pool_bytes += cls;
                 }
             }
             if (!b->ptr) {

@@ -46,7 +46,7 @@ def main(out: str, sizes_kib: list[int] | None = None) -> None:
         r = run_engine(tr, spec, memory=mem)
         rep = r.engine.report()
         del r
-        reps = 2
+        reps = int(os.environ.get("SWEEP_REPS", "2"))
         plain = best(lambda: run_plain_native(tr, spec, memory=mem), reps)
         enc = best(lambda: run_engine(tr, spec, memory=mem), reps)
         run_engine(tr, sync, memory=mem)
