@@ -137,11 +137,17 @@ struct Slab {
 };
 
 // A sealed message on the wire (channel.CiphertextMsg / DeviceCiphertext).
+struct View;
 struct Msg {
     BufP buf;  // payload at off, tag at tag_off (null in the dry plane)
     uint64_t off = 0, tag_off = 0, len = 0;
     bool nop = false;
     FenceP ready;  // producer's fence (recorded at its launch)
+    // H2D messages are opened on the device when sent (Engine::eager_open):
+    // the IV and destination of that open
+    bool opened = false;
+    uint64_t open_iv = 0;
+    std::shared_ptr<View> open_dst;
 };
 using MsgP = std::shared_ptr<Msg>;
 using Spans = PVec<std::pair<uint64_t, uint64_t>>;  // (offset, length) of the messages of one transfer
@@ -1793,27 +1799,56 @@ class Engine {
     }
 
     // GPU endpoint receives everything queued on the H2D lane: one batched open.
+    // Where the GPU endpoint puts an H2D message (engine.py:251-267).
+    View h2d_destination(const Msg &m, const Meta &meta) {
+        if (m.nop) return plane.dry ? View{} : plane.arena_scratch(m.len);
+        if (meta.block_id != NONE) {
+            Block &b = mem.block(meta.block_id);
+            uint64_t inner = meta.base - b.base + meta.offset;
+            View whole = device_buffer(meta.block_id);
+            return View{whole.buf, whole.off + inner, meta.nbytes};
+        }
+        return plane.dry ? View{} : plane.arena_scratch(meta.nbytes);
+    }
+    // The receiver's counter for an H2D message is its send counter (the
+    // lane is FIFO and lossless), so the device can open it as soon as it is
+    // on the wire instead of at the next drain: opens overlap the rest of the
+    // batch's copies rather than piling up at the sync.  The channel state
+    // (recv counter, deliveries) still advances at the reference's drain
+    // points.  SPPIPE_EAGER_OPEN=0 opens at the drain.
+    static bool eager_open() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_EAGER_OPEN");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+    void open_on_send(const MsgP &m, uint64_t iv, const Meta &meta) {
+        if (plane.dry || !eager_open()) return;
+        View dst = h2d_destination(*m, meta);
+        PVec<std::tuple<MsgP, uint64_t, View>> job;
+        job.emplace_back(m, iv, dst);
+        plane.open_into(job, H2D);
+        m->opened = true;
+        m->open_iv = iv;
+        m->open_dst = std::make_shared<View>(dst);
+    }
     void drain_gpu() {
         PVec<std::tuple<MsgP, uint64_t, View>> jobs;
         while (pending(H2D)) {
             auto mi = take(H2D);
             Meta meta = h2d_meta.front();
             h2d_meta.pop_front();
-            if (mi.first->nop) {
-                jobs.emplace_back(mi.first, mi.second, View{});
-                continue;
-            }
             View dst;
-            if (meta.block_id != NONE) {
-                Block &b = mem.block(meta.block_id);
-                uint64_t inner = meta.base - b.base + meta.offset;
-                View whole = device_buffer(meta.block_id);
-                dst = View{whole.buf, whole.off + inner, meta.nbytes};
-            } else if (!plane.dry) {
-                dst = plane.arena_scratch(meta.nbytes);
+            if (mi.first->opened) {
+                if (mi.first->open_iv != mi.second) throw EngineErr("H2D receive counter diverged from the send counter");
+                dst = *mi.first->open_dst;
+            } else {
+                dst = h2d_destination(*mi.first, meta);
+                jobs.emplace_back(mi.first, mi.second, dst);
             }
-            jobs.emplace_back(mi.first, mi.second, dst);
-            if (cfg.record_stream) delivered.push_back({meta.seq, meta.base + meta.offset, meta.nbytes, dst});
+            if (!mi.first->nop && cfg.record_stream)
+                delivered.push_back({meta.seq, meta.base + meta.offset, meta.nbytes, dst});
         }
         plane.open_into(jobs, H2D);
         if (cfg.strict_auth) plane.check_auth();
@@ -1835,6 +1870,7 @@ class Engine {
         }
         send(H2D, m);
         h2d_meta.push_back(meta);
+        open_on_send(m, iv, meta);
         ring_occupied--;
         counters[C_DATA_MSGS]++;
         act(SP_ACT_H2D_DATA, (int64_t)iv, m->len, record == NONE ? -1 : record, -1, record != NONE, record == NONE, 0,
@@ -2149,6 +2185,7 @@ class Engine {
             uint64_t iv = send_iv[H2D];
             send(H2D, m);
             h2d_meta.push_back(Meta{2, 0, NONE, 0, 0, cfg.nop_bytes});
+            open_on_send(m, iv, h2d_meta.back());
             counters[C_NOPS]++;
             act(SP_ACT_NOP, (int64_t)iv, cfg.nop_bytes);
         }
@@ -2625,6 +2662,13 @@ int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_
         k_xor_byte<<<1, 1, 0, st>>>(m->buf->ptr + m->off + byte_index, mask);
         ck(cudaGetLastError(), "k_xor_byte");
         ck(cudaStreamSynchronize(st), "test corrupt");
+        if (m->opened) {
+            // opened on send already: the receiver sees the flipped bytes now
+            PVec<std::tuple<MsgP, uint64_t, View>> job;
+            job.emplace_back(m, m->open_iv, *m->open_dst);
+            e.plane.open_into(job, dir & 1);
+            e.plane.flush();
+        }
     });
 }
 int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done) {
