@@ -387,3 +387,24 @@ def test_native_vs_python_random_traces_gpu():
         assert _schedule(runs[0].engine) == _schedule(runs[1].engine), seed
         assert runs[0].engine.delivered == runs[1].engine.delivered, seed
         assert runs[0].engine.d2h_stream == runs[1].engine.d2h_stream, seed
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("switch", ["SPPIPE_EAGER_OPEN=0", "SPPIPE_SLAB=0", "SPPIPE_OUT_STREAM=1",
+                                    "SPPIPE_BATCH_COPY=0"])
+def test_native_parity_under_data_plane_switches_gpu(switch):
+    """The data-plane switches (drain-time opens, pool-only buffers, own-stream
+    swap-out seals, per-copy calls) change scheduling only: the golden parity
+    test passes under each (read once per process, so in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    k, v = switch.split("=")
+    env = dict(os.environ, **{k: v})
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{here}/test_native_engine.py::test_native_engine_parity_gpu",
+                        f"{here}/test_native_engine.py::test_native_tamper_detected_gpu"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -1,0 +1,64 @@
+// Device time per k_gcm launch for small batches (NOP pads, tokens, KV
+// blocks), back to back on one stream and with a cross-stream event wait
+// between launches (the engine's small-batch pattern), via libspgcm's C-ABI.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I include tools/native/launch_latency.cu \
+//        -L paper_2411_03357_b200/lib -lspgcm -Xlinker -rpath,$PWD/paper_2411_03357_b200/lib -o /tmp/ll
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <vector>
+
+#include "spgcm.h"
+
+int main() {
+    uint8_t key[32];
+    for (int i = 0; i < 32; ++i) key[i] = (uint8_t)i;
+    sp_ctx *ctx = nullptr;
+    if (sp_ctx_create(key, &ctx) != SP_OK) return 1;
+    cudaStream_t s, s2;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+    uint8_t *buf, *tags;
+    cudaMalloc(&buf, 64 << 20);
+    cudaMalloc(&tags, 16 * 1024);
+    cudaMemset(buf, 0, 64 << 20);
+    cudaEvent_t a, b, x;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    struct Case {
+        const char *name;
+        int n;
+        size_t size;
+    } cases[] = {{"1 NOP (1 B)", 1, 1},       {"8 NOPs", 8, 1},           {"1 x 2 KiB token", 1, 2048},
+                 {"1 x 224 KiB KV", 1, 229376}, {"4 x 224 KiB KV", 4, 229376}, {"32 x 224 KiB KV", 32, 229376},
+                 {"1 x 1 MiB", 1, 1 << 20}};
+    for (auto &c : cases) {
+        std::vector<sp_desc> d(c.n);
+        for (int i = 0; i < c.n; ++i) {
+            d[i] = sp_desc{SP_DIR_H2D, 0u, (uint64_t)i, c.size, buf + i * c.size, buf + i * c.size, tags + 16 * i, nullptr};
+        }
+        for (int mode = 0; mode < 2; ++mode) {
+            const int reps = 2000;
+            for (int w = 0; w < 50; ++w) sp_seal_batch(ctx, d.data(), c.n, s);
+            cudaStreamSynchronize(s);
+            cudaEventRecord(a, s);
+            for (int r = 0; r < reps; ++r) {
+                if (mode == 1) {  // event hop through a second stream before every launch
+                    cudaEventRecord(x, s);
+                    cudaStreamWaitEvent(s2, x, 0);
+                    cudaEventRecord(x, s2);
+                    cudaStreamWaitEvent(s, x, 0);
+                }
+                sp_seal_batch(ctx, d.data(), c.n, s);
+            }
+            cudaEventRecord(b, s);
+            cudaEventSynchronize(b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            printf("%-18s %-16s %7.2f us/launch\n", c.name, mode ? "event-hop" : "back-to-back", ms * 1e3 / reps);
+        }
+    }
+    printf("launches %llu\n", (unsigned long long)sp_launch_count());
+    return 0;
+}
