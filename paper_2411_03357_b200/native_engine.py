@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import os
 import random
 import weakref
 from dataclasses import dataclass
@@ -271,7 +272,8 @@ class NativeEngine:
         cfg.dry = c.plane == "dry"
         cfg.hw_guards = bool(getattr(memory, "hw_guards", False))
         cfg.initial_h2d_iv, cfg.initial_d2h_iv = cpu.send_iv, gpu.send_iv
-        cfg.batch_bytes = 64 << 20
+        # queued compute bytes that trigger a flush (SPPIPE_BATCH_MB overrides, for sweeps)
+        cfg.batch_bytes = int(float(os.environ.get("SPPIPE_BATCH_MB", "64")) * (1 << 20))
         cfg.reserve_bytes = reserve_bytes
         h = ctypes.c_void_p()
         _check(self._lib.sp_pipe_create(ctypes.byref(cfg), bytes(cpu.key.key_bytes), predictor._h, ctypes.byref(h)))
