@@ -717,7 +717,7 @@ int run_batch(sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, int mode) {
 // Pieces of ~kPieceBytes (whole rows) flow H2D (stream a) -> kernel (stream b)
 // -> D2H (stream c); each stage waits on the previous stage's event.
 // Piece schedule of the host pipeline: pieces double from kPieceMinRows up to
-// max_piece_rows() and halve again over the tail, so the H2D of the first
+// max_piece_rows() (the first one twice) and halve again over the tail, so the H2D of the first
 // piece and the D2H of the last one (the only un-overlapped transfers) are
 // small while the steady state runs on large copies.
 constexpr uint64_t kPieceMinRows = (1ull << 20) / 512u;  // 1 MiB
@@ -736,6 +736,14 @@ std::vector<uint64_t> piece_schedule(uint64_t rows) {
     std::vector<uint64_t> out;
     const uint64_t cap = max_piece_rows();
     uint64_t done = 0, cur = std::min(kPieceMinRows, cap);
+    // ramp 1, 1, 2, 4, ... cap/2 MiB sums to cap: the steady-state pieces then
+    // start on multiples of cap, i.e. on 32 MiB message boundaries, so each
+    // moves as ONE copy per direction instead of a 1 MiB + 31 MiB pair (a
+    // 1 MiB copy runs at ~20 GB/s and opened a ~40 us gap per piece)
+    if (cap >= 2 * cur && rows > 2 * cur) {
+        out.push_back(cur);
+        done = cur;
+    }
     while (done < rows) {
         const uint64_t left = rows - done;
         uint64_t take = std::min(cur, left);
@@ -754,6 +762,7 @@ struct HostPipe {
     cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
     uint8_t *d_in = nullptr, *d_out = nullptr, *d_tags = nullptr;
     int32_t *d_status = nullptr;
+    uint8_t *h_tags = nullptr;  // pinned staging: all tags of a batch cross PCIe in one copy
     size_t cap_bytes = 0, cap_msgs = 0;
     std::vector<cudaEvent_t> ev_in, ev_k;
     std::mutex mu;
@@ -784,9 +793,11 @@ int ensure_pipe(HostPipe *hp, int device, size_t bytes, size_t nmsgs, size_t npi
         hp->cap_bytes = cap;
     }
     if (hp->cap_msgs < nmsgs) {
-        if (hp->d_tags) { cudaFree(hp->d_tags); cudaFree(hp->d_status); }
+        if (hp->d_tags) { cudaFree(hp->d_tags); cudaFree(hp->d_status); cudaFreeHost(hp->h_tags); }
         size_t cap = std::max<size_t>(nmsgs, 64);
         SP_CUDA(cudaMalloc(&hp->d_tags, cap * 16), "cudaMalloc(pipe tags)");
+        SP_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&hp->h_tags), cap * 16, cudaHostAllocDefault),
+                "cudaHostAlloc(pipe tags)");
         SP_CUDA(cudaMalloc(&hp->d_status, cap * sizeof(int32_t)), "cudaMalloc(pipe status)");
         hp->cap_msgs = cap;
     }
@@ -843,9 +854,10 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
         dd[(size_t)i].status = hp->d_status + i;
     }
     if (open) {
-        for (int i = 0; i < n; ++i)
-            SP_CUDA(cudaMemcpyAsync(hp->d_tags + 16u * (size_t)i, d[i].tag, 16, cudaMemcpyHostToDevice, hp->s_in),
-                    "cudaMemcpyAsync(tag)");
+        // the previous call's tag D2H out of h_tags finished at its stream sync
+        for (int i = 0; i < n; ++i) memcpy(hp->h_tags + 16u * (size_t)i, d[i].tag, 16);
+        SP_CUDA(cudaMemcpyAsync(hp->d_tags, hp->h_tags, 16u * (size_t)n, cudaMemcpyHostToDevice, hp->s_in),
+                "cudaMemcpyAsync(tags)");
     }
     Workspace *ws = workspace_for(ctx->device, hp->s_k);
     std::lock_guard<std::mutex> wlk(ws->mu);
@@ -861,6 +873,7 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
     const std::vector<MsgDev> &msgs = ws->h_msgs;
     while (g < rows) {
         const uint64_t g_end = std::min(rows, g + sched[k]);
+        const cudaStream_t s_in = hp->s_in;
         // H2D for every message slice in [g, g_end)
         int mj = mi;
         uint64_t gg = g;
@@ -871,12 +884,12 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
             rows_to_bytes(m.len, m.rows, t0, t1, lo, hi);
             if (hi > lo)
                 SP_CUDA(cudaMemcpyAsync(hp->d_in + off[(size_t)mj] + lo, static_cast<const uint8_t *>(d[mj].src) + lo,
-                                        hi - lo, cudaMemcpyHostToDevice, hp->s_in),
+                                        hi - lo, cudaMemcpyHostToDevice, s_in),
                         "cudaMemcpyAsync(H2D)");
             gg = m.row_begin + t1;
             if (t1 == m.rows) ++mj;
         }
-        SP_CUDA(cudaEventRecord(hp->ev_in[k], hp->s_in), "event record");
+        SP_CUDA(cudaEventRecord(hp->ev_in[k], s_in), "event record");
         SP_CUDA(cudaStreamWaitEvent(hp->s_k, hp->ev_in[k], 0), "wait");
         rc = launch_rows(ctx, p, g, g_end, hp->s_k);
         if (rc) return rc;
@@ -899,11 +912,9 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
         g = g_end;
         ++k;
     }
-    if (!open) {
-        for (int i = 0; i < n; ++i)
-            SP_CUDA(cudaMemcpyAsync(d[i].tag, hp->d_tags + 16u * (size_t)i, 16, cudaMemcpyDeviceToHost, hp->s_out),
-                    "cudaMemcpyAsync(tag D2H)");
-    }
+    if (!open)
+        SP_CUDA(cudaMemcpyAsync(hp->h_tags, hp->d_tags, 16u * (size_t)n, cudaMemcpyDeviceToHost, hp->s_out),
+                "cudaMemcpyAsync(tags D2H)");
     std::vector<int32_t> st;
     if (open) {
         st.resize((size_t)n);
@@ -912,6 +923,8 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
                 "cudaMemcpyAsync(status)");
     }
     SP_CUDA(cudaStreamSynchronize(hp->s_out), "cudaStreamSynchronize");
+    if (!open)
+        for (int i = 0; i < n; ++i) memcpy(d[i].tag, hp->h_tags + 16u * (size_t)i, 16);
     if (open) {
         int bad = 0;
         for (int i = 0; i < n; ++i) {

@@ -38,5 +38,5 @@ t0 = time.perf_counter()
 for _ in range(K):
     h_back.copy_(d2, non_blocking=True); torch.cuda.synchronize()
 d2h_ms = (time.perf_counter() - t0) * 1e3 / K
-print(f"piece={os.environ.get('SPGCM_PIECE_MIB','8')}MiB seal {seal_ms:.2f} ms ({total/seal_ms/1e6:.1f} GB/s) open {open_ms:.2f} ms "
+print(f"piece={os.environ.get('SPGCM_PIECE_MIB','32')}MiB seal {seal_ms:.2f} ms ({total/seal_ms/1e6:.1f} GB/s) open {open_ms:.2f} ms "
       f"({total/open_ms/1e6:.1f} GB/s) | plain duplex {dup_ms:.2f} ms, H2D only {h2d_ms:.2f} ({total/h2d_ms/1e6:.1f} GB/s), D2H only {d2h_ms:.2f} ({total/d2h_ms/1e6:.1f} GB/s)")
