@@ -32,6 +32,10 @@ import sys
 import tempfile
 import time
 
+# numpy's OpenBLAS pool busy-waits on idle cores after any BLAS call; nothing
+# here uses BLAS, so keep it from competing with the issuing thread
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -83,7 +83,7 @@ inline uint64_t round16(uint64_t n) { return (n + 15u) & ~uint64_t(15); }
 // ---- events and device buffers ------------------------------------------------
 class Plane;
 
-struct Fence {
+struct Fence : RcBase {
     cudaEvent_t ev = nullptr;
     cudaStream_t stream = nullptr;
     bool recorded = false;
@@ -93,12 +93,12 @@ struct Fence {
     Plane *plane = nullptr;
     ~Fence();
 };
-using FenceP = std::shared_ptr<Fence>;
+using FenceP = Rc<Fence>;
 
 struct Slab;
-struct Buf {
+struct Buf : RcBase {
     Plane *plane = nullptr;
-    std::shared_ptr<Slab> slab;  // sub-allocation of a slab (small buffers), else null
+    Rc<Slab> slab;  // sub-allocation of a slab (small buffers), else null
     uint8_t *ptr = nullptr;
     uint64_t size = 0;
     uint64_t alloc_size = 0;
@@ -122,7 +122,7 @@ struct Buf {
     }
     ~Buf();
 };
-using BufP = std::shared_ptr<Buf>;
+using BufP = Rc<Buf>;
 
 // Small buffers (<= 1 MiB: staging of small chunks, KV blocks, arenas) are
 // bump-allocated from 32 MiB slabs, one open slab per (stream, lane): a
@@ -131,14 +131,19 @@ using BufP = std::shared_ptr<Buf>;
 // slab; the slab retires (buffer cache, same reuse rules) when the last of
 // its sub-buffers is gone.  Ranges inside a slab are never reused while it
 // lives, so sub-buffers need no ordering among themselves.
-struct Slab {
+struct Slab : RcBase {
     BufP big;
     uint64_t off = 0;
 };
 
+struct View {
+    BufP buf;
+    uint64_t off = 0, len = 0;
+    uint8_t *ptr() const { return buf->ptr + off; }
+};
+
 // A sealed message on the wire (channel.CiphertextMsg / DeviceCiphertext).
-struct View;
-struct Msg {
+struct Msg : RcBase {
     BufP buf;  // payload at off, tag at tag_off (null in the dry plane)
     uint64_t off = 0, tag_off = 0, len = 0;
     bool nop = false;
@@ -147,16 +152,10 @@ struct Msg {
     // the IV and destination of that open
     bool opened = false;
     uint64_t open_iv = 0;
-    std::shared_ptr<View> open_dst;
+    View open_dst;
 };
-using MsgP = std::shared_ptr<Msg>;
+using MsgP = Rc<Msg>;
 using Spans = PVec<std::pair<uint64_t, uint64_t>>;  // (offset, length) of the messages of one transfer
-
-struct View {
-    BufP buf;
-    uint64_t off = 0, len = 0;
-    uint8_t *ptr() const { return buf->ptr + off; }
-};
 
 // ---- host memory model (memory.py) ---------------------------------------------
 struct Block {
@@ -707,7 +706,7 @@ class Plane {
         }();
         return on;
     }
-    std::map<std::pair<cudaStream_t, int>, std::shared_ptr<Slab>> slabs;  // open slab per (stream, lane)
+    std::map<std::pair<cudaStream_t, int>, Rc<Slab>> slabs;  // open slab per (stream, lane)
     // lane separates lifetimes: 0 = transient staging, 1 = device copies of blocks
     BufP alloc(uint64_t n, cudaStream_t st, int lane = 0) {
         if (!dry && n <= kSlabMax && slabs_enabled()) {
@@ -1831,7 +1830,7 @@ class Engine {
         plane.open_into(job, H2D);
         m->opened = true;
         m->open_iv = iv;
-        m->open_dst = std::make_shared<View>(dst);
+        m->open_dst = dst;
     }
     void drain_gpu() {
         PVec<std::tuple<MsgP, uint64_t, View>> jobs;
@@ -1842,7 +1841,7 @@ class Engine {
             View dst;
             if (mi.first->opened) {
                 if (mi.first->open_iv != mi.second) throw EngineErr("H2D receive counter diverged from the send counter");
-                dst = *mi.first->open_dst;
+                dst = mi.first->open_dst;
             } else {
                 dst = h2d_destination(*mi.first, meta);
                 jobs.emplace_back(mi.first, mi.second, dst);
@@ -2665,7 +2664,7 @@ int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_
         if (m->opened) {
             // opened on send already: the receiver sees the flipped bytes now
             PVec<std::tuple<MsgP, uint64_t, View>> job;
-            job.emplace_back(m, m->open_iv, *m->open_dst);
+            job.emplace_back(m, m->open_iv, m->open_dst);
             e.plane.open_into(job, dir & 1);
             e.plane.flush();
         }

@@ -99,9 +99,74 @@ using PUMap = std::unordered_map<K, V, H, std::equal_to<K>, PoolAlloc<std::pair<
 template <class K, class H = std::hash<K>>
 using PUSet = std::unordered_set<K, H, std::equal_to<K>, PoolAlloc<K>>;
 
+// Intrusive, non-atomic reference counting for the data plane's handles
+// (buffers, fences, messages, slabs).  std::shared_ptr counts atomically in
+// any process with threads (every Python process): at ~20 handle copies per
+// trace event the locked increments were ~10% of the host time.  A pipe has
+// one owner thread at a time, so plain counters suffice.
+struct RcBase {
+    uint32_t rc_ = 0;
+};
+
+template <class T>
+class Rc {
+  public:
+    Rc() noexcept = default;
+    Rc(std::nullptr_t) noexcept {}
+    explicit Rc(T *p) noexcept : p_(p) {
+        if (p_) ++p_->rc_;
+    }
+    Rc(const Rc &o) noexcept : p_(o.p_) {
+        if (p_) ++p_->rc_;
+    }
+    Rc(Rc &&o) noexcept : p_(o.p_) { o.p_ = nullptr; }
+    ~Rc() { drop(p_); }
+    Rc &operator=(const Rc &o) noexcept {
+        if (o.p_) ++o.p_->rc_;
+        T *old = p_;
+        p_ = o.p_;
+        drop(old);
+        return *this;
+    }
+    Rc &operator=(Rc &&o) noexcept {
+        if (this != &o) {
+            T *old = p_;
+            p_ = o.p_;
+            o.p_ = nullptr;
+            drop(old);
+        }
+        return *this;
+    }
+    Rc &operator=(std::nullptr_t) noexcept {
+        reset();
+        return *this;
+    }
+    void reset() noexcept {
+        T *old = p_;
+        p_ = nullptr;
+        drop(old);
+    }
+    T *get() const noexcept { return p_; }
+    T *operator->() const noexcept { return p_; }
+    T &operator*() const noexcept { return *p_; }
+    explicit operator bool() const noexcept { return p_ != nullptr; }
+    bool operator==(const Rc &o) const noexcept { return p_ == o.p_; }
+    bool operator!=(const Rc &o) const noexcept { return p_ != o.p_; }
+
+  private:
+    static void drop(T *p) noexcept {
+        if (p && --p->rc_ == 0) {
+            p->~T();
+            free_lists().put(p, sizeof(T));
+        }
+    }
+    T *p_ = nullptr;
+};
+
 template <class T, class... A>
-std::shared_ptr<T> pmake(A &&...a) {
-    return std::allocate_shared<T>(PoolAlloc<T>(), std::forward<A>(a)...);
+Rc<T> pmake(A &&...a) {
+    void *m = free_lists().get(sizeof(T));
+    return Rc<T>(new (m) T(std::forward<A>(a)...));
 }
 
 }  // namespace sppipe
