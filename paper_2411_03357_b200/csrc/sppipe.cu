@@ -21,15 +21,20 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -90,6 +95,7 @@ struct Fence : RcBase {
     bool complete = false;  // observed complete once (never re-recorded after that)
     uint64_t seq = 0;       // record order: on one stream a higher seq completes later
     uint64_t mark = 0;      // de-duplicates waits within one issue pass
+    uint64_t post_seq = 0;  // Issuer position of its cudaEventRecord (0: issued inline)
     Plane *plane = nullptr;
     ~Fence();
 };
@@ -502,9 +508,130 @@ struct Landing {
     int dir;
 };
 
+// Stream-ordered CUDA calls of a plane (copies, launches, event records and
+// waits, stream-ordered frees) are issued by one worker thread, in the order
+// the control plane posts them: the control plane (channel, validator,
+// predictor, staging decisions) overlaps the driver's per-call cost, which
+// dominates at small messages (64 KiB blocks: ~1.5 us of driver time per
+// event).  Posted closures capture only raw handles and pointers, never the
+// plane's reference-counted objects.  Anything that reads device state
+// (event queries of not-yet-issued records, stream/event syncs, status reads)
+// drains the queue first.  SPPIPE_ASYNC_ISSUE=0: every call inline.
+class Issuer {
+  public:
+    static bool enabled_by_env() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_ASYNC_ISSUE");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+    void start(int device) {
+        dev_ = device;
+        th_ = std::thread([this] { run(); });
+        on_ = true;
+    }
+    ~Issuer() { stop(); }
+    void stop() {
+        if (!on_) return;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            quit_ = true;
+            quit_flag_.store(true, std::memory_order_release);
+        }
+        cv_.notify_one();
+        th_.join();
+        on_ = false;
+    }
+    bool on() const { return on_; }
+    // Run `fn` now (inline mode) or queue it; returns its sequence number.
+    uint64_t post(std::function<void()> fn) {
+        if (!on_) {
+            fn();
+            return 0;
+        }
+        if (failed_.load(std::memory_order_acquire)) rethrow();
+        uint64_t seq;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(fn));
+            seq = ++posted_;
+            posted_seen_.store(seq, std::memory_order_release);
+        }
+        if (sleeping_.load(std::memory_order_acquire)) cv_.notify_one();
+        return seq;
+    }
+    bool done(uint64_t seq) const { return seq <= done_.load(std::memory_order_acquire); }
+    void drain() {
+        if (!on_) return;
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_done_.wait(lk, [&] { return done_.load(std::memory_order_acquire) == posted_; });
+        lk.unlock();
+        if (failed_.load(std::memory_order_acquire)) rethrow();
+    }
+
+  private:
+    void rethrow() {
+        std::lock_guard<std::mutex> lk(mu_);
+        std::string e = err_;
+        err_.clear();
+        failed_.store(false, std::memory_order_release);
+        throw CudaErr(e);
+    }
+    void run() {
+        cudaSetDevice(dev_);
+        std::vector<std::function<void()>> batch;
+        for (;;) {
+            // spin ~50 us for the next post before sleeping: a flush posts a
+            // burst of calls, and a futex wake-up would add its latency to
+            // every burst's first call
+            const auto t_spin = std::chrono::steady_clock::now();
+            while (posted_seen_.load(std::memory_order_acquire) == done_.load(std::memory_order_acquire) &&
+                   std::chrono::steady_clock::now() - t_spin < std::chrono::microseconds(50) &&
+                   !quit_flag_.load(std::memory_order_acquire)) {
+            }
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                sleeping_.store(true, std::memory_order_release);
+                cv_.wait(lk, [&] { return quit_ || !q_.empty(); });
+                sleeping_.store(false, std::memory_order_release);
+                if (q_.empty() && quit_) return;
+                batch.assign(std::make_move_iterator(q_.begin()), std::make_move_iterator(q_.end()));
+                q_.clear();
+            }
+            for (auto &fn : batch) {
+                try {
+                    fn();
+                } catch (const std::exception &e) {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    if (err_.empty()) err_ = e.what();
+                    failed_.store(true, std::memory_order_release);
+                }
+                {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    done_.fetch_add(1, std::memory_order_acq_rel);
+                }
+                cv_done_.notify_all();
+            }
+            batch.clear();
+        }
+    }
+    int dev_ = 0;
+    bool on_ = false, quit_ = false;
+    std::thread th_;
+    std::mutex mu_;
+    std::condition_variable cv_, cv_done_;
+    std::deque<std::function<void()>> q_;
+    uint64_t posted_ = 0;
+    std::atomic<uint64_t> done_{0}, posted_seen_{0};
+    std::atomic<bool> failed_{false}, sleeping_{false}, quit_flag_{false};
+    std::string err_;
+};
+
 class Plane {
   public:
     bool dry;
+    Issuer iss;
     int dev = 0;
     Streams s{};
     cudaMemPool_t pool = nullptr;
@@ -604,6 +731,7 @@ class Plane {
         ck(cudaMemset(zero_dev, 0, kZeroBytes), "cudaMemset(zero page)");
         ck(cudaMemset(status, 0, status_cap * sizeof(int32_t)), "cudaMemset(status)");
         window = new_fence();
+        if (Issuer::enabled_by_env()) iss.start(dev);
     }
     ~Plane() {
         if (dry) return;
@@ -613,6 +741,12 @@ class Plane {
         } catch (...) {
             idle = false;
         }
+        try {
+            iss.drain();
+        } catch (...) {
+            idle = false;
+        }
+        iss.stop();  // everything below runs inline
         ops.clear();
         landings.clear();
         host_ready.clear();
@@ -662,7 +796,8 @@ class Plane {
     }
     uint64_t record_seq = 0;
     void record(const FenceP &f, cudaStream_t st) {
-        ck(cudaEventRecord(f->ev, st), "cudaEventRecord");
+        const cudaEvent_t ev = f->ev;
+        f->post_seq = iss.post([ev, st] { ck(cudaEventRecord(ev, st), "cudaEventRecord"); });
         f->stream = st;
         f->recorded = true;
         f->seq = ++record_seq;
@@ -676,7 +811,8 @@ class Plane {
         if (!f) return;
         if (!f->recorded) throw std::logic_error("wait on an unrecorded fence");
         if (f->stream == st) return;  // stream order covers it
-        ck(cudaStreamWaitEvent(st, f->ev, 0), "cudaStreamWaitEvent");
+        const cudaEvent_t ev = f->ev;
+        iss.post([st, ev] { ck(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent"); });
     }
     // Size classes of the plane's buffer cache: 4 KiB steps up to 1 MiB,
     // then 1 MiB steps (staging sizes repeat: chunks, KV blocks, arenas).
@@ -684,8 +820,8 @@ class Plane {
         n = std::max<uint64_t>(n, 16);
         return n <= (1u << 20) ? (n + 4095u) & ~uint64_t(4095) : (n + (1u << 20) - 1) & ~uint64_t((1u << 20) - 1);
     }
-    static bool passed(Fence &f) {
-        if (!f.complete && cudaEventQuery(f.ev) == cudaSuccess) f.complete = true;
+    bool passed(Fence &f) {
+        if (!f.complete && iss.done(f.post_seq) && cudaEventQuery(f.ev) == cudaSuccess) f.complete = true;
         return f.complete;
     }
     // A retired buffer is reusable on stream st without any wait when every
@@ -752,11 +888,13 @@ class Plane {
                 // unbounded lead turns into slow pool growth and HBM use).
                 if (!b->ptr && pool_bytes + cls > pool_budget()) trim_cache();
                 if (!b->ptr && !v.empty() && pool_bytes + cls > pool_budget()) {
+                    iss.drain();
                     for (auto &u : v.front().uses) {
                         if (u.second && u.second->recorded) {
                             ck(cudaEventSynchronize(u.second->ev), "pool backpressure");
                         } else if (u.first != st) {
                             FenceP f = record_new(u.first);
+                            iss.drain();
                             ck(cudaEventSynchronize(f->ev), "pool backpressure");
                         }
                     }
@@ -802,7 +940,9 @@ class Plane {
                         break;
                     }
                 if (idle) {
-                    ck(cudaFreeAsync(v[k].ptr, s.comp), "cudaFreeAsync(trim)");
+                    void *ptr = v[k].ptr;
+                    const cudaStream_t st = s.comp;
+                    iss.post([ptr, st] { ck(cudaFreeAsync(ptr, st), "cudaFreeAsync(trim)"); });
                     pool_bytes -= std::min(pool_bytes, kv.first);
                     cached_bytes -= kv.first;
                 } else {
@@ -834,15 +974,12 @@ class Plane {
             cudaStream_t fs = x.last;
             for (auto &u : x.uses) {
                 if (u.first == fs) continue;
-                if (u.second && u.second->recorded) {
-                    ck(cudaStreamWaitEvent(fs, u.second->ev, 0), "cudaStreamWaitEvent(free)");
-                } else {
-                    FenceP f = record_new(u.first);
-                    ck(cudaStreamWaitEvent(fs, f->ev, 0), "cudaStreamWaitEvent(free)");
-                }
+                const cudaEvent_t ev = (u.second && u.second->recorded) ? u.second->ev : record_new(u.first)->ev;
+                iss.post([fs, ev] { ck(cudaStreamWaitEvent(fs, ev, 0), "cudaStreamWaitEvent(free)"); });
             }
             x.uses.clear();
-            ck(cudaFreeAsync(x.ptr, fs), "cudaFreeAsync");
+            void *ptr = x.ptr;
+            iss.post([ptr, fs] { ck(cudaFreeAsync(ptr, fs), "cudaFreeAsync"); });
             pool_bytes -= std::min(pool_bytes, x.size);
         }
         collecting = false;
@@ -857,6 +994,7 @@ class Plane {
         if (dry) return;
         flush();
         if (!status_used) return;
+        iss.drain();
         ck(cudaStreamSynchronize(s.comp), "sync comp");
         ck(cudaStreamSynchronize(s.land), "sync land");
         ck(cudaStreamSynchronize(s.d2h), "sync d2h");
@@ -976,7 +1114,7 @@ class Plane {
                     descs.push_back(op.d);
                 }
                 if (descs.empty()) continue;
-                ck_sp(sp_crypt_batch(ctx, descs.data(), (int)descs.size(), s.comp), "sp_crypt_batch");
+                post_batch(0, descs, s.comp, "sp_crypt_batch");
                 ++launches;
             }
             record(window, s.comp);
@@ -1030,6 +1168,7 @@ class Plane {
             auto &b = ring.busy.front();
             const bool overlap = std::get<0>(b) < hi && lo < std::get<1>(b);
             if (overlap) {
+                iss.drain();
                 ck(cudaEventSynchronize(std::get<2>(b)->ev), "ring slot wait");
             } else if (!passed(*std::get<2>(b))) {
                 break;
@@ -1082,7 +1221,7 @@ class Plane {
                 places.push_back({l.block, off, std::get<2>(j), m->len});
                 off += m->len;
             }
-        ck_sp(sp_open_batch(ctx, descs.data(), (int)descs.size(), s.land), "sp_open_batch(landing)");
+        post_batch(2, descs, s.land, "sp_open_batch(landing)");
         ++launches;
         FenceP opened = record_new(s.land);
         ++tick;
@@ -1145,21 +1284,31 @@ class Plane {
     // instead of a call per copy; plain cudaMemcpyAsync where unsupported.
     template <class F>
     void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
+        if (!count) return;
+        std::vector<void *> dsts(count), srcs(count);
+        std::vector<size_t> sizes(count);
+        for (size_t i = 0; i < count; ++i) get(i, dsts[i], srcs[i], sizes[i]);
+        const int device = dev;
+        iss.post([st, h2d, device, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes)]() mutable {
+            issue_copies(st, h2d, device, dsts, srcs, sizes);
+        });
+    }
+    // Runs on the issuing thread (or inline).
+    static void issue_copies(cudaStream_t st, bool h2d, int device, std::vector<void *> &dsts, std::vector<void *> &srcs,
+                             std::vector<size_t> &sizes) {
         static bool batch_ok = [] {  // SPPIPE_BATCH_COPY=0: per-copy calls (profilers show each copy)
             const char *e = getenv("SPPIPE_BATCH_COPY");
             return !(e && e[0] == '0');
         }();
+        const size_t count = sizes.size();
         if (count > 1 && batch_ok) {
-            std::vector<void *> dsts(count), srcs(count);
-            std::vector<size_t> sizes(count);
-            for (size_t i = 0; i < count; ++i) get(i, dsts[i], srcs[i], sizes[i]);
             cudaMemcpyAttributes attr;
             memset(&attr, 0, sizeof attr);
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             attr.srcLocHint.type = h2d ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
-            attr.srcLocHint.id = h2d ? 0 : dev;
+            attr.srcLocHint.id = h2d ? 0 : device;
             attr.dstLocHint.type = h2d ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-            attr.dstLocHint.id = h2d ? dev : 0;
+            attr.dstLocHint.id = h2d ? device : 0;
             size_t idx = 0, fail_idx = SIZE_MAX;
             cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), count, &attr, &idx, 1,
                                                  &fail_idx, st);
@@ -1169,12 +1318,20 @@ class Plane {
             cudaGetLastError();
             batch_ok = false;  // driver without batch copies: per-copy path from now on
         }
-        for (size_t i = 0; i < count; ++i) {
-            void *dst, *src;
-            size_t n;
-            get(i, dst, src, n);
-            ck(cudaMemcpyAsync(dst, src, n, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st), "batched copy");
-        }
+        for (size_t i = 0; i < count; ++i)
+            ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+               "batched copy");
+    }
+    // One seal / open / mixed launch of libspgcm, issued in order.
+    // kind: 0 sp_crypt_batch (per-message op), 1 sp_seal_batch, 2 sp_open_batch
+    void post_batch(int kind, const std::vector<sp_desc> &d, cudaStream_t st, const char *what) {
+        sp_ctx *c = ctx;
+        iss.post([c, kind, st, what, d = std::vector<sp_desc>(d)] {
+            const int n = (int)d.size();
+            const int rc = kind == 0 ? sp_crypt_batch(c, d.data(), n, st)
+                                     : (kind == 1 ? sp_seal_batch(c, d.data(), n, st) : sp_open_batch(c, d.data(), n, st));
+            ck_sp(rc, what);
+        });
     }
 
     void before_host_read_of(int64_t block_id) {
@@ -1296,7 +1453,7 @@ class Plane {
             if (p->dry || items.empty()) return;
             p->issue(copies);
             p->wait(p->s.spec, last_copy);
-            ck_sp(sp_seal_batch(p->ctx, items.data(), (int)items.size(), p->s.spec), "sp_seal_batch(spec)");
+            p->post_batch(1, items, p->s.spec, "sp_seal_batch(spec)");
             ++p->launches;
             p->record(ready, p->s.spec);
             ++p->tick;
@@ -1394,7 +1551,7 @@ class Plane {
         std::unordered_set<Fence *> seen;
         for (auto &f : outb.waits)
             if (seen.insert(f.get()).second) wait(s.out, f);
-        ck_sp(sp_seal_batch(ctx, outb.items.data(), (int)outb.items.size(), s.out), "sp_seal_batch(swap-out)");
+        post_batch(1, outb.items, s.out, "sp_seal_batch(swap-out)");
         ++launches;
         record(outb.ready, s.out);
         ++tick;
@@ -1507,6 +1664,7 @@ class Plane {
     void host_sync(int64_t block_id) {
         if (dry) return;
         flush();
+        iss.drain();
         if (block_id == INT64_MIN) {
             ck(cudaStreamSynchronize(s.d2h), "sync d2h");
             return;
@@ -1542,15 +1700,22 @@ class Plane {
         uint8_t *h = ring_reserve(n);
         memcpy(h, data, n);
         FenceP f;
+        const cudaStream_t st = s.host;
         if (b.host_dev) {
             const unsigned blocks = (unsigned)std::min<uint64_t>(148, (n + 4095) / 4096);
-            k_bytes<<<blocks, 256, 0, s.host>>>(b.host_dev + offset, h, n);
-            ck(cudaGetLastError(), "k_bytes(app write)");
+            uint8_t *dst = b.host_dev + offset;
+            iss.post([blocks, st, dst, h, n] {
+                k_bytes<<<blocks, 256, 0, st>>>(dst, h, n);
+                ck(cudaGetLastError(), "k_bytes(app write)");
+            });
             f = record_new(s.host);
         } else {
             BufP tmp = alloc(n, s.host);
-            ck(cudaMemcpyAsync(tmp->ptr, h, n, cudaMemcpyHostToDevice, s.host), "app write H2D");
-            ck(cudaMemcpyAsync(b.host + offset, tmp->ptr, n, cudaMemcpyDeviceToHost, s.host), "app write D2H");
+            uint8_t *t = tmp->ptr, *dst = b.host + offset;
+            iss.post([st, t, dst, h, n] {
+                ck(cudaMemcpyAsync(t, h, n, cudaMemcpyHostToDevice, st), "app write H2D");
+                ck(cudaMemcpyAsync(dst, t, n, cudaMemcpyDeviceToHost, st), "app write D2H");
+            });
             f = record_new(s.host);
             tmp->use(s.host, f, ++tick);
         }
@@ -1559,6 +1724,7 @@ class Plane {
     }
     void finish_streams() {
         flush();
+        iss.drain();
         cudaStream_t all[7] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
@@ -1575,6 +1741,7 @@ class Plane {
             finish_streams();
         } else {
             flush();
+            iss.drain();
             cudaStream_t obs[5] = {s.comp, s.out, s.land, s.d2h, s.host};
             for (auto st : obs) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         }
@@ -1582,6 +1749,7 @@ class Plane {
     }
     void copy_to_host(const View &v, void *out) {
         flush();
+        iss.drain();
         ck(cudaStreamSynchronize(s.comp), "sync comp");
         ck(cudaStreamSynchronize(s.land), "sync land");
         ck(cudaMemcpy(out, v.ptr(), v.len, cudaMemcpyDeviceToHost), "copy to host");
@@ -2274,6 +2442,7 @@ class Engine {
             return;
         }
         View v = plane.new_device_buffer(n);
+        plane.iss.drain();
         ck(cudaMemcpyAsync(v.ptr(), src, n, src_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, plane.s.comp),
            "seed_device copy");
         ck(cudaStreamSynchronize(plane.s.comp), "seed_device sync");
@@ -2373,9 +2542,13 @@ class Engine {
                 View v{pl.alloc(e.len, st), 0, e.len};
                 uint8_t *h = pl.ring_reserve(e.len);
                 if (h2d && payloads) memcpy(h, payloads + e.payload, e.len);
-                ck(cudaMemcpyAsync(h2d ? (void *)v.ptr() : (void *)h, h2d ? (const void *)h : (const void *)v.ptr(),
-                                   e.len, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
-                   "plain token copy");
+                void *cd = h2d ? (void *)v.ptr() : (void *)h;
+                const void *cs = h2d ? (const void *)h : (const void *)v.ptr();
+                const uint64_t cn = e.len;
+                pl.iss.post([cd, cs, cn, h2d, st] {
+                    ck(cudaMemcpyAsync(cd, cs, cn, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
+                       "plain token copy");
+                });
                 FenceP f = pl.record_new(st);
                 pl.ring_commit(h, e.len, f);
                 v.buf->use(st, f, ++pl.tick);
@@ -2657,6 +2830,7 @@ int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_
         if (byte_index >= m->len) throw ValueErr("byte index outside the message");
         if (e.plane.dry || !m->buf) return;
         e.plane.flush();  // its seal is issued; the flip is ordered after it on its producer stream
+        e.plane.iss.drain();
         cudaStream_t st = m->ready && m->ready->recorded ? m->ready->stream : e.plane.s.comp;
         k_xor_byte<<<1, 1, 0, st>>>(m->buf->ptr + m->off + byte_index, mask);
         ck(cudaGetLastError(), "k_xor_byte");
