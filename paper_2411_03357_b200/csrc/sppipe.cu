@@ -182,9 +182,7 @@ class HostMem {
   public:
     // id -> block (ids are small and dense, memory.py:117-166); stable addresses
     std::vector<std::unique_ptr<Block>> blocks;
-    std::map<uint64_t, int64_t> by_base;        // base -> id
     PMap<int64_t, WriteGuard> write_guards;  // owner (record id) -> guard (insertion order == id order)
-    PMap<int64_t, std::pair<uint64_t, uint64_t>> read_guards;  // task id -> (base, len)
 
     Block &block(int64_t id) {
         if (id < 0 || id >= (int64_t)blocks.size() || !blocks[(size_t)id]) throw KeyErr(std::to_string(id));
@@ -193,16 +191,23 @@ class HostMem {
     void add_block(const Block &b) {
         if (b.id < 0 || b.id > (int64_t)1 << 40) throw ValueErr("block id out of range");
         if ((size_t)b.id >= blocks.size()) blocks.resize((size_t)b.id + 1);
-        if (blocks[(size_t)b.id]) by_base.erase(blocks[(size_t)b.id]->base);
+        if (blocks[(size_t)b.id]) {
+            const uint64_t old = blocks[(size_t)b.id]->base;
+            for (size_t i = 0; i < by_base.size(); ++i)
+                if (by_base[i].first == old && by_base[i].second == b.id) {
+                    by_base.erase(by_base.begin() + (long)i);
+                    break;
+                }
+        }
         blocks[(size_t)b.id].reset(new Block(b));
-        by_base[b.base] = b.id;
+        if (!by_base.empty() && by_base.back().first >= b.base) by_base_sorted = false;
+        by_base.emplace_back(b.base, b.id);
     }
     // memory.py block_at: the block containing [base, base+len)
     std::pair<Block *, uint64_t> block_at(uint64_t base, uint64_t len) {
-        auto it = by_base.upper_bound(base);
-        if (it != by_base.begin()) {
-            --it;
-            Block &b = block(it->second);
+        const size_t i = block_index(base);
+        if (i != SIZE_MAX) {
+            Block &b = block(by_base[i].second);
             if (b.base <= base && base + len <= b.base + b.len) return {&b, base - b.base};
         }
         throw BoundsErr("range (" + hex(base) + ", " + std::to_string(len) + ") is not inside any block");
@@ -229,21 +234,34 @@ class HostMem {
         write_guards.erase(owner);
         if (hw) spg_release(owner);
     }
-    // Read guards are disjoint (install rejects overlaps), so an index by
-    // base answers overlap queries in O(log n + k); results come back in task
-    // id order = the reference's dict insertion order (memory.py:244-259).
-    PMap<uint64_t, std::pair<uint64_t, int64_t>> rg_by_base;  // base -> (len, task)
+
+    // Read guards are disjoint (install rejects overlaps).  Each is listed
+    // under every block it overlaps (swap-outs guard one block, so a query
+    // scans one short list after one binary search over block bases); a
+    // guard over no block goes to `rg_loose`.  Results come back in task id
+    // order = the reference's dict insertion order (memory.py:244-259).
+    struct ReadGuard {
+        uint64_t base, len;
+    };
+    PUMap<int64_t, ReadGuard> read_guards;  // task id -> range
+    std::vector<PVec<int64_t>> rg_block;    // block id -> tasks of the guards overlapping it
+    PVec<int64_t> rg_loose;
 
     PVec<int64_t> read_guards_over(uint64_t base, uint64_t len) const {
         PVec<int64_t> out;
-        if (!len) return out;
-        auto it = rg_by_base.lower_bound(base);
-        if (it != rg_by_base.begin()) {
-            auto pv = std::prev(it);
-            if (pv->first + pv->second.first > base) out.push_back(pv->second.second);
-        }
-        for (; it != rg_by_base.end() && it->first < base + len; ++it) out.push_back(it->second.second);
+        if (!len || read_guards.empty()) return out;
+        auto scan = [&](const PVec<int64_t> &tasks) {
+            for (int64_t t : tasks) {
+                const ReadGuard &g = read_guards.at(t);
+                if (overlaps(base, len, g.base, g.len)) out.push_back(t);
+            }
+        };
+        blocks_over(base, len, [&](int64_t bid) {
+            if ((size_t)bid < rg_block.size()) scan(rg_block[(size_t)bid]);
+        });
+        scan(rg_loose);
         std::sort(out.begin(), out.end());
+        out.erase(std::unique(out.begin(), out.end()), out.end());  // a guard over several blocks
         return out;
     }
     void install_read_guard(uint64_t base, uint64_t len, int64_t task) {
@@ -251,14 +269,63 @@ class HostMem {
         if (!hits.empty())
             throw GuardErr("read guard (" + hex(base) + ", " + std::to_string(len) + ") overlaps task " +
                            std::to_string(hits.front()));
-        read_guards[task] = {base, len};
-        rg_by_base[base] = {len, task};
+        read_guards[task] = ReadGuard{base, len};
+        bool any = false;
+        blocks_over(base, len, [&](int64_t bid) {
+            if ((size_t)bid >= rg_block.size()) rg_block.resize((size_t)bid + 1);
+            rg_block[(size_t)bid].push_back(task);
+            any = true;
+        });
+        if (!any) rg_loose.push_back(task);
     }
     void release_read_guard(int64_t task) {
         auto it = read_guards.find(task);
         if (it == read_guards.end()) return;
-        rg_by_base.erase(it->second.first);
+        auto drop = [task](PVec<int64_t> &v) {
+            for (size_t i = 0; i < v.size(); ++i)
+                if (v[i] == task) {
+                    v[i] = v.back();
+                    v.pop_back();
+                    return;
+                }
+        };
+        blocks_over(it->second.base, it->second.len, [&](int64_t bid) {
+            if ((size_t)bid < rg_block.size()) drop(rg_block[(size_t)bid]);
+        });
+        drop(rg_loose);
         read_guards.erase(it);
+    }
+
+  private:
+    // (base, id) of every block; sorted on demand (bump allocation appends in order)
+    mutable std::vector<std::pair<uint64_t, int64_t>> by_base;
+    mutable bool by_base_sorted = true;
+    void sort_bases() const {
+        if (by_base_sorted) return;
+        std::sort(by_base.begin(), by_base.end());
+        by_base_sorted = true;
+    }
+    // index in by_base of the last block whose base <= addr, or SIZE_MAX
+    size_t block_index(uint64_t addr) const {
+        sort_bases();
+        // traces walk blocks in order: try the last hit and its successor first
+        const size_t n = by_base.size();
+        for (size_t c = hint_; c < n && c <= hint_ + 1; ++c)
+            if (by_base[c].first <= addr && (c + 1 == n || by_base[c + 1].first > addr)) return hint_ = c;
+        auto it = std::upper_bound(by_base.begin(), by_base.end(), std::make_pair(addr, INT64_MAX));
+        if (it == by_base.begin()) return SIZE_MAX;
+        return hint_ = (size_t)(it - by_base.begin()) - 1;
+    }
+    mutable size_t hint_ = 0;
+    template <class F>
+    void blocks_over(uint64_t base, uint64_t len, F &&f) const {
+        sort_bases();
+        size_t i = block_index(base);
+        if (i == SIZE_MAX) i = 0;
+        for (; i < by_base.size() && by_base[i].first < base + len; ++i) {
+            const Block *b = blocks[(size_t)by_base[i].second].get();
+            if (b && overlaps(base, len, b->base, b->len)) f(by_base[i].second);
+        }
     }
 };
 
