@@ -1391,13 +1391,24 @@ class Plane {
     }
     // One seal / open / mixed launch of libspgcm, issued in order.
     // kind: 0 sp_crypt_batch (per-message op), 1 sp_seal_batch, 2 sp_open_batch
+    // Batches of more than 256 messages go out as several launches of <= 256:
+    // libspgcm passes up to 256 descriptors inside the kernel parameters,
+    // beyond that it stages them with an H2D copy on the launch stream, and
+    // that copy waits for a copy engine busy with bulk swap traffic (and
+    // throttles the issuing thread on its staging slots).  The messages of
+    // one batch are independent, so consecutive launches on the stream (PDL
+    // chained) are equivalent.
+    static constexpr size_t kLaunchMsgs = 256;
     void post_batch(int kind, const std::vector<sp_desc> &d, cudaStream_t st, const char *what) {
         sp_ctx *c = ctx;
         iss.post([c, kind, st, what, d = std::vector<sp_desc>(d)] {
-            const int n = (int)d.size();
-            const int rc = kind == 0 ? sp_crypt_batch(c, d.data(), n, st)
-                                     : (kind == 1 ? sp_seal_batch(c, d.data(), n, st) : sp_open_batch(c, d.data(), n, st));
-            ck_sp(rc, what);
+            for (size_t i = 0; i < d.size(); i += kLaunchMsgs) {
+                const int n = (int)std::min(kLaunchMsgs, d.size() - i);
+                const sp_desc *p = d.data() + i;
+                const int rc = kind == 0 ? sp_crypt_batch(c, p, n, st)
+                                         : (kind == 1 ? sp_seal_batch(c, p, n, st) : sp_open_batch(c, p, n, st));
+                ck_sp(rc, what);
+            }
         });
     }
 
