@@ -19,6 +19,7 @@
 // calls cudaMalloc; a buffer is returned to the pool on the stream of its
 // last use once every other stream that touched it has passed its fence.
 #include <cuda_runtime.h>
+#include <pthread.h>
 
 #include <algorithm>
 #include <atomic>
@@ -584,6 +585,9 @@ struct Landing {
 // plane's reference-counted objects.  Anything that reads device state
 // (event queries of not-yet-issued records, stream/event syncs, status reads)
 // drains the queue first.  SPPIPE_ASYNC_ISSUE=0: every call inline.
+// A forked child has no issuing threads: its planes fall back to inline calls.
+std::atomic<bool> g_forked{false};
+
 class Issuer {
   public:
     static bool enabled_by_env() {
@@ -594,6 +598,11 @@ class Issuer {
         return on;
     }
     void start(int device) {
+        static const bool hooked = [] {
+            pthread_atfork(nullptr, nullptr, [] { g_forked.store(true); });
+            return true;
+        }();
+        (void)hooked;
         dev_ = device;
         th_ = std::thread([this] { run(); });
         on_ = true;
@@ -601,6 +610,11 @@ class Issuer {
     ~Issuer() { stop(); }
     void stop() {
         if (!on_) return;
+        if (g_forked.load()) {  // the thread does not exist in this process: forget it
+            new (&th_) std::thread();
+            on_ = false;
+            return;
+        }
         {
             std::lock_guard<std::mutex> lk(mu_);
             quit_ = true;
@@ -613,7 +627,7 @@ class Issuer {
     bool on() const { return on_; }
     // Run `fn` now (inline mode) or queue it; returns its sequence number.
     uint64_t post(std::function<void()> fn) {
-        if (!on_) {
+        if (!on_ || g_forked.load(std::memory_order_relaxed)) {
             fn();
             return 0;
         }
@@ -630,7 +644,7 @@ class Issuer {
     }
     bool done(uint64_t seq) const { return seq <= done_.load(std::memory_order_acquire); }
     void drain() {
-        if (!on_) return;
+        if (!on_ || g_forked.load(std::memory_order_relaxed)) return;
         std::unique_lock<std::mutex> lk(mu_);
         cv_done_.wait(lk, [&] { return done_.load(std::memory_order_acquire) == posted_; });
         lk.unlock();
@@ -802,6 +816,14 @@ class Plane {
     }
     ~Plane() {
         if (dry) return;
+        if (g_forked.load()) {
+            // CUDA is unusable in a forked child: no stream syncs or frees
+            // (the parent still owns the device memory); members unwind
+            // without CUDA calls
+            closing = true;
+            iss.stop();
+            return;
+        }
         bool idle = true;
         try {
             finish_streams();

@@ -435,3 +435,4 @@ def test_native_opt66b_offload_round_trip_full_size_gpu(chunk_kib):
     assert res.engine.plane_stats()["bytes_d2h"] == tr.swap_bytes() // 2
     after = [hashlib.sha256(b.data).digest() for b in mem.blocks()]
     assert after == before
+
