@@ -141,6 +141,7 @@ using BufP = Rc<Buf>;
 struct Slab : RcBase {
     BufP big;
     uint64_t off = 0;
+    FenceP born;  // recorded on the allocating stream right after the slab's allocation
 };
 
 struct View {
@@ -471,6 +472,7 @@ class Validator {
 // ---- data plane -----------------------------------------------------------------------
 struct Streams {
     cudaStream_t comp, spec, h2d, d2h, land, host, out;  // host: ordered app writes; out: swap-out seals
+    cudaStream_t comp2;  // consecutive flushes alternate between comp and comp2
 };
 
 struct DevicePool {
@@ -510,7 +512,7 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[7] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out};
+    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
     for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
     g_streams[dev] = s;
     return s;
@@ -745,6 +747,20 @@ class Plane {
 
     // compute queue
     std::vector<Op> ops, ops_spare;
+    std::vector<FenceP> flush_waits;  // fences the next flush's stream must wait for (swap-out WAR)
+    uint64_t flush_no = 0;
+    // Consecutive flushes alternate between two compute streams so one
+    // batch boundary's launches can overlap the previous one's (small
+    // batches are launch-latency bound); the order between them comes from
+    // each buffer's per-stream fences instead of stream order.
+    // SPPIPE_COMP_STREAMS=1: one compute stream.
+    static bool two_comp() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_COMP_STREAMS");
+            return !(e && e[0] == '1');
+        }();
+        return on;
+    }
     struct Touch {
         uint64_t lo, hi;
         int level;
@@ -860,6 +876,7 @@ class Plane {
         cache.clear();
         collect();
         cudaStreamSynchronize(s.comp);
+        cudaStreamSynchronize(s.comp2);
         if (ring.ptr) {
             // every copy through the ring is done (streams drained): hand it on
             ring.busy.clear();
@@ -940,6 +957,7 @@ class Plane {
             if (!sl || sl->off + need > sl->big->size) {
                 sl = pmake<Slab>();
                 sl->big = alloc_whole(kSlabBytes, st);
+                sl->born = record_new(st);
             }
             auto b = pmake<Buf>();
             b->plane = this;
@@ -948,7 +966,9 @@ class Plane {
             sl->off += need;
             b->slab = sl;
             b->last_stream = st;
-            b->uses.emplace_back(st, FenceP());
+            // its range was never used before: other streams need only the
+            // slab's allocation to be ordered before them
+            b->uses.emplace_back(st, sl->born);
             return b;
         }
         return alloc_whole(n, st);
@@ -1085,6 +1105,7 @@ class Plane {
         if (!status_used) return;
         iss.drain();
         ck(cudaStreamSynchronize(s.comp), "sync comp");
+        ck(cudaStreamSynchronize(s.comp2), "sync comp2");
         ck(cudaStreamSynchronize(s.land), "sync land");
         ck(cudaStreamSynchronize(s.d2h), "sync d2h");
         std::vector<int32_t> h(status_used);
@@ -1105,7 +1126,7 @@ class Plane {
             const Buf *b = op.w[k].buf;
             if (b->out_pending) launch_out();
             for (auto &u : b->uses)
-                if (u.first == s.out && u.second && u.second->recorded) wait(s.comp, u.second);
+                if (u.first == s.out && u.second && u.second->recorded) flush_waits.push_back(u.second);
         }
         if (op.a) op.a->queued++;
         if (op.b) op.b->queued++;
@@ -1191,30 +1212,65 @@ class Plane {
                 for (size_t i = 0; i < q.size(); ++i) by_level[fill[(size_t)op_level[i]]++] = (uint32_t)i;
             }
             const uint64_t mk = ++mark_seq;
+            const cudaStream_t cs = (two_comp() && (flush_no++ & 1)) ? s.comp2 : s.comp;
+            const cudaStream_t other = cs == s.comp ? s.comp2 : s.comp;
+            for (auto &f : flush_waits)
+                if (f->mark != mk) {
+                    wait(cs, f);
+                    f->mark = mk;
+                }
+            flush_waits.clear();
+            if (two_comp()) {
+                // what the other compute stream last did to these buffers
+                // (or, for buffers allocated on comp, its allocation point)
+                FenceP alloc_point;
+                auto order_after_other = [&](Buf *b) {
+                    for (auto &u : b->uses) {
+                        if (u.first != other) continue;
+                        if (u.second) {
+                            if (!u.second->recorded) continue;  // this flush's own window
+                            if (u.second->mark != mk) {
+                                wait(cs, u.second);
+                                u.second->mark = mk;
+                            }
+                        } else {
+                            if (!alloc_point) alloc_point = record_new(other);
+                            if (alloc_point->mark != mk) {
+                                wait(cs, alloc_point);
+                                alloc_point->mark = mk;
+                            }
+                        }
+                    }
+                };
+                for (auto &op : q) {
+                    if (op.a) order_after_other(op.a.get());
+                    if (op.b && op.b != op.a) order_after_other(op.b.get());
+                }
+            }
             auto &descs = descs_scratch;
             for (int lv = 0; lv <= top; ++lv) {
                 descs.clear();
                 for (uint32_t k = level_start[(size_t)lv]; k < level_start[(size_t)lv + 1]; ++k) {
                     const Op &op = q[by_level[k]];
                     if (op.wait && op.wait->mark != mk) {
-                        wait(s.comp, op.wait);
+                        wait(cs, op.wait);
                         op.wait->mark = mk;
                     }
                     descs.push_back(op.d);
                 }
                 if (descs.empty()) continue;
-                post_batch(0, descs, s.comp, "sp_crypt_batch");
+                post_batch(0, descs, cs, "sp_crypt_batch");
                 ++launches;
             }
-            record(window, s.comp);
+            record(window, cs);
             ++tick;
             for (auto &op : q) {
                 if (op.a) {
-                    op.a->use(s.comp, window, tick);
+                    op.a->use(cs, window, tick);
                     op.a->queued--;
                 }
                 if (op.b) {
-                    op.b->use(s.comp, window, tick);
+                    op.b->use(cs, window, tick);
                     op.b->queued--;
                 }
             }
@@ -1825,7 +1881,7 @@ class Plane {
     void finish_streams() {
         flush();
         iss.drain();
-        cudaStream_t all[7] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out};
+        cudaStream_t all[8] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out, s.comp2};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
     // drain_all = false: wait only for work whose results can be observed —
@@ -1842,7 +1898,7 @@ class Plane {
         } else {
             flush();
             iss.drain();
-            cudaStream_t obs[5] = {s.comp, s.out, s.land, s.d2h, s.host};
+            cudaStream_t obs[6] = {s.comp, s.comp2, s.out, s.land, s.d2h, s.host};
             for (auto st : obs) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         }
         check_auth();
@@ -1851,6 +1907,7 @@ class Plane {
         flush();
         iss.drain();
         ck(cudaStreamSynchronize(s.comp), "sync comp");
+        ck(cudaStreamSynchronize(s.comp2), "sync comp2");
         ck(cudaStreamSynchronize(s.land), "sync land");
         ck(cudaMemcpy(out, v.ptr(), v.len, cudaMemcpyDeviceToHost), "copy to host");
     }

@@ -390,7 +390,7 @@ def test_native_vs_python_random_traces_gpu():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("switch", ["SPPIPE_EAGER_OPEN=0", "SPPIPE_SLAB=0", "SPPIPE_OUT_STREAM=1", "SPPIPE_ASYNC_ISSUE=0",
+@pytest.mark.parametrize("switch", ["SPPIPE_EAGER_OPEN=0", "SPPIPE_SLAB=0", "SPPIPE_OUT_STREAM=1", "SPPIPE_ASYNC_ISSUE=0", "SPPIPE_COMP_STREAMS=1",
                                     "SPPIPE_BATCH_COPY=0"])
 def test_native_parity_under_data_plane_switches_gpu(switch):
     """The data-plane switches (drain-time opens, pool-only buffers, own-stream
