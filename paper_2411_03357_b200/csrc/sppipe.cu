@@ -1988,6 +1988,54 @@ struct Deferred {
     PVec<std::tuple<MsgP, uint64_t, uint64_t>> chunks;  // msg, iv, offset
     bool done = false, landing = false;
 };
+
+// Pending deferred decrypts by task id.  Ids are handed out in increasing
+// order, so a deque indexed by (id - first id) with holes for resolved
+// tasks replaces an ordered map: O(1) insert / find / erase, iteration in
+// id order (the reference's dict order, engine.py:579-581).
+class DeferredTable {
+  public:
+    Deferred *find(int64_t id) {
+        if (id < base_ || id >= base_ + (int64_t)q_.size()) return nullptr;
+        auto &slot = q_[(size_t)(id - base_)];
+        return slot.first ? &slot.second : nullptr;
+    }
+    Deferred &insert(Deferred &&d) {
+        const int64_t id = d.task_id;
+        if (q_.empty()) base_ = id;
+        if (id < base_ + (int64_t)q_.size()) throw std::logic_error("deferred task ids must increase");
+        while (base_ + (int64_t)q_.size() < id) q_.emplace_back(false, Deferred{});
+        q_.emplace_back(true, std::move(d));
+        ++live_;
+        return q_.back().second;
+    }
+    void erase(int64_t id) {
+        Deferred *d = find(id);
+        if (!d) return;
+        auto &slot = q_[(size_t)(id - base_)];
+        slot.first = false;
+        slot.second = Deferred{};
+        --live_;
+        while (!q_.empty() && !q_.front().first) {
+            q_.pop_front();
+            ++base_;
+        }
+    }
+    bool contains(int64_t id) { return find(id) != nullptr; }
+    size_t size() const { return live_; }
+    std::vector<int64_t> ids() const {
+        std::vector<int64_t> out;
+        out.reserve(live_);
+        for (size_t i = 0; i < q_.size(); ++i)
+            if (q_[i].first) out.push_back(base_ + (int64_t)i);
+        return out;
+    }
+
+  private:
+    std::deque<std::pair<bool, Deferred>> q_;
+    int64_t base_ = 0;
+    size_t live_ = 0;
+};
 struct Meta {
     int kind;  // 0 data, 1 small_io, 2 nop
     uint64_t seq;
@@ -2028,7 +2076,7 @@ class Engine {
     std::vector<Suspended> suspended;
     PSet<uint64_t> suspended_seqs;
     std::vector<int64_t> batch_ins, predicted_queue;
-    PMap<int64_t, Deferred> deferred;
+    DeferredTable deferred;
     int64_t next_task_id = 1;
     uint64_t next_seq = 0, next_label_iv = 0;
     std::deque<Meta> h2d_meta;
@@ -2082,20 +2130,19 @@ class Engine {
     // -- deferred decrypts --
     void resolve_decrypts_over(uint64_t base, uint64_t len, bool blocking) {
         for (int64_t tid : mem.read_guards_over(base, len)) {
-            auto it = deferred.find(tid);
-            if (it != deferred.end()) apply_decrypt(tid, blocking);
+            if (deferred.contains(tid)) apply_decrypt(tid, blocking);
         }
     }
     void apply_decrypt(int64_t tid, bool blocking) {
-        auto it = deferred.find(tid);
-        if (it == deferred.end() || it->second.done) return;
-        Deferred &t = it->second;
+        Deferred *tp = deferred.find(tid);
+        if (!tp || tp->done) return;
+        Deferred &t = *tp;
         if (!t.landing) land(t);
         mem.release_read_guard(t.task_id);
         t.done = true;
         int64_t task_id = t.task_id;
         uint64_t len = t.len;
-        deferred.erase(it);
+        deferred.erase(tid);
         if (blocking) {
             counters[C_SYNC_DECRYPTS]++;
             act(SP_ACT_RESOLVE_DECRYPT, -1, len, -1, task_id);
@@ -2295,9 +2342,9 @@ class Engine {
             t.base = r.base;
             t.len = r.len;
             t.chunks = std::move(taken);
-            deferred[tid] = std::move(t);
+            Deferred &dt = deferred.insert(std::move(t));
             mem.install_read_guard(r.base, r.len, tid);
-            land(deferred[tid]);
+            land(dt);
             counters[C_DEFERRED_DECRYPTS]++;
             act(SP_ACT_D2H_DATA, -1, r.len, -1, tid, false, false, 0, (int64_t)sq);
         } else {
@@ -2368,7 +2415,7 @@ class Engine {
         if (!faults.empty()) {
             counters[C_READ_FAULTS] += (int64_t)faults.size();
             for (int64_t tid : faults)
-                if (deferred.count(tid)) apply_decrypt(tid, true);
+                if (deferred.contains(tid)) apply_decrypt(tid, true);
             plane.host_sync(block_id);
         }
         if (b.host) memcpy(out, b.host + offset, n);
@@ -2567,7 +2614,7 @@ class Engine {
 
     void drain_decrypts() {
         std::vector<int64_t> ids;
-        for (auto &kv : deferred) ids.push_back(kv.first);
+        ids = deferred.ids();
         for (int64_t id : ids) apply_decrypt(id, false);
     }
 
