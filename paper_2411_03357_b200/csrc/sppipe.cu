@@ -494,6 +494,16 @@ struct IdleBufs {
 };
 std::map<int, IdleBufs> g_idle;
 constexpr uint64_t kIdleBytes = 16ull << 30;
+// Off by default: with slab allocation a new pipe makes few pool calls, and
+// parked buffers of sizes the next pipe does not use would only keep memory
+// from the pool (measured equal on the bench traces).
+bool idle_cache_enabled() {  // SPPIPE_IDLE_CACHE=1: hand a destroyed pipe's idle buffers to the next pipe
+    static const bool on = [] {
+        const char *e = getenv("SPPIPE_IDLE_CACHE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 sp_ctx *ctx_for(int dev, const uint8_t key[32]) {
     std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -865,7 +875,7 @@ class Plane {
             IdleBufs &ib = g_idle[dev];
             for (auto &kv : cache)
                 for (auto &g : kv.second) {
-                    if (idle && ib.bytes + kv.first <= kIdleBytes) {
+                    if (idle && idle_cache_enabled() && ib.bytes + kv.first <= kIdleBytes) {
                         ib.by_size[kv.first].push_back(g.ptr);
                         ib.bytes += kv.first;
                     } else {
