@@ -147,7 +147,7 @@ typedef struct sp_pipe_config {
     uint8_t reference_compat; /* 1: reproduce defect C2; 0: OTF sends burn the record at their counter */
     uint8_t dry;              /* 1: no bytes, no device (schedule only) */
     uint8_t hw_guards;        /* 1: also mprotect guarded host pages (libspguard) */
-    uint8_t reserved;
+    uint8_t window_aware;     /* 1: speculate only whole predicted batches that fit the record window */
     uint64_t initial_h2d_iv; /* cpu endpoint send_iv */
     uint64_t initial_d2h_iv; /* gpu endpoint send_iv */
     uint64_t batch_bytes;    /* flush a batched launch at this much payload (64 MiB) */

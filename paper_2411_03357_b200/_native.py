@@ -133,7 +133,8 @@ class SpPipeConfig(ctypes.Structure):
         ("workers", ctypes.c_uint32), ("chunk_bytes", ctypes.c_uint64), ("nop_bytes", ctypes.c_uint32),
         ("ring_slots", ctypes.c_uint32), ("speculate", ctypes.c_uint8), ("defer_swap_decrypt", ctypes.c_uint8),
         ("record_stream", ctypes.c_uint8), ("strict_auth", ctypes.c_uint8), ("reference_compat", ctypes.c_uint8),
-        ("dry", ctypes.c_uint8), ("hw_guards", ctypes.c_uint8), ("reserved", ctypes.c_uint8), ("initial_h2d_iv", ctypes.c_uint64),
+        ("dry", ctypes.c_uint8), ("hw_guards", ctypes.c_uint8), ("window_aware", ctypes.c_uint8),
+        ("initial_h2d_iv", ctypes.c_uint64),
         ("initial_d2h_iv", ctypes.c_uint64), ("batch_bytes", ctypes.c_uint64), ("reserve_bytes", ctypes.c_uint64),
     ]
 

@@ -2438,6 +2438,17 @@ class Engine {
         auto flat = pred->predict_batches(send_iv[H2D], cfg.leeway, (int)cfg.depth);
         predicted_queue.clear();
         for (auto &p : flat) predicted_queue.push_back(p.block);
+        if (cfg.window_aware) {
+            // whole predicted batches only, while they fit the record window
+            size_t keep = 0;
+            while (keep < flat.size()) {
+                size_t end = keep;
+                while (end < flat.size() && flat[end].batch == flat[keep].batch) ++end;
+                if (end > (size_t)cfg.window) break;
+                keep = end;
+            }
+            flat.resize(keep);
+        }
         std::vector<int64_t> planned;
         {
             std::vector<std::pair<uint64_t, int64_t>> recs;

@@ -269,6 +269,7 @@ class NativeEngine:
         cfg.chunk_bytes, cfg.nop_bytes, cfg.ring_slots = c.chunk_bytes, c.nop_bytes, c.ring_slots
         cfg.speculate, cfg.defer_swap_decrypt, cfg.record_stream = c.speculate, c.defer_swap_decrypt, c.record_stream
         cfg.strict_auth, cfg.reference_compat = c.strict_auth, c.reference_compat
+        cfg.window_aware = 1 if c.window_aware_on else 0
         cfg.dry = c.plane == "dry"
         cfg.hw_guards = bool(getattr(memory, "hw_guards", False))
         cfg.initial_h2d_iv, cfg.initial_d2h_iv = cpu.send_iv, gpu.send_iv

@@ -41,6 +41,7 @@ class ReplayConfig:
     # seeding 4 GB at CPU speed would dominate setup time)
     fill: str = "seeded"
     reference_compat: bool = True
+    window_aware: bool | None = None  # EngineConfig.window_aware (None: on iff reference_compat is off)
     # "python": engine.Engine over devplane.GpuPlane; "native": libsppipe
     # (native_engine.NativeEngine), dispatching the whole trace in one
     # sp_pipe_replay call unless `native_dispatch` is "python" (per event)
@@ -100,7 +101,8 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
     econf = EngineConfig(
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
-        record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat)
+        record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat,
+        window_aware=config.window_aware)
     if native:
         from .native_engine import NativeEngine, NativePredictor
 

@@ -327,18 +327,24 @@ def test_layer_larger_than_window_hits_c2_in_both_engines(chunk_mib):
     """A FIFO weight-offload layer split into more chunks than the validator
     window (64) triggers the reference's defect C2 without
     any adversarial mutation; the native and the Python engine raise the same
-    EngineError at the same point, and both complete with the fix on."""
+    EngineError at the same point, and both complete with the fix on: the
+    reference's speculation policy then burns records, the window-aware one
+    does not speculate batches larger than the window at all."""
     chunk = chunk_mib << 20
     tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=chunk)
-    for compat in (True, False):
+    for compat, aware in ((True, None), (False, False), (False, None)):
         runs = [run_engine(tr, ReplayConfig(plane="dry", engine=e, chunk_bytes=chunk, predictor_chunk_bytes=chunk,
-                                            reference_compat=compat), catch=True) for e in ("python", "native")]
+                                            reference_compat=compat, window_aware=aware), catch=True)
+                for e in ("python", "native")]
         assert runs[0].error == runs[1].error
         assert _schedule(runs[0].engine) == _schedule(runs[1].engine)
         if compat:
             assert runs[0].error.startswith("EngineError: commit at counter")
-        else:
+        elif aware is False:
             assert runs[0].error is None and runs[0].engine.report()["otf_burned_records"] > 0
+        else:
+            rep = runs[0].engine.report()
+            assert runs[0].error is None and rep.get("otf_burned_records", 0) == 0 and rep["spec_encrypts"] == 0
 
 
 def test_native_validator_view_matches_python():
