@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import json
 import os
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # as bench.py: no idle BLAS pool spinning
 import sys
 import time
 

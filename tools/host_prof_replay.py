@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # as bench.py: no idle BLAS pool spinning
 import sys
 import time
 

@@ -1,6 +1,7 @@
 """The bench's OPT-30B KV-swap comparison (config 3) alone, for A/B runs of
 data-plane switches (SPPIPE_* env):  python tools/kv_ab.py [reps]"""
 import os
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # as bench.py: no idle BLAS pool spinning
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
