@@ -6,18 +6,22 @@
 // trace yields identical sent logs, actions, report() counters and decision
 // logs (tests/test_native_engine.py against the reference goldens).
 //
-// Data plane (B200): five long-lived streams per device
+// Data plane (B200): long-lived streams per device, shared by the pipes
 //   h2d   plaintext of swap-ins crosses PCIe from the caller's pinned blocks
 //   spec  encrypt-ahead seals (SpecBatch, engine.py:487-513), <= batch_bytes per launch
-//   comp  ordered queue of on-the-fly / NOP / swap-out seals and every
-//         receiver open, flushed as one k_gcm launch per run of same-kind ops
+//   comp, comp2  the compute queue of on-the-fly / NOP / swap-out seals and
+//         every receiver open, flushed as level-scheduled k_gcm launches;
+//         consecutive flushes alternate between the two streams
+//   out   swap-out seals of KV-cache evictions
 //   land  host-endpoint opens of swap-outs (deferred decrypts)
 //   d2h   plaintext lands in the caller's host blocks
-// Cross-stream order uses CUDA events only.  Device staging comes from a
-// stream-ordered CUDA memory pool (cudaMallocFromPoolAsync) kept reserved for
-// the life of the process (release threshold = max), so steady state never
-// calls cudaMalloc; a buffer is returned to the pool on the stream of its
-// last use once every other stream that touched it has passed its fence.
+//   host  ordered application writes into host blocks
+// Cross-stream order uses CUDA events only; the calls are issued in order by
+// one worker thread per pipe (Issuer).  Device buffers of <= 1 MiB come from
+// 32 MiB slabs, larger ones from a stream-ordered CUDA memory pool kept
+// reserved for the life of the process (release threshold = max); a buffer
+// is returned to the pool on the stream of its last use once every other
+// stream that touched it has passed its fence.
 #include <cuda_runtime.h>
 #include <pthread.h>
 
