@@ -127,6 +127,21 @@ int sp_pred_cycle_entry(sp_pred *p, int64_t i, int64_t *blocks, int32_t cap, int
 int sp_pred_predict_batches(sp_pred *p, uint64_t current_iv, uint64_t leeway, int32_t depth,
                             sp_prediction *out, int32_t cap, int32_t *n);
 int sp_pred_outstanding(sp_pred *p, int64_t *out, int64_t cap, int64_t *n); /* swap-out order */
+/* predict_batches with an explicit outstanding set (the reference's free
+ * function predict_batches(history, outstanding, ...), predictor.py:252-297). */
+int sp_pred_predict_batches_in(sp_pred *p, uint64_t current_iv, uint64_t leeway, int32_t depth,
+                               const int64_t *outstanding, int64_t n_out, sp_prediction *out, int32_t cap,
+                               int32_t *n);
+/* Scripted mode (the scenario mock of cli.py:241-259): predict_batches hands
+ * out `preds` once (grouped by their batch field), the outstanding set is
+ * `outstanding`, observations are ignored. */
+int sp_pred_script(sp_pred *p, const sp_prediction *preds, int32_t n, const int64_t *outstanding, int64_t n_out);
+/* SwapHistory.events (predictor.py:128-150): kind 0 swap-out (value = block),
+ * 1 swap-in (value = index of its batch in the in-batches), 2 sync. */
+int64_t sp_pred_event_count(sp_pred *p);
+int sp_pred_event(sp_pred *p, int64_t i, int32_t *kind, int64_t *value);
+/* SwapHistory.in_batches[i] (sorted blocks). */
+int sp_pred_in_batch(sp_pred *p, int64_t i, int64_t *blocks, int32_t cap, int32_t *n);
 int64_t sp_pred_in_batch_count(sp_pred *p);
 int64_t sp_pred_decision_count(sp_pred *p);
 int sp_pred_decision(sp_pred *p, int64_t i, sp_decision *out);
@@ -212,6 +227,8 @@ int sp_pipe_speculate(sp_pipe *p);
 int sp_pipe_relinquish(sp_pipe *p, int64_t *count);
 int sp_pipe_drain_decrypts(sp_pipe *p);
 int sp_pipe_finish(sp_pipe *p);
+/* audit() (engine.py:595-605): counter ledger and shared-ring checks. */
+int sp_pipe_audit(sp_pipe *p);
 /* finish() that returns once every observable result is final (all
  * committed transfers opened and verified, all landings and app writes on
  * the host) without waiting for encrypt-ahead work of records discarded at
@@ -264,6 +281,10 @@ typedef struct sp_record {
 } sp_record;
 int64_t sp_pipe_record_count(sp_pipe *p);
 int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out);
+/* Pending record ids in label order (validator.pending_records) and the
+ * pending record holding counter iv (-1: none). */
+int sp_pipe_pending(sp_pipe *p, int64_t *ids, int64_t cap, int64_t *n);
+int64_t sp_pipe_pending_at_iv(sp_pipe *p, uint64_t iv);
 int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which);
 int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, void *bytes);
 /* Data-plane statistics: bytes over PCIe per direction, kernel launches. */
@@ -272,6 +293,28 @@ int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t
  * handed out, bytes parked in this pipe's buffer cache. */
 int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t *cached);
 const char *sp_pipe_last_error(void);
+
+/* A standalone validator (specpipe.validator.Validator, validator.py:90-236):
+ * the pipe's own record window without an engine.  Records hold no payload
+ * here (the Python side keeps the ciphertext objects); span = number of
+ * consecutive counters (chunks).  Verdicts: SP_VERDICT_*; record_id -1 for
+ * MISS.  counters: hit, iv_ahead, iv_behind, stale, miss, evicted. */
+typedef struct sp_val sp_val;
+int sp_val_create(uint64_t window, sp_val **out);
+void sp_val_destroy(sp_val *v);
+int sp_val_label(sp_val *v, uint64_t base, uint64_t len, uint64_t iv, uint64_t span, int64_t block_id, int64_t *id);
+int sp_val_validate(sp_val *v, uint64_t base, uint64_t len, uint64_t current_iv, int32_t *verdict,
+                    int64_t *record_id);
+int sp_val_commit(sp_val *v, int64_t id);
+int sp_val_invalidate(sp_val *v, int64_t id);
+int sp_val_write_fault(sp_val *v, int64_t owner);
+int64_t sp_val_pending_at_iv(sp_val *v, uint64_t iv);
+int32_t sp_val_has_pending_range(sp_val *v, uint64_t base, uint64_t len);
+int sp_val_invalidate_pending_below(sp_val *v, uint64_t iv, int64_t *n);
+int sp_val_pending(sp_val *v, int64_t *ids, int64_t cap, int64_t *n);
+int64_t sp_val_record_count(sp_val *v);
+int sp_val_record(sp_val *v, int64_t id, sp_record *out);
+int sp_val_counters(sp_val *v, int64_t out[6]);
 
 #ifdef __cplusplus
 }

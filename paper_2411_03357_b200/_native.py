@@ -95,13 +95,18 @@ SPPIPE_SYMBOLS = (
     "sp_pred_create", "sp_pred_destroy", "sp_pred_classify", "sp_pred_observe_out", "sp_pred_observe_in",
     "sp_pred_observe_sync", "sp_pred_recognize", "sp_pred_cycle_entry", "sp_pred_predict_batches",
     "sp_pred_outstanding", "sp_pred_in_batch_count", "sp_pred_decision_count", "sp_pred_decision",
+    "sp_pred_predict_batches_in", "sp_pred_script", "sp_pred_event_count", "sp_pred_event", "sp_pred_in_batch",
     "sp_pipe_create", "sp_pipe_destroy", "sp_pipe_register_block", "sp_pipe_seed_device", "sp_pipe_submit_h2d",
     "sp_pipe_submit_d2h", "sp_pipe_small_io", "sp_pipe_sync", "sp_pipe_speculate", "sp_pipe_relinquish",
-    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_finish_observable", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
+    "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_audit", "sp_pipe_finish_observable", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
     "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
-    "sp_pipe_record_count", "sp_pipe_record", "sp_pipe_delivered_count", "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
+    "sp_pipe_record_count", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
+    "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
+    "sp_val_create", "sp_val_destroy", "sp_val_label", "sp_val_validate", "sp_val_commit", "sp_val_invalidate",
+    "sp_val_write_fault", "sp_val_pending_at_iv", "sp_val_has_pending_range", "sp_val_invalidate_pending_below", "sp_val_pending",
+    "sp_val_record_count", "sp_val_record", "sp_val_counters",
 )
 
 
@@ -192,6 +197,19 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pred_predict_batches": [vp, u64, u64, i32, P(SpPrediction), i32, P(i32)],
             "sp_pred_outstanding": [vp, P(i64), i64, P(i64)],
             "sp_pred_decision": [vp, i64, P(SpDecision)],
+            "sp_pred_predict_batches_in": [vp, u64, u64, i32, P(i64), i64, P(SpPrediction), i32, P(i32)],
+            "sp_pred_script": [vp, P(SpPrediction), i32, P(i64), i64],
+            "sp_pred_event": [vp, i64, P(i32), P(i64)],
+            "sp_pred_in_batch": [vp, i64, P(i64), i32, P(i32)],
+            "sp_pipe_pending": [vp, P(i64), i64, P(i64)],
+            "sp_val_create": [u64, P(vp)],
+            "sp_val_label": [vp, u64, u64, u64, u64, i64, P(i64)],
+            "sp_val_validate": [vp, u64, u64, u64, P(i32), P(i64)],
+            "sp_val_commit": [vp, i64], "sp_val_invalidate": [vp, i64], "sp_val_write_fault": [vp, i64],
+            "sp_val_invalidate_pending_below": [vp, u64, P(i64)],
+            "sp_val_pending": [vp, P(i64), i64, P(i64)],
+            "sp_val_record": [vp, i64, P(SpRecord)],
+            "sp_val_counters": [vp, P(i64)],
             "sp_pipe_create": [P(SpPipeConfig), ctypes.c_char_p, vp, P(vp)],
             "sp_pipe_register_block": [vp, i64, u64, u64, i32, vp],
             "sp_pipe_seed_device": [vp, i64, vp, u64, i32],
@@ -199,7 +217,7 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_submit_d2h": [vp, u64, u64, i32, i64, P(u64)],
             "sp_pipe_small_io": [vp, i32, vp, u64],
             "sp_pipe_sync": [vp], "sp_pipe_speculate": [vp], "sp_pipe_relinquish": [vp, P(i64)],
-            "sp_pipe_drain_decrypts": [vp], "sp_pipe_finish": [vp], "sp_pipe_finish_observable": [vp],
+            "sp_pipe_drain_decrypts": [vp], "sp_pipe_finish": [vp], "sp_pipe_audit": [vp], "sp_pipe_finish_observable": [vp],
             "sp_pipe_flush": [vp, i32],
             "sp_pipe_app_write": [vp, i64, u64, vp, u64, P(i64)],
             "sp_pipe_app_read": [vp, i64, u64, u64, vp],
@@ -221,15 +239,21 @@ def load_sppipe() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
-        for name in ("sp_pred_destroy", "sp_pipe_destroy"):
+        for name in ("sp_pred_destroy", "sp_pipe_destroy", "sp_val_destroy"):
             getattr(lib, name).argtypes = [vp]
             getattr(lib, name).restype = None
-        for name in ("sp_pred_in_batch_count", "sp_pred_decision_count"):
+        for name in ("sp_pred_in_batch_count", "sp_pred_decision_count", "sp_pred_event_count", "sp_val_record_count"):
             getattr(lib, name).argtypes = [vp]
             getattr(lib, name).restype = i64
         for name in ("sp_pipe_action_count",):
             getattr(lib, name).argtypes = [vp]
             getattr(lib, name).restype = i64
+        lib.sp_pipe_pending_at_iv.argtypes = [vp, u64]
+        lib.sp_pipe_pending_at_iv.restype = i64
+        lib.sp_val_pending_at_iv.argtypes = [vp, u64]
+        lib.sp_val_pending_at_iv.restype = i64
+        lib.sp_val_has_pending_range.argtypes = [vp, u64, u64]
+        lib.sp_val_has_pending_range.restype = i32
         lib.sp_pipe_sent_count.argtypes = [vp, i32]
         lib.sp_pipe_sent_count.restype = i64
         if hasattr(lib, "sp_pipe_record_count"):

@@ -67,6 +67,19 @@ __device__ __forceinline__ void fill_tables(uint8_t *sm, const P &p) {
     }
 }
 
+// Compact tables for latency-bound launches (SmallTabs layout): 10 KB.
+template <class P>
+__device__ __forceinline__ void fill_tables_small(uint8_t *sm, const P &p) {
+    // T0..T3 (4 x 256 words) + R8 (256 words) = 1280 words; M_G = 256 x 16 B
+    for (uint32_t f = threadIdx.x; f < 1280u; f += blockDim.x) {
+        const uint32_t v = __ldg(p.ttab + f);  // ttab = T0..T3 then R8, contiguous
+        if (f < 1024u) *reinterpret_cast<uint32_t *>(sm + kSmallT + f * 4u) = v;
+        else *reinterpret_cast<uint32_t *>(sm + kSmallR8 + (f - 1024u) * 4u) = v;
+    }
+    for (uint32_t f = threadIdx.x; f < 256u; f += blockDim.x)
+        *reinterpret_cast<uint4 *>(sm + kSmallMG + f * 16u) = __ldg(p.mg + f);
+}
+
 __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v) {
     uint32_t old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -78,13 +91,9 @@ __device__ __forceinline__ uint4 len_block(uint64_t len) {
     return make_uint4(0u, 0u, bswap32((uint32_t)(bits >> 32)), bswap32((uint32_t)bits));
 }
 
-// Tag finalisation for one message; S = GHASH without E_K(J0).  Warp-uniform.
-template <class P>
-__device__ __forceinline__ void finish_message(const uint8_t *sm, const P &p, const MsgDev &md,
-                                               uint4 S, uint32_t x0, uint32_t x1, uint32_t x2,
-                                               uint32_t lct, int lane) {
-    const uint4 ek = aes256_rounds(sm, p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
-    const uint4 tag = xor4(S, ek);
+// Tag finalisation for one message; T = GHASH xor E_K(J0) (the warp that
+// covered the message's first row folded E_K(J0) in).  Warp-uniform.
+__device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int lane) {
     if (!(md.dir & kOpenBit)) {
         if (lane == 0) {
             if ((reinterpret_cast<uintptr_t>(md.tag) & 15u) == 0)
@@ -102,20 +111,30 @@ __device__ __forceinline__ void finish_message(const uint8_t *sm, const P &p, co
     }
     bad = __shfl_sync(0xffffffffu, bad, 0);
     if (bad) {
-        // unverified plaintext never leaves: zero the whole output
-        for (uint64_t k = (uint64_t)lane; k < md.len; k += 32) md.dst[k] = 0;
+        // unverified plaintext never leaves: zero the whole output, 16 B per
+        // lane store where aligned
+        uint64_t k = 0;
+        const uint64_t head = (16u - (reinterpret_cast<uintptr_t>(md.dst) & 15u)) & 15u;
+        for (uint64_t j = (uint64_t)lane; j < min(head, md.len); j += 32) md.dst[j] = 0;
+        k = min(head, md.len);
+        const uint64_t nvec = (md.len - k) >> 4;
+        uint4 *v = reinterpret_cast<uint4 *>(md.dst + k);
+        for (uint64_t j = (uint64_t)lane; j < nvec; j += 32) v[j] = make_uint4(0, 0, 0, 0);
+        for (uint64_t j = k + (nvec << 4) + (uint64_t)lane; j < md.len; j += 32) md.dst[j] = 0;
     }
 }
 
-template <uint32_t INL>
-__global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KParamsT<INL> p) {
+template <uint32_t INL, class TB>
+__global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSmall ? 4 : 1)
+    k_gcm(const __grid_constant__ KParamsT<INL> p) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
     // let a dependent launch on this stream be scheduled now: its CTAs take
     // idle SMs and fill their tables while this grid runs (they read no data
     // before their own griddepcontrol.wait, which waits for this grid to end)
     asm volatile("griddepcontrol.launch_dependents;");
-    fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
+    if (TB::kSmall) fill_tables_small(sm, p);
+    else fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
     __syncthreads();
     // programmatic dependent launch: everything below may read what the
     // previous kernel on this stream wrote (messages, accumulators)
@@ -190,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             }
         }
         const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);
-        const CtrConst cc = ctr_const(p.rk, lct, x0, x1, x2);
+        const CtrConst cc = ctr_const<TB>(p.rk, lct, x0, x1, x2);
         CtrCache ck;
         ck.gid = 0xffffffffu;
         ck.d0 = ck.d1 = ck.d2 = ck.d3 = 0;
@@ -200,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             const uint4 nxt = (t + 1 < t_b) ? load_row(t + 1) : make_uint4(0, 0, 0, 0);
             const int64_t i = base_i + 32 * (int64_t)t;
             const uint32_t ctr = (uint32_t)(i + 2);
-            const uint4 ks = aes256_ctr(p.rk, lct, cc, ck, ctr);
+            const uint4 ks = aes256_ctr<TB>(p.rk, lct, cc, ck, ctr);
             uint4 out = xor4(cur, ks);
             uint4 gin = cur;
             if (i >= 0) {
@@ -213,20 +232,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
             } else {
                 gin = make_uint4(0, 0, 0, 0);
             }
-            y = (t == t_a) ? gin : xor4(gmul_g(y, lcm, lcr), gin);
+            y = (t == t_a) ? gin : xor4(gmul_g<TB>(y, lcm, lcr), gin);
             cur = nxt;
         }
 
-        // combine lanes: W = sum_l Y_l * H^(32 - l)
-        uint4 w = warp_xor(nt_mul_lane(p.nt + (size_t)(kNtLane + 31 - lane) * kNtEntries, y));
+        // combine lanes: W = sum_l Y_l * H^(32 - l); the lane-table loads
+        // are in flight while the warp covering the message's first row
+        // computes E_K(J0) (folded into W: XOR is order-free, so the
+        // finisher needs no AES of its own)
+        const uint4 lanes_w = nt_mul_lane(p.nt + (size_t)(kNtLane + 31 - lane) * kNtEntries, y);
+        uint4 ek = make_uint4(0, 0, 0, 0);
+        if (t_a == 0 && lane == 0) ek = aes256_rounds<TB>(p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
+        uint4 w = warp_xor(lanes_w);
         // scale by H^(32*r_end + 1), r_end = rows after this run
         const uint32_t r_end = md.rows - (uint32_t)t_b;
         w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
         if (r_end & 15u) w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+        if (t_a == 0) {
+            ek.x = __shfl_sync(0xffffffffu, ek.x, 0);
+            ek.y = __shfl_sync(0xffffffffu, ek.y, 0);
+            ek.z = __shfl_sync(0xffffffffu, ek.z, 0);
+            ek.w = __shfl_sync(0xffffffffu, ek.w, 0);
+            w = xor4(w, ek);
+        }
 
         if (t_a == 0 && t_b == md.rows) {
-            const uint4 S = xor4(w, warp_xor(lh_part));
-            finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
+            finish_message(md, xor4(w, warp_xor(lh_part)), lane);
         } else {
             uint32_t *acc = p.acc + (size_t)m * 8u;
             // XOR-accumulate (order-free, so deterministic) and count rows:
@@ -246,8 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gcm(const __grid_constant__ KPa
                 a.y = __shfl_sync(0xffffffffu, v, 1);
                 a.z = __shfl_sync(0xffffffffu, v, 2);
                 a.w = __shfl_sync(0xffffffffu, v, 3);
-                const uint4 S = xor4(a, warp_xor(lh_part));
-                finish_message(sm, p, md, S, x0, x1, x2, lct, lane);
+                finish_message(md, xor4(a, warp_xor(lh_part)), lane);
             }
         }
         g = md.row_begin + t_b;
@@ -563,6 +593,34 @@ void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, u
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }
 
+// Latency-bound launches (few rows: NOP pads, token I/O, KV blocks) run the
+// SmallTabs variant: 10 KB of tables per CTA instead of 192 KB, 128-thread
+// CTAs, up to 4 per SM, filling SMs one warp per CTA first.
+// SPGCM_SMALL_ROWS (default 256 rows = 128 KiB; 0 disables) and
+// SPGCM_SMALL_RPW (rows per warp, default 2) are for sweeps.
+uint64_t env_u64(const char *name, uint64_t dflt) {
+    const char *e = getenv(name);
+    return e ? (uint64_t)atoll(e) : dflt;
+}
+uint64_t small_rows_max() {
+    static const uint64_t v = env_u64("SPGCM_SMALL_ROWS", 256);
+    return v;
+}
+uint64_t small_rows_per_warp() {
+    static const uint64_t v = std::max<uint64_t>(1, env_u64("SPGCM_SMALL_RPW", 2));
+    return v;
+}
+
+void launch_shape_small(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
+    const uint64_t sms = (uint64_t)ctx->num_sms;
+    const uint64_t per_cta = kThreadsSmall / 32, ctas_per_sm = 4;
+    const uint64_t want_warps = std::max<uint64_t>(
+        1, std::min<uint64_t>(std::max(rows / small_rows_per_warp(), std::min(nmsgs, rows)),
+                              sms * ctas_per_sm * per_cta));
+    warps_used = (uint32_t)std::min<uint64_t>(per_cta, (want_warps + sms * ctas_per_sm - 1) / (sms * ctas_per_sm));
+    grid = (int)((want_warps + warps_used - 1) / warps_used);
+}
+
 int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
     if (ws->cap_msgs < nmsgs) {
         if (ws->d_msgs) SP_CUDA(cudaFree(ws->d_msgs), "cudaFree");
@@ -586,7 +644,9 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
     p.row_begin = row_begin;
     p.row_end = row_end;
     int grid = 1;
-    launch_shape(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
+    const bool small = row_end - row_begin <= small_rows_max();
+    if (small) launch_shape_small(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
+    else launch_shape(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
     // Programmatic dependent launch: a launch that directly follows another
     // kernel on the stream starts (and fills its shared-memory tables)
     // while that kernel's last CTAs drain; it waits in griddepcontrol.wait
@@ -597,15 +657,18 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
     }();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.blockDim = dim3(small ? kThreadsSmall : kThreads);
+    cfg.dynamicSmemBytes = small ? kSmallSmem : kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL>, p), "k_gcm launch");
+    if (small)
+        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, SmallTabs>, p), "k_gcm launch");
+    else
+        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, BigTabs>, p), "k_gcm launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SP_OK;
 }
@@ -961,10 +1024,10 @@ int sp_ctx_create(const uint8_t key[SP_KEY_BYTES], sp_ctx **out) {
     cudaDeviceProp prop;
     SP_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
     if (prop.major != 10) return fail(SP_ENODEV, "libspgcm is built for sm_100a (B200) only");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
-            "cudaFuncSetAttribute(k_gcm)");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes),
-            "cudaFuncSetAttribute(k_gcm big)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm big)");
     sp_ctx *c = new sp_ctx();
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;

@@ -30,6 +30,7 @@
 namespace spgcm {
 
 constexpr int kThreads = 512;
+constexpr int kThreadsSmall = 128;  // latency variant (SmallTabs): 4 warps, up to 4 CTAs per SM
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr uint64_t kMaxMsg = 32ull << 20;
 constexpr uint32_t kMaxRows = (uint32_t)((kMaxMsg / 16 + 31) / 32);  // 65536
@@ -132,17 +133,60 @@ __device__ __forceinline__ uint4 lds128_at(uint32_t addr) {
     return v;
 }
 
-template <uint32_t OFF>
-__device__ __forceinline__ uint32_t tl(uint32_t w, uint32_t sel, uint32_t lc) {
-    return lds32_at<OFF>(__byte_perm(w, lc, sel));
+// ---- table policies -----------------------------------------------------------
+// Big: the lane-replicated layout above (conflict-free LDS, one PRMT per
+// lookup; 192 KB per CTA).  Small: one copy of each table (T0..T3 1 KB each,
+// M_G 4 KB, R8 1 KB = 10 KB per CTA) for latency-bound launches: the fill is
+// 19x smaller, lookups cost one more ALU op and some bank conflicts.
+constexpr uint32_t kSmallT = 0;        // T0..T3: table t entry v at t*1024 + v*4
+constexpr uint32_t kSmallMG = 4096;    // M_G[v] at 4096 + v*16
+constexpr uint32_t kSmallR8 = 8192;    // R8[v]  at 8192 + v*4
+constexpr uint32_t kSmallSmem = 9216;
+
+template <int K>
+__device__ __forceinline__ uint32_t byte_x4(uint32_t w) {  // byte K of w, times 4
+    return K == 0 ? (w << 2) & 0x3fcu : (w >> (8 * K - 2)) & 0x3fcu;
+}
+template <int K>
+__device__ __forceinline__ uint32_t byte_x16(uint32_t w) {  // byte K of w, times 16
+    return K == 0 ? (w << 4) & 0xff0u : (w >> (8 * K - 4)) & 0xff0u;
 }
 
-#define T0L(w, b) tl<kSmAes0>(w, SP_SEL(b), lc)
-#define T1L(w, b) tl<kSmAes0 + 128>(w, SP_SEL(b), lc)
-#define T2L(w, b) tl<kSmAes1>(w, SP_SEL(b), lc)
-#define T3L(w, b) tl<kSmAes1 + 128>(w, SP_SEL(b), lc)
+struct BigTabs {
+    static constexpr bool kSmall = false;
+    template <int T, int K>
+    static __device__ __forceinline__ uint32_t t(uint32_t w, uint32_t lc) {
+        return lds32_at<(T < 2 ? kSmAes0 : kSmAes1) + (T & 1) * 128u>(__byte_perm(w, lc, SP_SEL(K)));
+    }
+    template <int K>
+    static __device__ __forceinline__ uint4 mg(uint32_t w, uint32_t lcm) {
+        return lds128_at<kSmGh>(__byte_perm(w, lcm, SP_SEL(K)));
+    }
+    static __device__ __forceinline__ uint32_t r8(uint32_t w, uint32_t lcr) {
+        return lds32_at<kSmGh>(__byte_perm(w, lcr, SP_SEL(3)));
+    }
+};
+
+struct SmallTabs {
+    static constexpr bool kSmall = true;
+    template <int T, int K>
+    static __device__ __forceinline__ uint32_t t(uint32_t w, uint32_t) {
+        return lds32_at<kSmallT + T * 1024u>(byte_x4<K>(w));
+    }
+    template <int K>
+    static __device__ __forceinline__ uint4 mg(uint32_t w, uint32_t) {
+        return lds128_at<kSmallMG>(byte_x16<K>(w));
+    }
+    static __device__ __forceinline__ uint32_t r8(uint32_t w, uint32_t) { return lds32_at<kSmallR8>(byte_x4<3>(w)); }
+};
+
+#define T0L(w, b) TB::template t<0, b>(w, lc)
+#define T1L(w, b) TB::template t<1, b>(w, lc)
+#define T2L(w, b) TB::template t<2, b>(w, lc)
+#define T3L(w, b) TB::template t<3, b>(w, lc)
 
 // Rounds r0..13 (full T-table rounds) on state s0..s3, then the final round.
+template <class TB>
 __device__ __forceinline__ uint4 aes256_from_round(int r0, const uint32_t *rk, uint32_t lc, uint32_t s0,
                                                    uint32_t s1, uint32_t s2, uint32_t s3) {
 #pragma unroll
@@ -169,9 +213,10 @@ __device__ __forceinline__ uint4 aes256_from_round(int r0, const uint32_t *rk, u
 }
 
 // s0..s3: counter block words already XORed with round key 0.
-__device__ __forceinline__ uint4 aes256_rounds(const uint8_t *, const uint32_t *rk, uint32_t lc, uint32_t s0,
-                                               uint32_t s1, uint32_t s2, uint32_t s3) {
-    return aes256_from_round(1, rk, lc, s0, s1, s2, s3);
+template <class TB>
+__device__ __forceinline__ uint4 aes256_rounds(const uint32_t *rk, uint32_t lc, uint32_t s0, uint32_t s1,
+                                               uint32_t s2, uint32_t s3) {
+    return aes256_from_round<TB>(1, rk, lc, s0, s1, s2, s3);
 }
 
 // ---- counter-mode caching ----------------------------------------------------
@@ -188,6 +233,7 @@ struct CtrCache {
     uint32_t d0, d1, d2, d3;  // round-2 partial columns (group constants)
 };
 
+template <class TB>
 __device__ __forceinline__ CtrConst ctr_const(const uint32_t *rk, uint32_t lc, uint32_t x0, uint32_t x1,
                                               uint32_t x2) {
     CtrConst c;
@@ -199,6 +245,7 @@ __device__ __forceinline__ CtrConst ctr_const(const uint32_t *rk, uint32_t lc, u
     return c;
 }
 
+template <class TB>
 __device__ __forceinline__ void ctr_refresh(CtrCache &k, const CtrConst &c, const uint32_t *rk, uint32_t lc,
                                             uint32_t s3, uint32_t gid) {
     const uint32_t t1 = c.c1 ^ T2L(s3, 2);
@@ -211,17 +258,18 @@ __device__ __forceinline__ void ctr_refresh(CtrCache &k, const CtrConst &c, cons
     k.gid = gid;
 }
 
+template <class TB>
 __device__ __forceinline__ uint4 aes256_ctr(const uint32_t *rk, uint32_t lc, const CtrConst &c, CtrCache &k,
                                             uint32_t ctr) {
     const uint32_t s3 = bswap32(ctr) ^ rk[3];
     const uint32_t gid = ctr >> 8;
-    if (gid != k.gid) ctr_refresh(k, c, rk, lc, s3, gid);
+    if (gid != k.gid) ctr_refresh<TB>(k, c, rk, lc, s3, gid);
     const uint32_t t0 = c.c0 ^ T3L(s3, 3);
     const uint32_t u0 = T0L(t0, 0) ^ k.d0;
     const uint32_t u1 = T3L(t0, 3) ^ k.d1;
     const uint32_t u2 = T2L(t0, 2) ^ k.d2;
     const uint32_t u3 = T1L(t0, 1) ^ k.d3;
-    return aes256_from_round(3, rk, lc, u0, u1, u2, u3);
+    return aes256_from_round<TB>(3, rk, lc, u0, u1, u2, u3);
 }
 
 // ---- GHASH: Y * G with an 8-bit Shoup table in shared memory ----------------
@@ -232,17 +280,23 @@ __device__ __forceinline__ uint4 aes256_ctr(const uint32_t *rk, uint32_t lc, con
 // pipe and moving the byte shifts there too removes 15 shared wavefronts per
 // row but lengthens every Horner step's dependency chain; it ran at 422 GB/s
 // vs 483 GB/s for the table version, so the table stays.)
+template <class TB>
 __device__ __forceinline__ uint4 gmul_g(uint4 y, uint32_t lcm, uint32_t lcr) {
-    uint4 z = lds128_at<kSmGh>(__byte_perm(y.w, lcm, SP_SEL(3)));
+    uint4 z = TB::template mg<3>(y.w, lcm);
 #pragma unroll
     for (int b = 14; b >= 0; --b) {
-        const uint32_t raddr = __byte_perm(z.w, lcr, SP_SEL(3));
+        const uint32_t r = TB::r8(z.w, lcr);
         z.w = __funnelshift_l(z.z, z.w, 8);
         z.z = __funnelshift_l(z.y, z.z, 8);
         z.y = __funnelshift_l(z.x, z.y, 8);
         z.x = z.x << 8;
-        const uint32_t r = lds32_at<kSmGh>(raddr);
-        const uint4 m = lds128_at<kSmGh>(__byte_perm(word_of(y, b >> 2), lcm, SP_SEL(b & 3)));
+        uint4 m;
+        switch (b & 3) {
+            case 0: m = TB::template mg<0>(word_of(y, b >> 2), lcm); break;
+            case 1: m = TB::template mg<1>(word_of(y, b >> 2), lcm); break;
+            case 2: m = TB::template mg<2>(word_of(y, b >> 2), lcm); break;
+            default: m = TB::template mg<3>(word_of(y, b >> 2), lcm); break;
+        }
         z.x ^= r ^ m.x;
         z.y ^= m.y;
         z.z ^= m.z;

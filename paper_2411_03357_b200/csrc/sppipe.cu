@@ -2822,6 +2822,13 @@ struct sp_pred {
 struct sp_pipe {
     std::unique_ptr<Engine> e;
 };
+// A validator of its own (validator.Validator used without an engine): the
+// same class the pipe runs, over an empty host-memory model.
+struct sp_val {
+    HostMem mem;
+    Validator v;
+    explicit sp_val(uint64_t window) : v(mem, window) {}
+};
 
 namespace {
 
@@ -2936,9 +2943,45 @@ int sp_pred_predict_batches(sp_pred *p, uint64_t current_iv, uint64_t leeway, in
 }
 int sp_pred_outstanding(sp_pred *p, int64_t *out, int64_t cap, int64_t *n) {
     return guarded([&] {
-        const auto &v = p->p.outstanding_in_order();
+        const auto v = p->p.outstanding_list();
         *n = (int64_t)v.size();
         for (int64_t k = 0; k < std::min<int64_t>(cap, *n); ++k) out[k] = v[(size_t)k];
+    });
+}
+int sp_pred_predict_batches_in(sp_pred *p, uint64_t current_iv, uint64_t leeway, int32_t depth,
+                               const int64_t *outstanding, int64_t n_out, sp_prediction *out, int32_t cap,
+                               int32_t *n) {
+    return guarded([&] {
+        std::unordered_set<int64_t> outs(outstanding, outstanding + (n_out > 0 ? n_out : 0));
+        auto v = p->p.predict_batches(current_iv, leeway, depth, &outs);
+        *n = (int32_t)v.size();
+        for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k)
+            out[k] = sp_prediction{v[(size_t)k].block, v[(size_t)k].iv, v[(size_t)k].leeway, v[(size_t)k].batch, 0};
+    });
+}
+int sp_pred_script(sp_pred *p, const sp_prediction *preds, int32_t n, const int64_t *outstanding, int64_t n_out) {
+    return guarded([&] {
+        std::vector<Prediction> v;
+        for (int32_t k = 0; k < n; ++k) v.push_back({preds[k].block, preds[k].predicted_iv, preds[k].leeway, preds[k].batch});
+        p->p.script(std::move(v), std::vector<int64_t>(outstanding, outstanding + (n_out > 0 ? n_out : 0)));
+    });
+}
+int64_t sp_pred_event_count(sp_pred *p) { return (int64_t)p->p.events().size(); }
+int sp_pred_event(sp_pred *p, int64_t i, int32_t *kind, int64_t *value) {
+    if (i < 0 || i >= (int64_t)p->p.events().size()) {
+        g_err = "event " + std::to_string(i);
+        return SP_EKEY;
+    }
+    *kind = p->p.events()[(size_t)i].kind;
+    *value = p->p.events()[(size_t)i].a;
+    return SP_OK;
+}
+int sp_pred_in_batch(sp_pred *p, int64_t i, int64_t *blocks, int32_t cap, int32_t *n) {
+    return guarded([&] {
+        if (i < 0 || i >= (int64_t)p->p.in_batch_count()) throw KeyErr("in-batch " + std::to_string(i));
+        const auto &b = p->p.in_batch((size_t)i);
+        *n = (int32_t)b.size();
+        for (int32_t k = 0; k < std::min<int32_t>(cap, *n); ++k) blocks[k] = b[(size_t)k];
     });
 }
 int64_t sp_pred_in_batch_count(sp_pred *p) { return (int64_t)p->p.in_batch_count(); }
@@ -3023,6 +3066,9 @@ int sp_pipe_drain_decrypts(sp_pipe *p) {
 }
 int sp_pipe_finish(sp_pipe *p) {
     return guarded([&] { p->e->finish(); });
+}
+int sp_pipe_audit(sp_pipe *p) {
+    return guarded([&] { p->e->audit(); });
 }
 int sp_pipe_finish_observable(sp_pipe *p) {
     return guarded([&] { p->e->finish(false); });
@@ -3114,6 +3160,17 @@ int sp_pipe_sent_log(sp_pipe *p, int32_t dir, int64_t from, sp_sent *out, int64_
     return SP_OK;
 }
 int64_t sp_pipe_record_count(sp_pipe *p) { return (int64_t)p->e->val.records.size(); }
+int sp_pipe_pending(sp_pipe *p, int64_t *ids, int64_t cap, int64_t *n) {
+    return guarded([&] {
+        *n = (int64_t)p->e->val.order.size();
+        int64_t k = 0;
+        for (int64_t id : p->e->val.order) {
+            if (k >= cap) break;
+            ids[k++] = id;
+        }
+    });
+}
+int64_t sp_pipe_pending_at_iv(sp_pipe *p, uint64_t iv) { return p->e->val.pending_at_iv(iv); }
 int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out) {
     Validator &v = p->e->val;
     if (id < 1 || id > (int64_t)v.records.size()) {
@@ -3156,6 +3213,74 @@ int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t
     if (bytes_h2d) *bytes_h2d = p->e->plane.bytes_h2d;
     if (bytes_d2h) *bytes_d2h = p->e->plane.bytes_d2h;
     if (launches) *launches = p->e->plane.launches;
+    return SP_OK;
+}
+
+
+// ---- standalone validator (validator.Validator, validator.py:90-236) -------------------------
+int sp_val_create(uint64_t window, sp_val **out) {
+    if (!out) return SP_EINVAL;
+    return guarded([&] { *out = new sp_val(window); });
+}
+void sp_val_destroy(sp_val *v) { delete v; }
+int sp_val_label(sp_val *v, uint64_t base, uint64_t len, uint64_t iv, uint64_t span, int64_t block_id, int64_t *id) {
+    return guarded([&] {
+        if (span < 1) throw ValueErr("a record spans at least one counter");
+        PVec<uint64_t> lens;
+        for (uint64_t k = 0; k < span; ++k) lens.push_back(0);
+        *id = v->v.label(PVec<MsgP>(), std::move(lens), base, len, iv, block_id);
+    });
+}
+int sp_val_validate(sp_val *v, uint64_t base, uint64_t len, uint64_t current_iv, int32_t *verdict, int64_t *record_id) {
+    return guarded([&] {
+        int64_t rid = -1;
+        *verdict = v->v.validate(base, len, current_iv, rid);
+        *record_id = rid;
+    });
+}
+int sp_val_commit(sp_val *v, int64_t id) {
+    return guarded([&] {
+        if (id < 1 || id >= v->v.next_id) throw KeyErr(std::to_string(id));
+        v->v.commit(id);
+    });
+}
+int sp_val_invalidate(sp_val *v, int64_t id) {
+    return guarded([&] {
+        if (id < 1 || id >= v->v.next_id) throw KeyErr(std::to_string(id));
+        v->v.invalidate(id);
+    });
+}
+int sp_val_write_fault(sp_val *v, int64_t owner) {
+    return guarded([&] { v->v.on_write_fault(owner); });
+}
+int64_t sp_val_pending_at_iv(sp_val *v, uint64_t iv) { return v->v.pending_at_iv(iv); }
+int32_t sp_val_has_pending_range(sp_val *v, uint64_t base, uint64_t len) { return v->v.has_pending_range(base, len) ? 1 : 0; }
+int sp_val_invalidate_pending_below(sp_val *v, uint64_t iv, int64_t *n) {
+    return guarded([&] { *n = v->v.invalidate_pending_below(iv); });
+}
+int sp_val_pending(sp_val *v, int64_t *ids, int64_t cap, int64_t *n) {
+    return guarded([&] {
+        *n = (int64_t)v->v.order.size();
+        int64_t k = 0;
+        for (int64_t id : v->v.order) {
+            if (k >= cap) break;
+            ids[k++] = id;
+        }
+    });
+}
+int64_t sp_val_record_count(sp_val *v) { return (int64_t)v->v.records.size(); }
+int sp_val_record(sp_val *v, int64_t id, sp_record *out) {
+    if (id < 1 || id > (int64_t)v->v.records.size()) {
+        g_err = "no record " + std::to_string(id);
+        return SP_EKEY;
+    }
+    const Record &r = v->v.rec(id);
+    *out = sp_record{r.id, r.base, r.len, r.iv, r.span(), r.block_id, (int32_t)r.state, 0};
+    return SP_OK;
+}
+int sp_val_counters(sp_val *v, int64_t out[6]) {
+    for (int k = 0; k < 5; ++k) out[k] = v->v.counters[k];
+    out[5] = v->v.evicted;
     return SP_OK;
 }
 

@@ -95,20 +95,48 @@ class Predictor {
         return classify(size, cfg);
     }
 
-    bool is_outstanding(int64_t b) const { return out_pos_.count(b) != 0; }
+    bool is_outstanding(int64_t b) const { return scripted_ ? script_out_.count(b) != 0 : out_pos_.count(b) != 0; }
     // outstanding blocks in swap-out order (== the reference's stack)
     const std::vector<int64_t>& outstanding_in_order() const { return stack_; }
     size_t in_batch_count() const { return in_batches_.size(); }
 
+    // Event log of SwapHistory.events (predictor.py:128-150): kind 0 = swap
+    // out (a = block), 1 = swap-in batch (a = index into the in-batches),
+    // 2 = sync.
+    struct Event {
+        int32_t kind;
+        int64_t a;
+    };
+    const std::vector<Event>& events() const { return events_; }
+
+    // Scripted mode: a fixed prediction schedule handed out once, a fixed
+    // outstanding set, observations ignored (the reference's scenario mock,
+    // cli.py:241-259 _ScriptedPredictor).
+    void script(std::vector<Prediction> preds, std::vector<int64_t> outstanding) {
+        scripted_ = true;
+        script_ = std::move(preds);
+        script_out_ = std::unordered_set<int64_t>(outstanding.begin(), outstanding.end());
+    }
+    bool scripted() const { return scripted_; }
+    std::vector<int64_t> outstanding_list() const {
+        if (!scripted_) return stack_;
+        std::vector<int64_t> v(script_out_.begin(), script_out_.end());
+        std::sort(v.begin(), v.end());
+        return v;
+    }
+
     void observe_swap_out(int64_t block) {
+        if (scripted_) return;
         if (is_outstanding(block))
             throw UnknownBlockErr("block " + std::to_string(block) + " is already swapped out");
         out_pos_.insert(block);
         stack_.push_back(block);
         open_.push_back(block);
+        events_.push_back({0, block});
     }
 
     void observe_swap_in(const std::vector<int64_t>& blocks_in) {
+        if (scripted_) return;
         std::vector<int64_t> batch(blocks_in);
         std::sort(batch.begin(), batch.end());
         batch.erase(std::unique(batch.begin(), batch.end()), batch.end());
@@ -121,6 +149,7 @@ class Predictor {
             for (size_t i = 0; i < missing.size(); ++i) m += (i ? ", " : "") + std::to_string(missing[i]);
             throw UnknownBlockErr(m + "]");
         }
+        events_.push_back({1, (int64_t)in_batches_.size()});
         in_batches_.push_back(intern(batch));
         std::unordered_set<int64_t> bs(batch.begin(), batch.end());
         for (int64_t b : batch) out_pos_.erase(b);
@@ -158,7 +187,12 @@ class Predictor {
         }
     }
 
-    void observe_sync() { close_group(); }
+    void observe_sync() {
+        if (scripted_) return;
+        events_.push_back({2, 0});
+        close_group();
+    }
+    const std::vector<int64_t>& in_batch(size_t i) const { return batch_of(in_batches_.at(i)); }
 
     Hypothesis recognize() {
         int64_t n = (int64_t)in_batches_.size();
@@ -182,9 +216,18 @@ class Predictor {
         return h;
     }
 
-    // predictor.py:252-297 (stateful facade 365-370)
-    std::vector<Prediction> predict_batches(uint64_t current_iv, uint64_t leeway, int depth) {
+    // predictor.py:252-297 (stateful facade 365-370).  `outstanding`, when
+    // given, replaces the history's outstanding set in the two places the
+    // reference's free function takes it as a parameter (the REPETITIVE
+    // subset test and the counter assignment).
+    std::vector<Prediction> predict_batches(uint64_t current_iv, uint64_t leeway, int depth,
+                                            const std::unordered_set<int64_t>* outstanding = nullptr) {
         std::vector<Prediction> out;
+        if (scripted_) {
+            out.swap(script_);  // handed out once
+            return out;
+        }
+        auto is_out = [&](int64_t b) { return outstanding ? outstanding->count(b) != 0 : is_outstanding(b); };
         Hypothesis h = recognize();
         if (h.kind == PK_UNKNOWN) return out;
         std::vector<std::vector<int64_t>> batches;
@@ -193,7 +236,7 @@ class Predictor {
                 const auto& nxt = batch_of(h.cycle[(size_t)((h.phase + i) % (int64_t)h.cycle.size())]);
                 bool sub = true;
                 for (int64_t b : nxt)
-                    if (!is_outstanding(b)) { sub = false; break; }
+                    if (!is_out(b)) { sub = false; break; }
                 if (!sub) break;
                 batches.push_back(nxt);
             }
@@ -215,7 +258,7 @@ class Predictor {
         for (size_t bi = 0; bi < batches.size(); ++bi) {
             std::vector<Prediction> preds;
             for (int64_t b : batches[bi]) {
-                if (!is_outstanding(b)) return out;
+                if (!is_out(b)) return out;
                 preds.push_back({b, iv, leeway, (int32_t)bi});
                 ++iv;
             }
@@ -278,6 +321,10 @@ class Predictor {
         return false;
     }
 
+    std::vector<Event> events_;
+    bool scripted_ = false;
+    std::vector<Prediction> script_;
+    std::unordered_set<int64_t> script_out_;
     std::unordered_set<int64_t> out_pos_;
     std::vector<int64_t> stack_;
     std::vector<int64_t> open_;

@@ -42,10 +42,10 @@ class ReplayConfig:
     fill: str = "seeded"
     reference_compat: bool = True
     window_aware: bool | None = None  # EngineConfig.window_aware (None: on iff reference_compat is off)
-    # "python": engine.Engine over devplane.GpuPlane; "native": libsppipe
-    # (native_engine.NativeEngine), dispatching the whole trace in one
-    # sp_pipe_replay call unless `native_dispatch` is "python" (per event)
-    engine: str = "python"
+    # the engine is libsppipe (engine.Engine); the whole trace is dispatched
+    # in one sp_pipe_replay call unless `native_dispatch` is "python" (one
+    # Engine call per event, the reference driver's shape)
+    engine: str = "native"
     native_dispatch: str = "replay"
     reserve_bytes: int = 0
 
@@ -96,21 +96,16 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
     cpu, gpu = new_channel(seed=config.seed)
     pconf = PredictorConfig() if config.predictor_chunk_bytes is None else \
         PredictorConfig(chunk_bytes=config.predictor_chunk_bytes)
-    native = config.engine == "native"
+    if config.engine != "native":
+        raise ValueError("the only engine is libsppipe (engine='native')")
     spec_on = config.system == "specpipe"
     econf = EngineConfig(
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
         record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat,
         window_aware=config.window_aware)
-    if native:
-        from .native_engine import NativeEngine, NativePredictor
-
-        predictor = NativePredictor(header.profile, pconf)
-        engine = NativeEngine(memory, cpu, gpu, predictor, econf, reserve_bytes=config.reserve_bytes)
-    else:
-        predictor = Predictor(header.profile, pconf)
-        engine = Engine(memory, cpu, gpu, predictor, econf)
+    predictor = Predictor(header.profile, pconf)
+    engine = Engine(memory, cpu, gpu, predictor, econf, reserve_bytes=config.reserve_bytes)
     blocks = {}
     for spec in header.blocks:
         if spec.resident == "cpu":
@@ -120,7 +115,7 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
         else:
             block = memory.block(spec.id) if reuse else memory.alloc(spec.kind, spec.nbytes)
             if config.plane == "gpu":
-                dev = _device_bytes(spec.nbytes) if native else engine.plane.new_device_buffer(spec.nbytes)
+                dev = _device_bytes(spec.nbytes)
                 if config.fill == "fast":
                     _fast_random(dev, spec.content_seed)
                 else:
@@ -129,12 +124,19 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
                     dev.copy_(torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)))
                 engine.seed_device(block.id, dev)
             else:
-                from .devplane import _DryPayload
-
-                engine.seed_device(block.id, _DryPayload(spec.nbytes) if native else
-                                   engine.plane.new_device_buffer(spec.nbytes))
+                engine.seed_device(block.id, _DryPayload(spec.nbytes))
         blocks[spec.id] = (block, classify(spec.nbytes, header.profile, pconf))
     return engine, blocks
+
+
+class _DryPayload:
+    """Device content of the dry plane: a size, no bytes."""
+
+    def __init__(self, n: int) -> None:
+        self.n = n
+
+    def numel(self) -> int:
+        return self.n
 
 
 def _device_bytes(n: int):
@@ -147,10 +149,7 @@ def _drain(engine, config: ReplayConfig) -> None:
     """Issue and finish all device work queued so far (clock boundaries)."""
     if config.plane != "gpu":
         return
-    if config.engine == "native":
-        engine.flush(wait=True)
-    else:
-        engine.plane.finish()
+    engine.flush(wait=True)
 
 
 _EV_CODES = {"h2d": 2, "d2h": 3}
@@ -159,7 +158,7 @@ _EV_CODES = {"h2d": 2, "d2h": 3}
 def encode_events(trace: Trace, blocks: dict, config: ReplayConfig, start: int = 0, stop: int | None = None):
     """Trace events -> sp_event tuples + payload bytes (small I/O and app
     writes, generated exactly as the per-event driver does)."""
-    from .native_engine import _CLASS
+    from .engine import _CLASS
 
     events, payload = [], bytearray()
     io_index = sum(1 for e in trace.events[:start] if isinstance(e, SmallIoEvent))
@@ -236,7 +235,7 @@ def run_engine(trace: Trace, config: ReplayConfig = ReplayConfig(), catch: bool 
 
     segments = None
     observable = None
-    if config.engine == "native" and config.native_dispatch == "replay":
+    if config.native_dispatch == "replay":
         # trace -> sp_event arrays before the clock starts (trace loading, not engine work)
         cut = measure_from if measure_from else 0
         segments = [engine.encode(*encode_events(trace, blocks, config, 0, cut))] if cut else []
@@ -312,71 +311,6 @@ def run_plain_native(trace: Trace, config: ReplayConfig = ReplayConfig(), memory
     return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
 
 
-def run_plain(trace: Trace, seed: int = 0, fill: str = "seeded", measure_from: int = 0,
-              memory: HostMemory | None = None) -> ReplayResult:
-    """NoCc on the GPU: the same swaps as plain pinned copies, no crypto."""
-    import torch
-
-    cfg = ReplayConfig(fill=fill)
-    if memory is None:
-        memory = prepare_memory(trace, cfg)
-    else:
-        memory.reset_runtime_state()
-    dev = torch.device("cuda", torch.cuda.current_device())
-    from .devplane import device_streams
-
-    s_h2d, s_d2h = device_streams(dev, 2)
-    blocks, device_mem = {}, {}
-    for spec in trace.header.blocks:
-        blocks[spec.id] = memory.block(spec.id)
-        if spec.resident != "cpu":
-            d = torch.empty(spec.nbytes, dtype=torch.uint8, device=dev)
-            if fill == "fast":
-                _fast_random(d, spec.content_seed)
-            else:
-                d.copy_(torch.from_numpy(random_bytes(spec.content_seed, spec.nbytes)))
-            device_mem[spec.id] = d
-    torch.cuda.synchronize()
-    pending_in: list = []
-    host_ready: dict = {}
-    t0 = time.perf_counter()
-    for k, ev in enumerate(trace.events):
-        if k == measure_from and k:
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-        if isinstance(ev, SwapInRequest):
-            b = blocks[ev.block]
-            landed = host_ready.pop(ev.block, None)
-            if landed is not None:  # the block's last swap-out must land before it is read again
-                s_h2d.wait_event(landed)
-            with torch.cuda.stream(s_h2d):
-                d = torch.empty(b.len, dtype=torch.uint8, device=dev)
-                d.copy_(b.pinned if b.pinned is not None else torch.from_numpy(b.data), non_blocking=True)
-            device_mem[ev.block] = d
-            pending_in.append(d)
-        elif isinstance(ev, SwapOut):
-            b = blocks[ev.block]
-            d = device_mem.pop(ev.block)
-            s_d2h.wait_stream(s_h2d)
-            with torch.cuda.stream(s_d2h):
-                (b.pinned if b.pinned is not None else torch.from_numpy(b.data)).copy_(d, non_blocking=True)
-                d.record_stream(s_d2h)
-                host_ready[ev.block] = torch.cuda.Event()
-                host_ready[ev.block].record(s_d2h)
-        elif isinstance(ev, SyncEvent):
-            # like the engine, the batch boundary orders the device side only
-            # (later swap-outs wait on the swap-in stream); the host runs on
-            pending_in.clear()
-        elif isinstance(ev, SmallIoEvent):
-            payload = torch.frombuffer(bytearray(ev.size), dtype=torch.uint8)
-            with torch.cuda.stream(s_h2d if ev.direction == "h2d" else s_d2h):
-                if ev.direction == "h2d":
-                    payload.to(dev, non_blocking=True)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
-
-
 def main(argv: list[str] | None = None) -> int:
     """Replay reference-format JSONL traces (workload.py:188-260 schema v1)
     on the B200: one JSON line per (trace, system) with measured swap GB/s,
@@ -391,8 +325,9 @@ def main(argv: list[str] | None = None) -> int:
     ap.add_argument("trace", nargs="+", help="JSONL trace file(s) in the reference schema")
     ap.add_argument("--system", action="append", choices=["specpipe", "synccc", "nocc"],
                     help="systems to run (default: all three)")
-    ap.add_argument("--engine", choices=["native", "python"], default="native")
     ap.add_argument("--plane", choices=["gpu", "dry"], default="gpu")
+    ap.add_argument("--dispatch", choices=["replay", "python"], default="replay",
+                    help="one sp_pipe_replay call per trace, or one Engine call per event")
     ap.add_argument("--window", type=int, default=64)
     ap.add_argument("--leeway", type=int, default=8)
     ap.add_argument("--depth", type=int, default=1)
@@ -404,16 +339,16 @@ def main(argv: list[str] | None = None) -> int:
     for path in args.trace:
         trace = load_trace(path)
         for system in systems:
-            cfg = ReplayConfig(system="specpipe" if system == "nocc" else system, engine=args.engine,
+            cfg = ReplayConfig(system="specpipe" if system == "nocc" else system,
                                plane=args.plane, window=args.window, leeway=args.leeway, depth=args.depth,
                                seed=args.seed, record_stream=False, fill="fast" if args.plane == "gpu" else "seeded",
-                               reference_compat=not args.fix_c2)
+                               reference_compat=not args.fix_c2, native_dispatch=args.dispatch)
             memory = prepare_memory(trace, cfg)
-            row = {"trace": str(path), "system": system, "engine": args.engine, "plane": args.plane,
+            row = {"trace": str(path), "system": system, "engine": "native", "plane": args.plane,
                    "swap_bytes": trace.swap_bytes(), "events": len(trace.events)}
             if system == "nocc":
-                if args.plane != "gpu" or args.engine != "native":
-                    row["error"] = "nocc replays need --engine native --plane gpu"
+                if args.plane != "gpu":
+                    row["error"] = "nocc replays need --plane gpu"
                 else:
                     runs = [run_plain_native(trace, cfg, memory=memory) for _ in range(args.reps + 1)][1:]
                     row["swap_gbs"] = round(max(r.swap_gbs for r in runs), 3)

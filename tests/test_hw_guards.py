@@ -18,18 +18,17 @@ SCRIPT = textwrap.dedent('''
     from paper_2411_03357_b200.channel import new_channel
     from paper_2411_03357_b200.engine import CopyRequest, Engine, EngineConfig
     from paper_2411_03357_b200.memory import HostMemory, ModelLayer, prng_fill
-    from paper_2411_03357_b200.predictor import Prediction, TransferClass
+    from paper_2411_03357_b200.predictor import Prediction, Predictor, TransferClass
     from paper_2411_03357_b200.validator import RecordState
-    from tests.test_engine_scenarios import ScriptedPredictor
 
     mem = HostMemory(pinned=False, hw_guards=True)
     cpu, gpu = new_channel(seed=1)
     b = mem.alloc(ModelLayer(1), 256 * 1024, prng_fill(3))
     c = mem.alloc(ModelLayer(2), 256 * 1024, prng_fill(4))
-    eng = Engine(mem, cpu, gpu, ScriptedPredictor([[Prediction(b.id, 0, 0), Prediction(c.id, 1, 0)]], {b.id, c.id}),
+    eng = Engine(mem, cpu, gpu, Predictor.scripted([[Prediction(b.id, 0, 0), Prediction(c.id, 1, 0)]], {b.id, c.id}),
                  EngineConfig(leeway=0, plane="dry"))
-    eng.speculate_tick()
-    eng._complete_spec_tasks()
+    eng.speculate_tick()   # queue the encrypt-ahead
+    eng.speculate_tick()   # the next entry point seals, labels and guards it
     assert guards.active() == 2, guards.active()
     rec_b = next(r for r in eng.validator.records.values() if r.block_id == b.id)
     # 1) a direct store (numpy, no HostMemory.write) into b's guarded pages
@@ -92,16 +91,15 @@ NATIVE_SCRIPT = textwrap.dedent('''
     sys.path.insert(0, %r)
     from paper_2411_03357_b200 import guards
     from paper_2411_03357_b200.channel import new_channel
-    from paper_2411_03357_b200.engine import CopyRequest, EngineConfig
+    from paper_2411_03357_b200.engine import CopyRequest, Engine, EngineConfig
     from paper_2411_03357_b200.memory import HostMemory, ModelLayer, prng_fill
-    from paper_2411_03357_b200.native_engine import NativeEngine, NativePredictor
-    from paper_2411_03357_b200.predictor import ModelProfile, TransferClass
+    from paper_2411_03357_b200.predictor import ModelProfile, Predictor, TransferClass
 
     W = TransferClass.MODEL_WEIGHTS
     mem = HostMemory(pinned=PINNED, hw_guards=True)
     cpu, gpu = new_channel(seed=1)
-    pred = NativePredictor(ModelProfile("m", 256 * 1024, 4096))
-    eng = NativeEngine(mem, cpu, gpu, pred, EngineConfig(leeway=0, plane=PLANE))
+    pred = Predictor(ModelProfile("m", 256 * 1024, 4096))
+    eng = Engine(mem, cpu, gpu, pred, EngineConfig(leeway=0, plane=PLANE))
     blocks = [mem.alloc(ModelLayer(i), 256 * 1024, prng_fill(i)) for i in range(4)]
     for b in blocks:
         pred.observe_swap_out(b.id)
@@ -126,7 +124,7 @@ NATIVE_SCRIPT = textwrap.dedent('''
 ''' % ROOT)
 
 
-def test_native_hw_guard_invalidates_on_direct_store():
+def test_hw_guard_from_learned_prediction():
     script = NATIVE_SCRIPT.replace("PINNED", "False").replace("PLANE", '"dry"')
     out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=120, cwd=ROOT)
     assert out.returncode == 0, out.stdout + out.stderr
@@ -134,7 +132,7 @@ def test_native_hw_guard_invalidates_on_direct_store():
 
 
 @pytest.mark.gpu
-def test_native_hw_guard_gpu():
+def test_hw_guard_from_learned_prediction_gpu():
     script = NATIVE_SCRIPT.replace("PINNED", "True").replace("PLANE", '"gpu"')
     out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stdout + out.stderr

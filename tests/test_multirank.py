@@ -28,7 +28,7 @@ def _worker(rank, world, port, out):
     # each rank: its own channel seed and its own trace, dry data plane
     tr = workload.gen_offload_trace(4, [1, 2, 3, 4], 2, layer_bytes=4096, seed=rank)
     res = run_engine(tr, ReplayConfig(seed=rank, plane="dry"))
-    nat = run_engine(tr, ReplayConfig(seed=rank, plane="dry", engine="native"))  # libsppipe per rank
+    nat = run_engine(tr, ReplayConfig(seed=rank, plane="dry", native_dispatch="python"))  # per-event calls
     assert nat.engine.report() == res.engine.report()
     key = res.engine.cpu.key.key_bytes
     local = float(10 + rank)

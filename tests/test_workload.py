@@ -60,9 +60,9 @@ def test_opt_shapes():
 
 
 def test_jsonl_replay_cli_dry(tmp_path, capsys):
-    """Reference-format JSONL traces replay through either engine from the
-    command line (python -m paper_2411_03357_b200.replay); both engines
-    report the same decisions."""
+    """Reference-format JSONL traces replay through libsppipe from the
+    command line (python -m paper_2411_03357_b200.replay), dispatched as one
+    sp_pipe_replay call or event by event: the same decisions."""
     import json
 
     from paper_2411_03357_b200 import workload
@@ -72,8 +72,7 @@ def test_jsonl_replay_cli_dry(tmp_path, capsys):
     path = tmp_path / "kv.jsonl"
     workload.save_trace(tr, path)
     rows = []
-    for engine in ("native", "python"):
-        assert main([str(path), "--plane", "dry", "--engine", engine, "--system", "specpipe"]) == 0
+    for dispatch in ("replay", "python"):
+        assert main([str(path), "--plane", "dry", "--dispatch", dispatch, "--system", "specpipe"]) == 0
         rows.append(json.loads(capsys.readouterr().out.strip().splitlines()[-1]))
-    strip = lambda r: {k: v for k, v in r.items() if k != "engine"}  # noqa: E731
-    assert strip(rows[0]) == strip(rows[1]) and rows[0]["error"] is None and rows[0]["data_msgs"] > 0
+    assert rows[0] == rows[1] and rows[0]["error"] is None and rows[0]["data_msgs"] > 0

@@ -10,6 +10,8 @@
 
 #include "spgcm.h"
 
+__global__ void k_empty() {}
+
 int main() {
     uint8_t key[32];
     for (int i = 0; i < 32; ++i) key[i] = (uint8_t)i;
@@ -26,12 +28,25 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    {  // launch floor: an empty kernel back to back
+        cudaEvent_t a0, b0;
+        cudaEventCreate(&a0);
+        cudaEventCreate(&b0);
+        for (int w = 0; w < 100; ++w) k_empty<<<1, 32, 0, s>>>();
+        cudaEventRecord(a0, s);
+        for (int r = 0; r < 2000; ++r) k_empty<<<1, 32, 0, s>>>();
+        cudaEventRecord(b0, s);
+        cudaEventSynchronize(b0);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a0, b0);
+        printf("%-18s %-16s %7.2f us/launch\n", "empty kernel", "back-to-back", ms * 1e3 / 2000);
+    }
     struct Case {
         const char *name;
         int n;
         size_t size;
     } cases[] = {{"1 NOP (1 B)", 1, 1},       {"8 NOPs", 8, 1},           {"1 x 2 KiB token", 1, 2048},
-                 {"1 x 224 KiB KV", 1, 229376}, {"4 x 224 KiB KV", 4, 229376}, {"32 x 224 KiB KV", 32, 229376},
+                 {"1 x 16 KiB", 1, 16384}, {"1 x 64 KiB", 1, 65536}, {"1 x 224 KiB KV", 1, 229376}, {"4 x 224 KiB KV", 4, 229376}, {"32 x 224 KiB KV", 32, 229376},
                  {"1 x 1 MiB", 1, 1 << 20}};
     for (auto &c : cases) {
         std::vector<sp_desc> d(c.n);
