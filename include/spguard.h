@@ -16,7 +16,16 @@
  *
  * Pages only partially covered by a guard are left writable (page
  * granularity must not create faults the byte-precise reference would not
- * raise); the byte-precise HostMemory.write check still covers them.
+ * raise) unless the caller states that it owns the rest of that page
+ * (spg_protect_ex flags: page-aligned, page-padded pinned blocks guarded
+ * from their first / to their last byte).  Guards whose bytes are not all
+ * under protection are counted (spg_uncovered); the byte-precise
+ * HostMemory.write check still covers them.
+ *
+ * Concurrency: a store that faults while another thread lifts the same
+ * guard (a concurrent fault, or spg_release on commit/invalidate) retries
+ * instead of reaching the previous SIGSEGV handler: the handler also matches
+ * ranges that are being lifted and a ring of recently released ranges.
  */
 #ifndef SPGUARD_H_
 #define SPGUARD_H_
@@ -39,6 +48,12 @@ int spg_init(void);
 /* Protect the whole pages inside [addr, addr+len) for `owner` (record id).
  * Returns SPG_OK even if no whole page is inside (nothing to protect). */
 int spg_protect(const void *addr, size_t len, int64_t owner);
+/* flags for spg_protect_ex: the caller exclusively owns the rest of the
+ * partial page before addr (HEAD) / after addr+len (TAIL), so that page is
+ * protected too. */
+#define SPG_HEAD_OWNED 1
+#define SPG_TAIL_OWNED 2
+int spg_protect_ex(const void *addr, size_t len, int64_t owner, int flags);
 /* Lift the guard of `owner` (commit / invalidate / eviction). */
 int spg_release(int64_t owner);
 /* Pop up to `cap` faulted owners into `out`; returns how many. */
@@ -47,6 +62,8 @@ int spg_drain(int64_t *out, int cap);
 int spg_active(void);
 uint64_t spg_faults(void);
 int spg_errno(void);
+/* Guards installed with part of their byte range left writable. */
+uint64_t spg_uncovered(void);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,12 @@ extern "C" {
 #define SP_KIND_LAYER 0
 #define SP_KIND_KV 1
 #define SP_KIND_SMALL 2
+/* sp_pipe_register_block kind flag: the host buffer starts on a page
+ * boundary and its last page belongs to no other object (pinned slab
+ * blocks are page-aligned and page-padded), so hardware write guards
+ * covering the block's first / last byte protect the partial pages too
+ * (spg_protect_ex). */
+#define SP_BLOCK_PAGE_OWNED 0x100
 
 /* Verdicts (validator.VerdictKind); SP_VERDICT_NONE for SMALL_IO submits. */
 #define SP_VERDICT_HIT 0
@@ -104,7 +110,7 @@ typedef struct sp_prediction {
     uint64_t predicted_iv;
     uint64_t leeway;
     int32_t batch; /* index of the predicted batch this entry belongs to */
-    int32_t reserved;
+    int32_t reserved; /* sp_pred_script: round (the predict call that hands it out); else 0 */
 } sp_prediction;
 
 typedef struct sp_decision {
@@ -133,8 +139,9 @@ int sp_pred_predict_batches_in(sp_pred *p, uint64_t current_iv, uint64_t leeway,
                                const int64_t *outstanding, int64_t n_out, sp_prediction *out, int32_t cap,
                                int32_t *n);
 /* Scripted mode (the scenario mock of cli.py:241-259): predict_batches hands
- * out `preds` once (grouped by their batch field), the outstanding set is
- * `outstanding`, observations are ignored. */
+ * out `preds` once (grouped by their batch field; entries with reserved = r
+ * on the r-th call), the outstanding set is `outstanding`, observations are
+ * ignored. */
 int sp_pred_script(sp_pred *p, const sp_prediction *preds, int32_t n, const int64_t *outstanding, int64_t n_out);
 /* SwapHistory.events (predictor.py:128-150): kind 0 swap-out (value = block),
  * 1 swap-in (value = index of its batch in the in-batches), 2 sync. */
@@ -147,6 +154,10 @@ int64_t sp_pred_decision_count(sp_pred *p);
 int sp_pred_decision(sp_pred *p, int64_t i, sp_decision *out);
 
 /* engine.EngineConfig (engine.py:78-92) + B200 data-plane knobs. */
+#define SP_WINDOW_AWARE_AUTO 0
+#define SP_WINDOW_AWARE_ON 1
+#define SP_WINDOW_AWARE_OFF 2
+
 typedef struct sp_pipe_config {
     uint32_t window;      /* 64 */
     uint32_t leeway;      /* 8 */
@@ -162,11 +173,15 @@ typedef struct sp_pipe_config {
     uint8_t reference_compat; /* 1: reproduce defect C2; 0: OTF sends burn the record at their counter */
     uint8_t dry;              /* 1: no bytes, no device (schedule only) */
     uint8_t hw_guards;        /* 1: also mprotect guarded host pages (libspguard) */
-    uint8_t window_aware;     /* 1: speculate only whole predicted batches that fit the record window */
+    uint8_t window_aware;     /* SP_WINDOW_AWARE_*: speculate only whole predicted batches that fit the
+                                 record window; AUTO (0) = on iff reference_compat is 0, as Python's
+                                 EngineConfig(window_aware=None) */
     uint64_t initial_h2d_iv; /* cpu endpoint send_iv */
     uint64_t initial_d2h_iv; /* gpu endpoint send_iv */
     uint64_t batch_bytes;    /* flush a batched launch at this much payload (64 MiB) */
     uint64_t reserve_bytes;  /* device pool bytes reserved at create (0: grow on demand) */
+    uint64_t record_history; /* finished validator records kept (0: all, as the reference); older ones
+                                below the oldest pending record are forgotten at sync (long-running pipes) */
 } sp_pipe_config;
 
 typedef struct sp_action {
@@ -279,7 +294,8 @@ typedef struct sp_record {
     int32_t state;
     int32_t reserved;
 } sp_record;
-int64_t sp_pipe_record_count(sp_pipe *p);
+int64_t sp_pipe_record_count(sp_pipe *p);  /* ids labeled so far (1..count) */
+int64_t sp_pipe_record_first(sp_pipe *p);  /* oldest retained id (record_history) */
 int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out);
 /* Pending record ids in label order (validator.pending_records) and the
  * pending record holding counter iv (-1: none). */

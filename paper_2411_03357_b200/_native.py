@@ -102,7 +102,7 @@ SPPIPE_SYMBOLS = (
     "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
-    "sp_pipe_record_count", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
+    "sp_pipe_record_count", "sp_pipe_record_first", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
     "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
     "sp_val_create", "sp_val_destroy", "sp_val_label", "sp_val_validate", "sp_val_commit", "sp_val_invalidate",
     "sp_val_write_fault", "sp_val_pending_at_iv", "sp_val_has_pending_range", "sp_val_invalidate_pending_below", "sp_val_pending",
@@ -141,6 +141,7 @@ class SpPipeConfig(ctypes.Structure):
         ("dry", ctypes.c_uint8), ("hw_guards", ctypes.c_uint8), ("window_aware", ctypes.c_uint8),
         ("initial_h2d_iv", ctypes.c_uint64),
         ("initial_d2h_iv", ctypes.c_uint64), ("batch_bytes", ctypes.c_uint64), ("reserve_bytes", ctypes.c_uint64),
+        ("record_history", ctypes.c_uint64),
     ]
 
 
@@ -256,9 +257,9 @@ def load_sppipe() -> ctypes.CDLL:
         lib.sp_val_has_pending_range.restype = i32
         lib.sp_pipe_sent_count.argtypes = [vp, i32]
         lib.sp_pipe_sent_count.restype = i64
-        if hasattr(lib, "sp_pipe_record_count"):
-            lib.sp_pipe_record_count.argtypes = [vp]
-            lib.sp_pipe_record_count.restype = i64
+        for name in ("sp_pipe_record_count", "sp_pipe_record_first"):
+            getattr(lib, name).argtypes = [vp]
+            getattr(lib, name).restype = i64
         lib.sp_pipe_delivered_count.argtypes = [vp, i32]
         lib.sp_pipe_delivered_count.restype = i64
         for name in ("sp_pipe_send_iv", "sp_pipe_recv_iv"):

@@ -16,6 +16,7 @@
 
 #define SPG_MAX_GUARDS 4096
 #define SPG_RING 8192
+#define SPG_TOMB 1024  // recently lifted ranges (see handler)
 
 typedef struct {
     _Atomic uintptr_t lo;   // first protected page (0 = free slot)
@@ -33,7 +34,14 @@ static _Atomic uint32_t g_head = 0, g_tail = 0;  // head: next write, tail: next
 static struct sigaction g_prev;
 static _Atomic int g_inited = 0;
 static _Atomic int g_errno = 0;
+static _Atomic uint64_t g_uncovered = 0;  // guards whose byte range is not fully under protection
 static uintptr_t g_page = 4096;
+// Tombstones: ranges whose protection was lifted by spg_release.  A store
+// that faulted just before the lift may reach the handler after the slot
+// was cleared; finding its range here, the handler lets it retry on the
+// (now writable) page instead of treating the fault as foreign.
+static _Atomic uintptr_t g_tomb_lo[SPG_TOMB], g_tomb_hi[SPG_TOMB];
+static _Atomic uint32_t g_tomb_head = 0;
 
 static void lock(void) {
     int expected = 0;
@@ -49,12 +57,13 @@ static void ring_push(int64_t owner) {
 static void handler(int sig, siginfo_t *info, void *uctx) {
     const uintptr_t a = (uintptr_t)info->si_addr;
     int hit = 0;
+    // 1. an active guard covering the address: the first faulting thread
+    //    lifts it and records the owner
     for (int i = 0; i < SPG_MAX_GUARDS; ++i) {
         if (!atomic_load(&g_guards[i].active)) continue;
         const uintptr_t lo = atomic_load(&g_guards[i].lo), hi = atomic_load(&g_guards[i].hi);
         if (a >= lo && a < hi) {
             int one = 1;
-            // first faulting thread wins the guard; others just retry
             if (atomic_compare_exchange_strong(&g_guards[i].active, &one, 0)) {
                 mprotect((void *)lo, hi - lo, PROT_READ | PROT_WRITE);
                 ring_push(atomic_load(&g_guards[i].owner));
@@ -65,6 +74,18 @@ static void handler(int sig, siginfo_t *info, void *uctx) {
         }
     }
     if (hit) return;  // the faulting store retries on a writable page
+    // 2. a guard another thread (a concurrent fault, or spg_release) is
+    //    lifting right now: its slot is inactive but still holds the range;
+    //    the store retries and faults again until the mprotect has landed
+    for (int i = 0; i < SPG_MAX_GUARDS; ++i) {
+        const uintptr_t lo = atomic_load(&g_guards[i].lo), hi = atomic_load(&g_guards[i].hi);
+        if (lo && a >= lo && a < hi) return;
+    }
+    // 3. a range lifted by a release that has since cleared its slot
+    for (int i = 0; i < SPG_TOMB; ++i) {
+        const uintptr_t lo = atomic_load(&g_tomb_lo[i]), hi = atomic_load(&g_tomb_hi[i]);
+        if (lo && a >= lo && a < hi) return;
+    }
     // not ours: hand over to whoever was installed before us
     if (g_prev.sa_flags & SA_SIGINFO) {
         if (g_prev.sa_sigaction) { g_prev.sa_sigaction(sig, info, uctx); return; }
@@ -93,12 +114,15 @@ int spg_init(void) {
     return SPG_OK;
 }
 
-int spg_protect(const void *addr, size_t len, int64_t owner) {
-    if (!addr || !len) return SPG_EINVAL;
+int spg_protect_ex(const void *addr, size_t len, int64_t owner, int flags) {
+    if (!addr || !len || (flags & ~(SPG_HEAD_OWNED | SPG_TAIL_OWNED))) return SPG_EINVAL;
     if (!atomic_load(&g_inited) && spg_init() != SPG_OK) return SPG_ESYS;
     const uintptr_t a = (uintptr_t)addr;
-    const uintptr_t lo = (a + g_page - 1) & ~(g_page - 1);     // round the start up
-    const uintptr_t hi = (a + len) & ~(g_page - 1);            // round the end down
+    // whole pages inside the range; a partial head / tail page is included
+    // when the caller owns the rest of that page exclusively
+    const uintptr_t lo = (flags & SPG_HEAD_OWNED) ? a & ~(g_page - 1) : (a + g_page - 1) & ~(g_page - 1);
+    const uintptr_t hi = (flags & SPG_TAIL_OWNED) ? (a + len + g_page - 1) & ~(g_page - 1) : (a + len) & ~(g_page - 1);
+    if (lo > a || hi < a + len) atomic_fetch_add(&g_uncovered, 1u);
     if (hi <= lo) return SPG_OK;                                // no whole page inside
     lock();
     int slot = -1;
@@ -119,6 +143,8 @@ int spg_protect(const void *addr, size_t len, int64_t owner) {
     return SPG_OK;
 }
 
+int spg_protect(const void *addr, size_t len, int64_t owner) { return spg_protect_ex(addr, len, owner, 0); }
+
 int spg_release(int64_t owner) {
     lock();
     for (int i = 0; i < SPG_MAX_GUARDS; ++i) {
@@ -129,6 +155,11 @@ int spg_release(int64_t owner) {
                      atomic_load(&g_guards[i].hi) - atomic_load(&g_guards[i].lo), PROT_READ | PROT_WRITE);
             atomic_fetch_sub(&g_nactive, 1);
         }
+        // tombstone before the slot forgets the range (handler step 3)
+        const uint32_t t = atomic_fetch_add(&g_tomb_head, 1u) % SPG_TOMB;
+        atomic_store(&g_tomb_lo[t], 0);
+        atomic_store(&g_tomb_hi[t], atomic_load(&g_guards[i].hi));
+        atomic_store(&g_tomb_lo[t], atomic_load(&g_guards[i].lo));
         atomic_store(&g_guards[i].lo, 0);
         atomic_store(&g_guards[i].hi, 0);
     }
@@ -150,3 +181,4 @@ int spg_drain(int64_t *out, int cap) {
 int spg_active(void) { return atomic_load(&g_nactive); }
 uint64_t spg_faults(void) { return atomic_load(&g_faults); }
 int spg_errno(void) { return atomic_load(&g_errno); }
+uint64_t spg_uncovered(void) { return atomic_load(&g_uncovered); }

@@ -176,6 +176,7 @@ struct Block {
     int kind;
     uint8_t *host;
     uint8_t *host_dev = nullptr;  // device-accessible alias of a pinned host block (UVA), else null
+    bool page_owned = false;      // SP_BLOCK_PAGE_OWNED: whole pages, exclusively this block's
 };
 
 struct WriteGuard {
@@ -232,7 +233,11 @@ class HostMem {
         write_guards[owner] = WriteGuard{base, len, owner, true};
         if (hw) {
             auto bi = block_at(base, len);
-            if (bi.first->host && spg_protect(bi.first->host + bi.second, len, owner) != SPG_OK)
+            const Block &hb = *bi.first;
+            const int flags = hb.page_owned ? ((bi.second == 0 ? SPG_HEAD_OWNED : 0) |
+                                               (bi.second + len == hb.len ? SPG_TAIL_OWNED : 0))
+                                            : 0;
+            if (hb.host && spg_protect_ex(hb.host + bi.second, len, owner, flags) != SPG_OK)
                 throw std::runtime_error("spg_protect failed (errno " + std::to_string(spg_errno()) + ")");
         }
     }
@@ -363,7 +368,9 @@ class Validator {
     Validator(HostMem &m, uint64_t window) : mem(m), window(window) {}
     HostMem &mem;
     uint64_t window;
-    std::deque<Record> records;  // id i at index i-1
+    std::deque<Record> records;  // id i at index i - first_id
+    int64_t first_id = 1;        // oldest retained record (compact())
+    uint64_t history = 0;        // retained finished records (0: all, as the reference keeps them)
     int64_t next_id = 1;
     PUMap<RangeKey, int64_t, RangeHash> by_range, stale;
     PUMap<uint64_t, int64_t> by_iv;
@@ -372,7 +379,20 @@ class Validator {
     int64_t counters[5] = {0, 0, 0, 0, 0};
     int64_t evicted = 0;
 
-    Record &rec(int64_t id) { return records[(size_t)(id - 1)]; }
+    Record &rec(int64_t id) { return records[(size_t)(id - first_id)]; }
+    bool retained(int64_t id) const { return id >= first_id && id < next_id; }
+
+    // Forget finished records older than every pending one, beyond the last
+    // `history`: a long-running pipe's record list stays bounded (their
+    // payloads are already released; STALE verdicts keep only the range map).
+    void compact() {
+        if (!history || records.size() <= history + history / 2) return;
+        const int64_t oldest_pending = order.empty() ? next_id : *order.begin();
+        while (records.size() > history && records.front().id < oldest_pending) {
+            records.pop_front();
+            ++first_id;
+        }
+    }
 
     int64_t label(PVec<MsgP> chunks, PVec<uint64_t> lens, uint64_t base, uint64_t len, uint64_t iv,
                   int64_t block_id) {
@@ -453,7 +473,7 @@ class Validator {
         r.chunks.clear();  // device payloads go back to the pool
     }
     void on_write_fault(int64_t owner) {
-        if (owner >= 1 && owner < next_id && rec(owner).state == PENDING) invalidate(owner);
+        if (retained(owner) && rec(owner).state == PENDING) invalidate(owner);
     }
     std::vector<int64_t> pending_ids() const { return std::vector<int64_t>(order.begin(), order.end()); }
     int64_t pending_at_iv(uint64_t iv) const {
@@ -1441,6 +1461,7 @@ class Plane {
     }
     // Copies of one flush / batch: one cudaMemcpyBatchAsync (CUDA 12.8+)
     // instead of a call per copy; plain cudaMemcpyAsync where unsupported.
+    static constexpr size_t kMaxBatchCopies = 128;
     template <class F>
     void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
         if (!count) return;
@@ -1460,7 +1481,12 @@ class Plane {
             return !(e && e[0] == '0');
         }();
         const size_t count = sizes.size();
-        if (count > 1 && batch_ok) {
+        size_t done = 0;
+        // At most kMaxBatchCopies copies per cudaMemcpyBatchAsync call: on
+        // driver 580 / B200 a call carrying many H2D copies can fault the
+        // GPU (Xid 32, B200_PROFILING.md), so long flushes go out in chunks.
+        while (count - done > 1 && batch_ok) {
+            const size_t n = std::min(kMaxBatchCopies, count - done);
             cudaMemcpyAttributes attr;
             memset(&attr, 0, sizeof attr);
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
@@ -1469,15 +1495,18 @@ class Plane {
             attr.dstLocHint.type = h2d ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
             attr.dstLocHint.id = h2d ? device : 0;
             size_t idx = 0, fail_idx = SIZE_MAX;
-            cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), count, &attr, &idx, 1,
-                                                 &fail_idx, st);
-            if (e == cudaSuccess) return;
+            cudaError_t e = cudaMemcpyBatchAsync(dsts.data() + done, srcs.data() + done, sizes.data() + done, n,
+                                                 &attr, &idx, 1, &fail_idx, st);
+            if (e == cudaSuccess) {
+                done += n;
+                continue;
+            }
             if (fail_idx != SIZE_MAX || (e != cudaErrorNotSupported && e != cudaErrorInvalidValue))
                 ck(e, "cudaMemcpyBatchAsync");
             cudaGetLastError();
             batch_ok = false;  // driver without batch copies: per-copy path from now on
         }
-        for (size_t i = 0; i < count; ++i)
+        for (size_t i = done; i < count; ++i)
             ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
                "batched copy");
     }
@@ -2101,6 +2130,7 @@ class Engine {
     Engine(const sp_pipe_config &c, const uint8_t key[32], Predictor *p)
         : cfg(c), plane(c.dry != 0, key, c.batch_bytes ? c.batch_bytes : (64ull << 20), c.reserve_bytes), pred(p),
           val(mem, c.window) {
+        val.history = c.record_history;
         if (c.hw_guards) {
             if (spg_init() != SPG_OK) throw std::runtime_error("spg_init failed");
             mem.hw = true;
@@ -2442,6 +2472,7 @@ class Engine {
         auto flat = pred->predict_batches(send_iv[H2D], cfg.leeway, (int)cfg.depth);
         predicted_queue.clear();
         for (auto &p : flat) predicted_queue.push_back(p.block);
+        bool trimmed = false;
         if (cfg.window_aware) {
             // whole predicted batches only, while they fit the record window
             size_t keep = 0;
@@ -2451,6 +2482,7 @@ class Engine {
                 if (end > (size_t)cfg.window) break;
                 keep = end;
             }
+            trimmed = keep < flat.size();
             flat.resize(keep);
         }
         std::vector<int64_t> planned;
@@ -2471,6 +2503,11 @@ class Engine {
                 diverged = true;
                 break;
             }
+        // Window-aware trimming dropped predictions: pending records and
+        // queued tasks past the kept plan belong to an earlier plan (the
+        // prefix comparison above never sees them) and would hold window
+        // slots until sync expiry; discard them like any other replan.
+        if (trimmed && planned.size() > flat.size()) diverged = true;
         if (diverged) {
             int64_t n = discard_pipeline();
             counters[C_REPLANS]++;
@@ -2635,6 +2672,7 @@ class Engine {
         act(SP_ACT_SYNC_POINT);
         counters[C_SYNCS]++;
         speculate_tick();
+        val.compact();  // no suspended request refers to a record here
     }
 
     void drain_decrypts() {
@@ -2962,8 +3000,13 @@ int sp_pred_predict_batches_in(sp_pred *p, uint64_t current_iv, uint64_t leeway,
 int sp_pred_script(sp_pred *p, const sp_prediction *preds, int32_t n, const int64_t *outstanding, int64_t n_out) {
     return guarded([&] {
         std::vector<Prediction> v;
-        for (int32_t k = 0; k < n; ++k) v.push_back({preds[k].block, preds[k].predicted_iv, preds[k].leeway, preds[k].batch});
-        p->p.script(std::move(v), std::vector<int64_t>(outstanding, outstanding + (n_out > 0 ? n_out : 0)));
+        std::vector<int> rounds;
+        for (int32_t k = 0; k < n; ++k) {
+            v.push_back({preds[k].block, preds[k].predicted_iv, preds[k].leeway, preds[k].batch});
+            rounds.push_back(preds[k].reserved);
+        }
+        p->p.script(std::move(v), std::vector<int64_t>(outstanding, outstanding + (n_out > 0 ? n_out : 0)),
+                    std::move(rounds));
     });
 }
 int64_t sp_pred_event_count(sp_pred *p) { return (int64_t)p->p.events().size(); }
@@ -3002,7 +3045,17 @@ int sp_pipe_create(const sp_pipe_config *cfg, const uint8_t key[SP_KEY_BYTES], s
     return guarded([&] {
         auto p = new sp_pipe();
         try {
-            p->e.reset(new Engine(*cfg, key, &pred->p));
+            sp_pipe_config c = *cfg;
+            // tri-state window_aware: AUTO (0, a zero-initialised config)
+            // follows reference_compat exactly like Python's EngineConfig
+            // (window_aware=None: on iff the C2 fix is on)
+            if (c.window_aware > SP_WINDOW_AWARE_OFF) {
+                g_err = "window_aware must be SP_WINDOW_AWARE_AUTO, _ON or _OFF";
+                throw ValueErr(g_err);
+            }
+            c.window_aware = c.window_aware == SP_WINDOW_AWARE_AUTO ? (c.reference_compat ? 0 : 1)
+                                                                     : (c.window_aware == SP_WINDOW_AWARE_ON ? 1 : 0);
+            p->e.reset(new Engine(c, key, &pred->p));
         } catch (...) {
             delete p;
             throw;
@@ -3014,7 +3067,8 @@ void sp_pipe_destroy(sp_pipe *p) { delete p; }
 
 int sp_pipe_register_block(sp_pipe *p, int64_t id, uint64_t base, uint64_t len, int32_t kind, void *host) {
     return guarded([&] {
-        Block b{id, base, len, kind, static_cast<uint8_t *>(host)};
+        Block b{id, base, len, kind & 0xff, static_cast<uint8_t *>(host)};
+        b.page_owned = (kind & SP_BLOCK_PAGE_OWNED) && (reinterpret_cast<uintptr_t>(host) & 4095u) == 0;
         if (host && !p->e->plane.dry) {
             cudaPointerAttributes a;
             if (cudaPointerGetAttributes(&a, host) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
@@ -3159,7 +3213,8 @@ int sp_pipe_sent_log(sp_pipe *p, int32_t dir, int64_t from, sp_sent *out, int64_
     *n = k;
     return SP_OK;
 }
-int64_t sp_pipe_record_count(sp_pipe *p) { return (int64_t)p->e->val.records.size(); }
+int64_t sp_pipe_record_count(sp_pipe *p) { return p->e->val.next_id - 1; }
+int64_t sp_pipe_record_first(sp_pipe *p) { return p->e->val.first_id; }
 int sp_pipe_pending(sp_pipe *p, int64_t *ids, int64_t cap, int64_t *n) {
     return guarded([&] {
         *n = (int64_t)p->e->val.order.size();
@@ -3173,8 +3228,9 @@ int sp_pipe_pending(sp_pipe *p, int64_t *ids, int64_t cap, int64_t *n) {
 int64_t sp_pipe_pending_at_iv(sp_pipe *p, uint64_t iv) { return p->e->val.pending_at_iv(iv); }
 int sp_pipe_record(sp_pipe *p, int64_t id, sp_record *out) {
     Validator &v = p->e->val;
-    if (id < 1 || id > (int64_t)v.records.size()) {
-        g_err = "no record " + std::to_string(id);
+    if (!v.retained(id)) {
+        g_err = id >= 1 && id < v.first_id ? "record " + std::to_string(id) + " compacted (record_history)"
+                                           : "no record " + std::to_string(id);
         return SP_EKEY;
     }
     const Record &r = v.rec(id);
@@ -3268,9 +3324,9 @@ int sp_val_pending(sp_val *v, int64_t *ids, int64_t cap, int64_t *n) {
         }
     });
 }
-int64_t sp_val_record_count(sp_val *v) { return (int64_t)v->v.records.size(); }
+int64_t sp_val_record_count(sp_val *v) { return v->v.next_id - 1; }
 int sp_val_record(sp_val *v, int64_t id, sp_record *out) {
-    if (id < 1 || id > (int64_t)v->v.records.size()) {
+    if (!v->v.retained(id)) {
         g_err = "no record " + std::to_string(id);
         return SP_EKEY;
     }

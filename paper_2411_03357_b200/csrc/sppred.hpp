@@ -111,10 +111,16 @@ class Predictor {
 
     // Scripted mode: a fixed prediction schedule handed out once, a fixed
     // outstanding set, observations ignored (the reference's scenario mock,
-    // cli.py:241-259 _ScriptedPredictor).
-    void script(std::vector<Prediction> preds, std::vector<int64_t> outstanding) {
+    // cli.py:241-259 _ScriptedPredictor).  `rounds` (optional, one entry per
+    // prediction) hands entries of round r out on the r-th predict call.
+    void script(std::vector<Prediction> preds, std::vector<int64_t> outstanding, std::vector<int> rounds = {}) {
         scripted_ = true;
-        script_ = std::move(preds);
+        script_rounds_.clear();
+        for (size_t k = 0; k < preds.size(); ++k) {
+            const size_t r = k < rounds.size() ? (size_t)std::max(0, rounds[k]) : 0;
+            if (script_rounds_.size() <= r) script_rounds_.resize(r + 1);
+            script_rounds_[r].push_back(preds[k]);
+        }
         script_out_ = std::unordered_set<int64_t>(outstanding.begin(), outstanding.end());
     }
     bool scripted() const { return scripted_; }
@@ -224,7 +230,7 @@ class Predictor {
                                             const std::unordered_set<int64_t>* outstanding = nullptr) {
         std::vector<Prediction> out;
         if (scripted_) {
-            out.swap(script_);  // handed out once
+            if (script_next_ < script_rounds_.size()) out.swap(script_rounds_[script_next_++]);  // each round once
             return out;
         }
         auto is_out = [&](int64_t b) { return outstanding ? outstanding->count(b) != 0 : is_outstanding(b); };
@@ -323,7 +329,8 @@ class Predictor {
 
     std::vector<Event> events_;
     bool scripted_ = false;
-    std::vector<Prediction> script_;
+    std::vector<std::vector<Prediction>> script_rounds_;
+    size_t script_next_ = 0;
     std::unordered_set<int64_t> script_out_;
     std::unordered_set<int64_t> out_pos_;
     std::vector<int64_t> stack_;

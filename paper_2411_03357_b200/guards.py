@@ -13,7 +13,10 @@ from ._native import LIB_DIR
 _PATH = os.path.join(LIB_DIR, "libspguard.so")
 _lib = None
 
-SYMBOLS = ("spg_init", "spg_protect", "spg_release", "spg_drain", "spg_active", "spg_faults", "spg_errno")
+SYMBOLS = ("spg_init", "spg_protect", "spg_protect_ex", "spg_release", "spg_drain", "spg_active", "spg_faults",
+           "spg_errno", "spg_uncovered")
+HEAD_OWNED = 1  # SPG_HEAD_OWNED
+TAIL_OWNED = 2  # SPG_TAIL_OWNED
 
 
 def lib() -> ctypes.CDLL:
@@ -23,6 +26,8 @@ def lib() -> ctypes.CDLL:
             raise RuntimeError(f"{_PATH} missing; run __graft_entry__.build()")
         L = ctypes.CDLL(_PATH)
         L.spg_protect.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64]
+        L.spg_protect_ex.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64, ctypes.c_int]
+        L.spg_uncovered.restype = ctypes.c_uint64
         L.spg_release.argtypes = [ctypes.c_int64]
         L.spg_drain.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.spg_faults.restype = ctypes.c_uint64
@@ -32,8 +37,10 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-def protect(addr: int, length: int, owner: int) -> None:
-    rc = lib().spg_protect(addr, length, owner)
+def protect(addr: int, length: int, owner: int, flags: int = 0) -> None:
+    """Guard [addr, addr+length); flags HEAD_OWNED / TAIL_OWNED extend the
+    protection over partial pages the caller owns exclusively."""
+    rc = lib().spg_protect_ex(addr, length, owner, flags)
     if rc != 0:
         raise OSError(lib().spg_errno(), f"spg_protect rc={rc}")
 
@@ -58,3 +65,8 @@ def active() -> int:
 
 def faults() -> int:
     return int(lib().spg_faults())
+
+
+def uncovered() -> int:
+    """Guards installed with part of their bytes left writable."""
+    return int(lib().spg_uncovered())

@@ -48,6 +48,7 @@ class ReplayConfig:
     engine: str = "native"
     native_dispatch: str = "replay"
     reserve_bytes: int = 0
+    record_history: int = 0  # EngineConfig.record_history (0: keep every validator record)
 
 
 @dataclass
@@ -103,7 +104,7 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
         record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat,
-        window_aware=config.window_aware)
+        window_aware=config.window_aware, record_history=config.record_history)
     predictor = Predictor(header.profile, pconf)
     engine = Engine(memory, cpu, gpu, predictor, econf, reserve_bytes=config.reserve_bytes)
     blocks = {}

@@ -64,3 +64,42 @@ def relinquish_scenario(plane: str):
 
 def test_relinquish_is_metadata_only():
     relinquish_scenario("dry")
+
+
+def test_window_aware_trim_discards_the_earlier_plan():
+    """with window-aware speculation, a prediction switching from
+    a batch that fits the record window to one that does not trims the plan
+    to nothing; the records encrypted ahead for the earlier plan must be
+    discarded (a replan), not left holding window slots until sync expiry."""
+    memory = HostMemory(pinned=False)
+    cpu, gpu = new_channel(seed=3)
+    blocks = [memory.alloc(ModelLayer(i), 4096, prng_fill(i)) for i in range(1, 8)]
+    fits = [[Prediction(blocks[0].id, 0, 0)]]
+    too_big = [[Prediction(b.id, 1 + k, 0) for k, b in enumerate(blocks[1:6])]]  # 5 blocks > window 4
+    pred = Predictor.scripted(None, {b.id for b in blocks}, rounds=[fits, too_big])
+    eng = Engine(memory, cpu, gpu, pred, EngineConfig(leeway=0, window=4, reference_compat=False, plane="dry"))
+    eng.speculate_tick()   # plan [b1]: queued
+    assert eng.report()["replans"] == 0
+    eng.speculate_tick()   # seals b1 ahead; the new prediction (5 blocks) does not fit: nothing kept
+    rep = eng.report()
+    assert rep["spec_encrypts"] == 1 and rep["replans"] == 1, rep
+    assert eng.validator.pending_count() == 0
+    assert all(r.state is RecordState.INVALIDATED for r in eng.validator.records.values())
+
+
+def test_record_history_bounds_the_record_list():
+    """a long-running pipe's validator list stays bounded with
+    EngineConfig.record_history; decisions are unchanged (same report as the
+    keep-everything run) and pending records are never forgotten."""
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import ReplayConfig, run_engine
+
+    tr = workload.gen_offload_trace(6, [1, 2, 3, 4, 5, 6], 12, layer_bytes=65536, seed=0)
+    runs = [run_engine(tr, ReplayConfig(plane="dry", record_history=h)).engine for h in (0, 8)]
+    assert runs[0].report() == runs[1].report()
+    full, capped = runs[0].validator.records, runs[1].validator.records
+    total = runs[1]._lib.sp_pipe_record_count(runs[1]._h)
+    assert len(full) == total and min(full) == 1
+    assert len(capped) <= 12 and min(capped) > 1 and max(capped) == total
+    assert {i: r.state for i, r in capped.items()} == {i: full[i].state for i in capped}
+    assert {r.id for r in runs[1].validator.pending_records()} <= set(capped)

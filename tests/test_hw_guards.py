@@ -137,3 +137,63 @@ def test_hw_guard_from_learned_prediction_gpu():
     out = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "native hw guards ok 1" in out.stdout
+
+
+RACE_SCRIPT = textwrap.dedent('''
+    import ctypes, mmap, sys, threading
+    sys.path.insert(0, %r)
+    import numpy as np
+    from paper_2411_03357_b200 import guards
+
+    PAGE = mmap.PAGESIZE
+    L = guards.lib()
+    m = mmap.mmap(-1, 8 * PAGE)
+    buf = np.frombuffer(m, dtype=np.uint8)
+    base = buf.ctypes.data
+    assert base %% PAGE == 0
+
+    # (1) partial tail page: protected only when the caller owns it
+    u0 = guards.uncovered()
+    guards.protect(base, 2 * PAGE + 100, 1)              # tail page left writable
+    assert guards.uncovered() == u0 + 1
+    ctypes.memset(base + 2 * PAGE + 50, 7, 1)             # no fault: page not covered
+    assert guards.faults() == 0
+    guards.release(1)
+    guards.protect(base, 2 * PAGE + 100, 2, guards.HEAD_OWNED | guards.TAIL_OWNED)
+    assert guards.uncovered() == u0 + 1
+    ctypes.memset(base + 2 * PAGE + 50, 8, 1)             # traps: the tail page is the block's
+    assert guards.faults() == 1 and guards.drain() == [2]
+    guards.release(2)
+
+    # (2) many threads storing into one guard at once, and a release racing
+    #     the stores: every store must retry and land, none may crash
+    n_rounds, n_threads = 200, 8
+    for r in range(n_rounds):
+        guards.protect(base + 4 * PAGE, 2 * PAGE, 100 + r)
+        go = threading.Event()
+        def store(k):
+            go.wait()
+            ctypes.memset(base + 4 * PAGE + 64 * k, r & 0xFF, 64)   # ctypes drops the GIL
+        ts = [threading.Thread(target=store, args=(k,)) for k in range(n_threads)]
+        if r %% 2:
+            ts.append(threading.Thread(target=lambda: (go.wait(), guards.release(100 + r))))
+        for t in ts:
+            t.start()
+        go.set()
+        for t in ts:
+            t.join()
+        guards.release(100 + r)
+        assert all(buf[4 * PAGE + 64 * k] == (r & 0xFF) for k in range(n_threads))
+    drained = guards.drain()
+    assert len(drained) <= n_rounds and guards.active() == 0
+    print("guard race ok", guards.faults())
+''' % ROOT)
+
+
+def test_hw_guard_tail_page_and_concurrent_stores():
+    """ADVICE r1: partial tail pages of page-owned blocks are protected; a
+    store racing another thread's fault or a release retries instead of
+    reaching SIG_DFL."""
+    out = subprocess.run([sys.executable, "-c", RACE_SCRIPT], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "guard race ok" in out.stdout
