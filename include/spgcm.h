@@ -113,6 +113,14 @@ int sp_open_host(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t
 int sp_seal_host_batch(sp_ctx *ctx, const sp_desc *descs, int n);
 int sp_open_host_batch(sp_ctx *ctx, const sp_desc *descs, int n);
 
+/* SM budget: launches of this context use at most max_sms SMs (0 = all),
+ * so the crypto kernels leave the rest of the GPU to model compute running
+ * beside them (SURVEY §7 "cap the grid").  Throughput scales with the
+ * budget; results are identical.  Applies to launches issued after the
+ * call; the only mutable context state (an atomic). */
+int sp_ctx_set_max_sms(sp_ctx *ctx, int max_sms);
+int sp_ctx_max_sms(const sp_ctx *ctx);
+
 /* Diagnostics. */
 const char *sp_last_error(void);
 const char *sp_version(void);

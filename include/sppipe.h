@@ -182,6 +182,8 @@ typedef struct sp_pipe_config {
     uint64_t reserve_bytes;  /* device pool bytes reserved at create (0: grow on demand) */
     uint64_t record_history; /* finished validator records kept (0: all, as the reference); older ones
                                 below the oldest pending record are forgotten at sync (long-running pipes) */
+    uint32_t crypto_sms;     /* SM budget of the pipe's seal/open launches (0: all SMs; sp_ctx_set_max_sms) */
+    uint32_t reserved2;
 } sp_pipe_config;
 
 typedef struct sp_action {
@@ -304,6 +306,15 @@ int64_t sp_pipe_pending_at_iv(sp_pipe *p, uint64_t iv);
 int64_t sp_pipe_delivered_count(sp_pipe *p, int32_t which);
 int sp_pipe_delivered(sp_pipe *p, int32_t which, int64_t i, sp_delivery *out, void *bytes);
 /* Data-plane statistics: bytes over PCIe per direction, kernel launches. */
+/* Model compute of a trace ComputeEvent (simulator.py:431-434 charges it to
+ * the GPU): duration_ns of calibrated FMA work over every SM on the pipe's
+ * app stream, after the swap-ins of the last sync; later swap-out seals
+ * wait for it.  sp_pipe_replay / sp_pipe_plain_replay issue SP_EV_COMPUTE
+ * events the same way. */
+int sp_pipe_compute(sp_pipe *p, uint64_t duration_ns);
+/* Compute launches so far, their requested (idle-GPU) duration and the
+ * device time they actually took (waits for them). */
+int sp_pipe_compute_stats(sp_pipe *p, uint64_t *launches, uint64_t *requested_ns, uint64_t *measured_ns);
 int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches);
 /* Device memory: bytes the stream-ordered pool holds from the driver, bytes
  * handed out, bytes parked in this pipe's buffer cache. */

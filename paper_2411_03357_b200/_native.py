@@ -22,6 +22,7 @@ SPGCM_SYMBOLS = (
     "sp_ctx_create", "sp_ctx_destroy", "sp_seal", "sp_open", "sp_seal_batch", "sp_open_batch",
     "sp_crypt_batch", "sp_seal_host", "sp_open_host", "sp_seal_host_batch", "sp_open_host_batch",
     "sp_last_error", "sp_version", "sp_launch_count", "sp_ctx_round_keys", "sp_ctx_hash_key",
+    "sp_ctx_set_max_sms", "sp_ctx_max_sms",
 )
 
 
@@ -75,6 +76,8 @@ def load_spgcm() -> ctypes.CDLL:
         lib.sp_launch_count.restype = ctypes.c_uint64
         lib.sp_ctx_round_keys.argtypes = [vp, vp]
         lib.sp_ctx_hash_key.argtypes = [vp, vp]
+        lib.sp_ctx_set_max_sms.argtypes = [vp, ctypes.c_int]
+        lib.sp_ctx_max_sms.argtypes = [vp]
         _lib = lib
         return lib
 
@@ -103,7 +106,7 @@ SPPIPE_SYMBOLS = (
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
     "sp_pipe_record_count", "sp_pipe_record_first", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
-    "sp_pipe_delivered", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
+    "sp_pipe_delivered", "sp_pipe_compute", "sp_pipe_compute_stats", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
     "sp_val_create", "sp_val_destroy", "sp_val_label", "sp_val_validate", "sp_val_commit", "sp_val_invalidate",
     "sp_val_write_fault", "sp_val_pending_at_iv", "sp_val_has_pending_range", "sp_val_invalidate_pending_below", "sp_val_pending",
     "sp_val_record_count", "sp_val_record", "sp_val_counters",
@@ -141,7 +144,7 @@ class SpPipeConfig(ctypes.Structure):
         ("dry", ctypes.c_uint8), ("hw_guards", ctypes.c_uint8), ("window_aware", ctypes.c_uint8),
         ("initial_h2d_iv", ctypes.c_uint64),
         ("initial_d2h_iv", ctypes.c_uint64), ("batch_bytes", ctypes.c_uint64), ("reserve_bytes", ctypes.c_uint64),
-        ("record_history", ctypes.c_uint64),
+        ("record_history", ctypes.c_uint64), ("crypto_sms", ctypes.c_uint32), ("reserved2", ctypes.c_uint32),
     ]
 
 
@@ -232,6 +235,8 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_delivered": [vp, i32, i64, P(SpDelivery), vp],
             "sp_pipe_record": [vp, i64, P(SpRecord)],
             "sp_pipe_stats": [vp, P(u64), P(u64), P(u64)],
+            "sp_pipe_compute": [vp, u64],
+            "sp_pipe_compute_stats": [vp, P(u64), P(u64), P(u64)],
             "sp_pipe_pool_stats": [vp, P(u64), P(u64), P(u64)],
         }
         for name, args in sig.items():

@@ -528,6 +528,11 @@ std::map<std::pair<int, cudaStream_t>, Workspace *> g_ws;
 struct sp_ctx {
     int device = 0;
     int num_sms = 148;
+    std::atomic<int> max_sms{0};  // SM budget (0: all); sp_ctx_set_max_sms
+    int sms() const {
+        const int m = max_sms.load(std::memory_order_relaxed);
+        return m > 0 && m < num_sms ? m : num_sms;
+    }
     uint32_t rk[60];
     uint32_t *d_ttab = nullptr;  // T[4][256] + R8[256]
     uint4 *d_mg = nullptr;
@@ -585,7 +590,7 @@ uint64_t rows_per_warp() {
 }
 
 void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
-    const uint64_t sms = (uint64_t)ctx->num_sms;
+    const uint64_t sms = (uint64_t)ctx->sms();
     const uint64_t want_warps =
         std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rows_per_warp(), std::min(nmsgs, rows)),
                                                  sms * kWarpsPerCta));
@@ -612,8 +617,10 @@ uint64_t small_rows_per_warp() {
 }
 
 void launch_shape_small(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
-    const uint64_t sms = (uint64_t)ctx->num_sms;
-    const uint64_t per_cta = kThreadsSmall / 32, ctas_per_sm = 4;
+    const uint64_t sms = (uint64_t)ctx->sms();
+    // under an SM budget the grid stays within `sms` CTAs (the scheduler
+    // may place co-resident CTAs on different SMs)
+    const uint64_t per_cta = kThreadsSmall / 32, ctas_per_sm = sms < (uint64_t)ctx->num_sms ? 1 : 4;
     const uint64_t want_warps = std::max<uint64_t>(
         1, std::min<uint64_t>(std::max(rows / small_rows_per_warp(), std::min(nmsgs, rows)),
                               sms * ctas_per_sm * per_cta));
@@ -1075,6 +1082,14 @@ int sp_ctx_round_keys(const sp_ctx *c, uint8_t out[240]) {
     memcpy(out, c->rk, 240);
     return SP_OK;
 }
+
+int sp_ctx_set_max_sms(sp_ctx *c, int max_sms) {
+    if (!c || max_sms < 0) return fail(SP_EINVAL, "max_sms must be >= 0");
+    c->max_sms.store(max_sms, std::memory_order_relaxed);
+    return SP_OK;
+}
+
+int sp_ctx_max_sms(const sp_ctx *c) { return c ? c->sms() : 0; }
 
 int sp_ctx_hash_key(const sp_ctx *c, uint8_t out[16]) {
     if (!c || !out) return fail(SP_EINVAL, "null argument");

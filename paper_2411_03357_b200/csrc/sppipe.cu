@@ -59,6 +59,39 @@ __global__ void k_bytes(uint8_t *__restrict__ dst, const uint8_t *__restrict__ s
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
 }
 
+// Model compute of a trace's ComputeEvent (the reference charges it to the
+// GPU timeline, simulator.py:431-434): a fixed amount of FMA work per
+// launch, calibrated to the event's duration on an idle GPU, over every SM
+// (4 CTAs x 256 threads each).  Fixed work, not a timed spin, so SM
+// contention with the crypto kernels slows it down measurably.  Each launch
+// stamps its first-CTA start and last-CTA end (globaltimer) into its span
+// slot: slot[0] = min start, slot[1] = ~max end (both atomicMin on a slot
+// initialised to all ones).
+constexpr int kComputeThreads = 256;
+constexpr int kComputeCtasPerSm = 4;
+__global__ void __launch_bounds__(kComputeThreads) k_layer_compute(uint64_t iters, unsigned long long *slot) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0 && slot) atomicMin(slot, t0);
+    float x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = (float)(threadIdx.x + c);
+    for (uint64_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) x[c] = fmaf(x[c], 0.999999f, 0.5f);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc += x[c];
+    __syncthreads();
+    if (threadIdx.x == 0 && slot) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        atomicMin(slot + 1, ~t1);
+        if (acc == -1.0f) slot[0] = 0;  // never: keeps the FMA chains live
+    }
+}
+
 // ---- error classes (Python exception names) -----------------------------------
 struct EngineErr : std::runtime_error { using std::runtime_error::runtime_error; };
 struct OverlapErr : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -497,6 +530,7 @@ class Validator {
 struct Streams {
     cudaStream_t comp, spec, h2d, d2h, land, host, out;  // host: ordered app writes; out: swap-out seals
     cudaStream_t comp2;  // consecutive flushes alternate between comp and comp2
+    cudaStream_t app;    // the model's compute (trace ComputeEvents)
 };
 
 struct DevicePool {
@@ -546,7 +580,7 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
+    cudaStream_t *all[9] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2, &s.app};
     for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
     g_streams[dev] = s;
     return s;
@@ -920,6 +954,7 @@ class Plane {
         for (cudaEvent_t e : free_events) cudaEventDestroy(e);
         if (status) cudaFree(status);
         if (zero_dev) cudaFree(zero_dev);
+        if (d_spans) cudaFree(d_spans);
     }
 
     // -- events / buffers --------------------------------------------------------------
@@ -1688,6 +1723,7 @@ class Plane {
                 Op op = make_op(SP_OP_SEAL, (uint32_t)dir, iv0 + i, m->len,
                                 View{src.buf, src.off + spans[i].first, m->len}, View{buf, m->off, m->len}, buf,
                                 m->tag_off, nullptr);
+                op.wait = app_fence;  // the model's compute before this swap-out (if any)
                 m->ready = window;
                 queue(std::move(op), m->len);
                 msgs.push_back(m);
@@ -1698,6 +1734,7 @@ class Plane {
         if (src.buf->queued) flush();
         for (auto &u : src.buf->uses)
             if (u.first != s.out && u.second && u.second->recorded) outb.waits.push_back(u.second);
+        if (app_fence) outb.waits.push_back(app_fence);  // the model's compute before this swap-out
         if (!outb.ready) outb.ready = new_fence();
         BufP buf = alloc(round16(total) + kTag * spans.size(), s.out);
         for (size_t i = 0; i < spans.size(); ++i) {
@@ -1924,8 +1961,113 @@ class Plane {
     void finish_streams() {
         flush();
         iss.drain();
-        cudaStream_t all[8] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out, s.comp2};
+        cudaStream_t all[9] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out, s.comp2, s.app};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    }
+
+    // -- model compute (trace ComputeEvents) -----------------------------------------
+    // The app stream runs the model: each compute waits for the swap-in data
+    // of the batch synced before it (compute_inputs), and every swap-out
+    // seal waits for the compute before it (app_fence) — the dependencies a
+    // real layer has.  Swap-ins of later layers do not wait: prefetch
+    // overlaps compute, as in FlexGen.
+    FenceP compute_inputs[2];  // recorded at each sync (the streams that land swap-in data)
+    FenceP app_fence;          // the last compute launch
+    unsigned long long *d_spans = nullptr;
+    uint64_t span_cap = 0, span_used = 0;
+    uint64_t compute_launches = 0, compute_ns_requested = 0;
+    static double compute_ns_per_iter(int dev, int sms) {
+        // calibrated once per device on an idle GPU (the first compute event
+        // of the process pays it, synchronously)
+        static std::mutex mu;
+        static std::map<int, double> cal;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cal.find(dev);
+        if (it != cal.end()) return it->second;
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "calibration stream");
+        cudaEvent_t a, b;
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+        const uint64_t iters = 1 << 16;
+        double best = 1e30;
+        for (int r = 0; r < 4; ++r) {
+            ck(cudaEventRecord(a, st), "event");
+            k_layer_compute<<<sms * kComputeCtasPerSm, kComputeThreads, 0, st>>>(iters, nullptr);
+            ck(cudaEventRecord(b, st), "event");
+            ck(cudaEventSynchronize(b), "calibration");
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+            if (r) best = std::min(best, (double)ms * 1e6);  // first launch warms up
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(st);
+        return cal[dev] = best / (double)iters;
+    }
+    void mark_compute_inputs() {
+        if (dry) return;
+        compute_inputs[0] = record_new(s.comp);
+        compute_inputs[1] = record_new(s.comp2);
+    }
+    void compute(uint64_t ns, const FenceP *deps, int ndeps) {
+        if (dry || !ns) return;
+        int sms = 148;
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        const double per_iter = compute_ns_per_iter(dev, sms);
+        const uint64_t iters = std::max<uint64_t>(1, (uint64_t)((double)ns / per_iter + 0.5));
+        if (span_used == span_cap) {  // grow the span ring (rare): copy the used slots over
+            const uint64_t cap = std::max<uint64_t>(4096, span_cap * 2);
+            unsigned long long *nd = nullptr;
+            iss.drain();
+            ck(cudaMalloc(&nd, cap * 2 * sizeof(unsigned long long)), "cudaMalloc(spans)");
+            ck(cudaMemset(nd, 0xff, cap * 2 * sizeof(unsigned long long)), "cudaMemset(spans)");
+            if (d_spans) {
+                ck(cudaStreamSynchronize(s.app), "sync app");
+                ck(cudaMemcpy(nd, d_spans, span_used * 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice),
+                   "span copy");
+                cudaFree(d_spans);
+            }
+            d_spans = nd;
+            span_cap = cap;
+        }
+        for (int k = 0; k < ndeps; ++k)
+            if (deps[k]) wait(s.app, deps[k]);
+        unsigned long long *slot = d_spans + 2 * span_used++;
+        const cudaStream_t st = s.app;
+        const unsigned grid = (unsigned)(sms * kComputeCtasPerSm);
+        iss.post([iters, slot, st, grid] {
+            k_layer_compute<<<grid, kComputeThreads, 0, st>>>(iters, slot);
+            ck(cudaGetLastError(), "k_layer_compute launch");
+        });
+        app_fence = record_new(s.app);
+        ++compute_launches;
+        compute_ns_requested += ns;
+    }
+    // Device time the compute launches took (sum of first-start..last-end),
+    // in ns; waits for them.
+    uint64_t compute_ns_measured() {
+        if (dry || !span_used) return 0;
+        iss.drain();
+        ck(cudaStreamSynchronize(s.app), "sync app");
+        std::vector<unsigned long long> h(2 * span_used);
+        ck(cudaMemcpy(h.data(), d_spans, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "spans");
+        uint64_t sum = 0;
+        for (uint64_t k = 0; k < span_used; ++k) {
+            const unsigned long long t0 = h[2 * k], t1 = ~h[2 * k + 1];
+            if (t0 != ~0ull && t1 >= t0) sum += t1 - t0;
+        }
+        return sum;
+    }
+    void reset_compute_stats() {
+        if (d_spans && span_used) {
+            iss.drain();
+            ck(cudaStreamSynchronize(s.app), "sync app");
+            ck(cudaMemset(d_spans, 0xff, span_used * 2 * sizeof(unsigned long long)), "cudaMemset(spans)");
+        }
+        span_used = 0;
+        compute_launches = 0;
+        compute_ns_requested = 0;
     }
     // drain_all = false: wait only for work whose results can be observed —
     // every receiver open and verdict (comp; it waited for the encrypt-ahead
@@ -2131,6 +2273,7 @@ class Engine {
         : cfg(c), plane(c.dry != 0, key, c.batch_bytes ? c.batch_bytes : (64ull << 20), c.reserve_bytes), pred(p),
           val(mem, c.window) {
         val.history = c.record_history;
+        if (!plane.dry) ck_sp(sp_ctx_set_max_sms(plane.ctx, (int)c.crypto_sms), "sp_ctx_set_max_sms");
         if (c.hw_guards) {
             if (spg_init() != SPG_OK) throw std::runtime_error("spg_init failed");
             mem.hw = true;
@@ -2645,6 +2788,7 @@ class Engine {
         counters[C_EXPIRED_RECORDS] += val.invalidate_pending_below(send_iv[H2D]);
         drain_decrypts();
         plane.flush();
+        plane.mark_compute_inputs();  // the batch's swap-in data, for the compute after this sync
         if (!batch_ins.empty()) {
             std::vector<int64_t> batch(batch_ins);
             batch_ins.clear();
@@ -2746,6 +2890,8 @@ class Engine {
             }
         };
         Pend pin, pout;
+        std::unordered_map<int64_t, FenceP> in_fence;  // block -> the H2D flush that carried its swap-in
+        FenceP sync_in;                                // swap-ins up to the last sync (what compute reads)
         auto issue = [&](Pend &q, cudaStream_t st, bool h2d) {
             pl.copy_batch(st, h2d, q.n.size(), [&](size_t i, void *&d, void *&src, size_t &k) {
                 d = q.dst[i];
@@ -2760,11 +2906,19 @@ class Engine {
         auto flush_in = [&] {
             if (pin.n.empty()) return;
             last_in = issue(pin, pl.s.h2d, true);
+            for (int64_t b : pin.blocks) in_fence[b] = last_in;
             pin = Pend{};
         };
         auto flush_out = [&] {
             if (pout.n.empty()) return;
-            if (last_in) pl.wait(pl.s.d2h, last_in);  // swap-outs follow the swap-ins issued before them
+            // a swap-out reads what its own swap-in brought (and what the
+            // model computed since), the same dependencies the engine has
+            std::unordered_set<Fence *> waited;
+            for (int64_t b : pout.blocks) {
+                auto it = in_fence.find(b);
+                if (it != in_fence.end() && waited.insert(it->second.get()).second) pl.wait(pl.s.d2h, it->second);
+            }
+            if (pl.app_fence) pl.wait(pl.s.d2h, pl.app_fence);
             FenceP f = issue(pout, pl.s.d2h, false);
             for (int64_t b : pout.blocks) landed[b] = f;
             pout = Pend{};
@@ -2794,6 +2948,9 @@ class Engine {
             } else if (e.kind == SP_EV_SYNC) {
                 flush_in();
                 flush_out();
+                sync_in = last_in;
+            } else if (e.kind == SP_EV_COMPUTE) {
+                pl.compute(e.len, &sync_in, 1);
             } else if (e.kind == SP_EV_APP_WRITE) {
                 // the same ordered host write the engine performs (after the block's pending DMA)
                 flush_in();
@@ -2829,6 +2986,13 @@ class Engine {
     }
 
     // Replay driver (simulator.py:404-426 dispatch, workload event kinds).
+    // A trace ComputeEvent (duration in ns): model work on the app stream
+    // after the last sync's swap-ins; later swap-outs wait for it.
+    void compute(uint64_t ns) {
+        complete_spec_tasks();
+        plane.compute(ns, plane.compute_inputs, 2);
+    }
+
     void replay(const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
         for (uint64_t k = 0; k < n; ++k) {
             const sp_event &e = ev[k];
@@ -2840,6 +3004,7 @@ class Engine {
                 case SP_EV_SMALL_IO_D2H: small_io(D2H, payloads ? payloads + e.payload : nullptr, e.len); break;
                 case SP_EV_SYNC: sync(); break;
                 case SP_EV_APP_WRITE: app_write(e.block, e.base, payloads + e.payload, e.len); break;
+                case SP_EV_COMPUTE: compute(e.len); break;
                 default: break;
             }
             if (done) *done = k + 1;
@@ -3264,6 +3429,16 @@ int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t 
     if (used) *used = u;
     if (cached) *cached = pl.cached_bytes;
     return SP_OK;
+}
+int sp_pipe_compute(sp_pipe *p, uint64_t duration_ns) {
+    return guarded([&] { p->e->compute(duration_ns); });
+}
+int sp_pipe_compute_stats(sp_pipe *p, uint64_t *launches, uint64_t *requested_ns, uint64_t *measured_ns) {
+    return guarded([&] {
+        if (launches) *launches = p->e->plane.compute_launches;
+        if (requested_ns) *requested_ns = p->e->plane.compute_ns_requested;
+        if (measured_ns) *measured_ns = p->e->plane.compute_ns_measured();
+    });
 }
 int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches) {
     if (bytes_h2d) *bytes_h2d = p->e->plane.bytes_h2d;

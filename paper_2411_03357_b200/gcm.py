@@ -142,6 +142,14 @@ class GcmContext:
         _check(self._lib.sp_open_host_batch(self._h, descs, len(items)), "sp_open_host_batch")
 
     # -- device tensors --------------------------------------------------------
+    def set_max_sms(self, max_sms: int) -> None:
+        """SM budget of this context's launches (0: every SM)."""
+        _check(self._lib.sp_ctx_set_max_sms(self._h, int(max_sms)), "sp_ctx_set_max_sms")
+
+    @property
+    def max_sms(self) -> int:
+        return int(self._lib.sp_ctx_max_sms(self._h))
+
     def seal_batch(self, items: Sequence[tuple], stream=None) -> None:
         """items: (dir, iv, src, dst, tag) with device tensors (or int
         pointers + explicit len via a 6th element)."""

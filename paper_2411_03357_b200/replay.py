@@ -49,6 +49,11 @@ class ReplayConfig:
     native_dispatch: str = "replay"
     reserve_bytes: int = 0
     record_history: int = 0  # EngineConfig.record_history (0: keep every validator record)
+    # replay the trace's ComputeEvents as model work on the GPU (the
+    # reference simulator charges them to the GPU timeline,
+    # simulator.py:431-434); off: swaps only
+    compute: bool = False
+    crypto_sms: int = 0  # EngineConfig.crypto_sms: SM budget of the crypto launches (0: all)
 
 
 @dataclass
@@ -104,7 +109,7 @@ def build_engine(trace: Trace, config: ReplayConfig, memory: HostMemory | None =
         window=config.window, leeway=config.leeway, depth=config.depth, workers=config.workers,
         chunk_bytes=config.chunk_bytes, speculate=spec_on, defer_swap_decrypt=spec_on,
         record_stream=config.record_stream, plane=config.plane, reference_compat=config.reference_compat,
-        window_aware=config.window_aware, record_history=config.record_history)
+        window_aware=config.window_aware, record_history=config.record_history, crypto_sms=config.crypto_sms)
     predictor = Predictor(header.profile, pconf)
     engine = Engine(memory, cpu, gpu, predictor, econf, reserve_bytes=config.reserve_bytes)
     blocks = {}
@@ -180,6 +185,8 @@ def encode_events(trace: Trace, blocks: dict, config: ReplayConfig, start: int =
             block, _ = blocks[ev.block]
             events.append((5, 0, block.id, ev.offset, ev.size, len(payload)))
             payload += app_write_payload(ev.data_seed, ev.size)
+        elif isinstance(ev, ComputeEvent) and config.compute:
+            events.append((6, 0, 0, 0, ev.duration, 0))
     return events, bytes(payload)
 
 
@@ -287,7 +294,8 @@ def _dispatch_all(engine: Engine, blocks: dict, trace: Trace, config: ReplayConf
             block, _ = blocks[ev.block]
             engine.app_write(block.id, ev.offset, app_write_payload(ev.data_seed, ev.size))
         elif isinstance(ev, ComputeEvent):
-            pass
+            if config.compute:
+                engine.compute(ev.duration)
     engine.finish()
 
 
@@ -309,7 +317,9 @@ def run_plain_native(trace: Trace, config: ReplayConfig = ReplayConfig(), memory
     t0 = time.perf_counter()
     engine.plain_replay_encoded(seg)
     wall = time.perf_counter() - t0
-    return ReplayResult(None, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
+    # the engine only carries the plain run's device state (compute_stats);
+    # its control plane saw no events
+    return ReplayResult(engine, wall, _swap_bytes_from(trace, measure_from), trace.payload_bytes())
 
 
 def main(argv: list[str] | None = None) -> int:

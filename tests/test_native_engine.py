@@ -22,7 +22,7 @@ import pytest
 
 from paper_2411_03357_b200 import _native, workload
 from paper_2411_03357_b200.predictor import ModelProfile, Predictor
-from paper_2411_03357_b200.replay import ReplayConfig, run_engine
+from paper_2411_03357_b200.replay import ReplayConfig, run_engine, run_plain_native
 from tests.golden_io import (action_tuple, assert_schedule_matches, replay_schedule_case, schedule_case,
                              schedules_golden)
 from tests.test_abi import declared
@@ -446,3 +446,59 @@ def test_opt66b_bench_schedule_gpu(system):
     rec = schedule_case("opt66b_bench", system)
     _, res = replay_schedule_case(rec, "gpu", fill="fast", record_stream=False)
     assert_schedule_matches(rec, res)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("crypto_sms", [0, 8])
+def test_offload_with_model_compute_gpu(crypto_sms):
+    """ComputeEvents replayed as GPU work (simulator.py:431-434) beside the
+    swaps, with and without an SM budget on the crypto launches: the same
+    decisions as the swap-only replay, every delivered swap-in byte-exact,
+    the host blocks restored by the swap-outs, and one compute launch per
+    ComputeEvent that took device time."""
+    import hashlib
+
+    from paper_2411_03357_b200 import prng
+
+    tr = workload.gen_offload_trace(6, [1, 2, 3, 4, 5, 6], 3, layer_bytes=1 << 20, seed=0)
+    n_compute = sum(1 for e in tr.events if isinstance(e, workload.ComputeEvent))
+    base = run_engine(tr, ReplayConfig(system="specpipe", record_stream=True, plane="gpu"))
+    res = run_engine(tr, ReplayConfig(system="specpipe", record_stream=True, plane="gpu", compute=True,
+                                      crypto_sms=crypto_sms))
+    assert res.engine.report() == base.engine.report()
+    assert [d[:3] for d in res.engine.delivered] == [d[:3] for d in base.engine.delivered]
+    by_base = {b.base: b for b in res.engine.memory.blocks()}
+    for _seq, addr, nbytes, digest in res.engine.delivered:
+        assert digest == hashlib.sha256(by_base[addr].data[:nbytes].tobytes()).hexdigest()
+    for spec in tr.header.blocks:
+        blk = res.engine.memory.block(spec.id)
+        assert hashlib.sha256(blk.data).hexdigest() == \
+            hashlib.sha256(prng.random_bytes(spec.content_seed, spec.nbytes)).hexdigest()
+    st = res.engine.compute_stats()
+    assert st["launches"] == n_compute and st["requested_ns"] == n_compute * 200_000
+    assert st["measured_ns"] >= 0.5 * st["requested_ns"], st
+    plain = run_plain_native(tr, ReplayConfig(plane="gpu", compute=True))
+    assert plain.engine.compute_stats()["launches"] == n_compute
+
+
+@pytest.mark.gpu
+def test_sm_budget_keeps_results_gpu():
+    """sp_ctx_set_max_sms: a capped context seals the same bytes and tags."""
+    import torch
+
+    from paper_2411_03357_b200.gcm import GcmContext
+
+    ctx = GcmContext(bytes(range(32)))
+    sizes = [1, 4096, 229_376, (1 << 20) + 5, 8 << 20]
+    src = [torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda") for n in sizes]
+    outs = []
+    for sms in (0, 4, 37):
+        ctx.set_max_sms(sms)
+        assert ctx.max_sms == (sms or torch.cuda.get_device_properties(0).multi_processor_count)
+        dst = [torch.empty_like(s) for s in src]
+        tags = torch.empty((len(sizes), 16), dtype=torch.uint8, device="cuda")
+        ctx.seal_batch([(0, 7 + i, s, d, tags[i]) for i, (s, d) in enumerate(zip(src, dst))])
+        torch.cuda.synchronize()
+        outs.append(([bytes(d.cpu().numpy()) for d in dst], bytes(tags.cpu().numpy())))
+    assert outs[0] == outs[1] == outs[2]
+    ctx.set_max_sms(0)

@@ -56,10 +56,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_alu(uint32_t seed, int per_sm_s
 template <int WIDE>
 __global__ void __launch_bounds__(kThreads, 1) k_lds(uint32_t seed, int per_sm_slot) {
     extern __shared__ __align__(16) uint32_t tab[];  // 64 KiB: 256 entries x 256 B
-    for (int i = threadIdx.x; i < 16384; i += blockDim.x) tab[i] = (i * 2654435761u) >> 8;
+    for (int i = threadIdx.x; i < 16384; i += blockDim.x) tab[i] = ((i * 2654435761u) >> 8) & 0xffu;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+    // k_gcm's lookup: one PRMT forms (byte << 8) | lane constant, then
+    // LDS [reg + imm] at the absolute dynamic-smem base (0x400, checked)
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(tab)) != 0x400u) __trap();
+    const uint32_t lc = WIDE ? (lane & 7u) * 16u : lane * 4u;
     uint32_t v[kChains];
 #pragma unroll
     for (int c = 0; c < kChains; ++c) v[c] = (seed + c * 77u + threadIdx.x) & 0xffu;
@@ -67,15 +70,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_lds(uint32_t seed, int per_sm_s
     if (!WIDE) {
         CHAIN_LOOP({
             uint32_t r;
-            const uint32_t a = base + ((v[c] & 0xffu) << 8) + lane * 4u;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+            const uint32_t a = __byte_perm(v[c], lc, 0x5504u);
+            asm volatile("ld.shared.u32 %0, [%1+0x400];" : "=r"(r) : "r"(a));
             v[c] = r;
         });
     } else {
         CHAIN_LOOP({
             uint32_t r0, r1, r2, r3;
-            const uint32_t a = base + ((v[c] & 0xffu) << 8) + (lane & 7u) * 16u;
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
+            const uint32_t a = __byte_perm(v[c], lc, 0x5504u);
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4+0x400];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
             v[c] = r0 ^ r1 ^ r2 ^ r3;
         });
     }
