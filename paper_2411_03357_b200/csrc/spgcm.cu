@@ -93,7 +93,12 @@ __device__ __forceinline__ uint4 len_block(uint64_t len) {
 
 // Tag finalisation for one message; T = GHASH xor E_K(J0) (the warp that
 // covered the message's first row folded E_K(J0) in).  Warp-uniform.
-__device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int lane) {
+__device__ __forceinline__ uint4 load_tag(const uint8_t *t) {
+    return (reinterpret_cast<uintptr_t>(t) & 15u) == 0 ? __ldg(reinterpret_cast<const uint4 *>(t)) : load_bytes(t, 16);
+}
+
+// want: the expected tag, already loaded by lane 0 (have_want) or loaded here.
+__device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int lane, uint4 want, bool have_want) {
     if (!(md.dir & kOpenBit)) {
         if (lane == 0) {
             if ((reinterpret_cast<uintptr_t>(md.tag) & 15u) == 0)
@@ -105,7 +110,7 @@ __device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int 
     }
     uint32_t bad = 0;
     if (lane == 0) {
-        const uint4 want = load_bytes(md.tag, 16);
+        if (!have_want) want = load_tag(md.tag);
         bad = (want.x ^ tag.x) | (want.y ^ tag.y) | (want.z ^ tag.z) | (want.w ^ tag.w);
         if (md.status) *md.status = bad ? 1 : 0;
     }
@@ -195,20 +200,25 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
 
         // Prefetch into L2 the F / H^(32b) rows this lane's epilogue reads
         // (2 lines each; cold in HBM otherwise): overlaps two of the
-        // epilogue's dependent DRAM round trips with the row loop.
-        {
-            const uint32_t r_end_pf = md.rows - (uint32_t)t_b;
-            const char *ft = reinterpret_cast<const char *>(p.nt + (size_t)(kNtF + (r_end_pf >> 4)) * kNtEntries + lane * 16);
+        // epilogue's dependent DRAM round trips with the row loop.  A run
+        // that ends at its message's end (r_end = 0) needs neither.
+        const uint32_t r_end = md.rows - (uint32_t)t_b;
+        if (r_end) {
+            const char *ft = reinterpret_cast<const char *>(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries + lane * 16);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ft));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ft + 128));
-            if (r_end_pf & 15u) {
+            if (r_end & 15u) {
                 const char *pt = reinterpret_cast<const char *>(
-                    p.nt + (size_t)(kNtP32 + (r_end_pf & 15u) - 1u) * kNtEntries + lane * 16);
+                    p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries + lane * 16);
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pt));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pt + 128));
             }
         }
-        const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);
+        // the expected tag of an open whose last row this run covers: read
+        // now, not after the epilogue
+        const bool have_want = opening && t_b == md.rows && lane == 0;
+        const uint4 want = have_want ? load_tag(md.tag) : make_uint4(0, 0, 0, 0);
+        const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);  // L x H
         const CtrConst cc = ctr_const<TB>(p.rk, lct, x0, x1, x2);
         CtrCache ck;
         ck.gid = 0xffffffffu;
@@ -236,18 +246,22 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
             cur = nxt;
         }
 
-        // combine lanes: W = sum_l Y_l * H^(32 - l); the lane-table loads
-        // are in flight while the warp covering the message's first row
-        // computes E_K(J0) (folded into W: XOR is order-free, so the
-        // finisher needs no AES of its own)
-        const uint4 lanes_w = nt_mul_lane(p.nt + (size_t)(kNtLane + 31 - lane) * kNtEntries, y);
+        // combine lanes: W = sum_l Y_l * H^(32 - l), then x H^(32 r_end + 1).
+        // A run that ends at its message's end (r_end = 0) walks the tables
+        // of H^(33 - l) and is done (one dependent round trip fewer).  The
+        // lane-table loads are in flight while the warp covering the
+        // message's first row computes E_K(J0) (folded into W: XOR is
+        // order-free, so the finisher needs no AES of its own).
+        const uint4 lanes_w =
+            nt_mul_lane(p.nt + (size_t)(kNtLane + (r_end ? 31u : 32u) - (uint32_t)lane) * kNtEntries, y);
         uint4 ek = make_uint4(0, 0, 0, 0);
         if (t_a == 0 && lane == 0) ek = aes256_rounds<TB>(p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
         uint4 w = warp_xor(lanes_w);
-        // scale by H^(32*r_end + 1), r_end = rows after this run
-        const uint32_t r_end = md.rows - (uint32_t)t_b;
-        w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
-        if (r_end & 15u) w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+        if (r_end) {  // scale by H^(32 r_end + 1) = F[r_end / 16] x H^(32 (r_end mod 16))
+            w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
+            if (r_end & 15u)
+                w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+        }
         if (t_a == 0) {
             ek.x = __shfl_sync(0xffffffffu, ek.x, 0);
             ek.y = __shfl_sync(0xffffffffu, ek.y, 0);
@@ -257,7 +271,7 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
         }
 
         if (t_a == 0 && t_b == md.rows) {
-            finish_message(md, xor4(w, warp_xor(lh_part)), lane);
+            finish_message(md, xor4(w, warp_xor(lh_part)), lane, want, have_want);
         } else {
             uint32_t *acc = p.acc + (size_t)m * 8u;
             // XOR-accumulate (order-free, so deterministic) and count rows:
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
                 a.y = __shfl_sync(0xffffffffu, v, 1);
                 a.z = __shfl_sync(0xffffffffu, v, 2);
                 a.w = __shfl_sync(0xffffffffu, v, 3);
-                finish_message(md, xor4(a, warp_xor(lh_part)), lane);
+                finish_message(md, xor4(a, warp_xor(lh_part)), lane, want, have_want);
             }
         }
         g = md.row_begin + t_b;
@@ -376,7 +390,7 @@ __global__ void k_setup_powers(const uint4 *hptr, uint4 *powers) {
     if (idx > kNumNt) return;
     const G128 h = g_from_words(*hptr);
     uint64_t e;
-    if (idx < kNtF) e = idx + 1;                                   // H^1..H^32
+    if (idx < kNtF) e = idx + 1;                                   // H^1..H^33
     else if (idx < kNtP32) e = 512ull * (idx - kNtF) + 1;          // F_a
     else if (idx < kNumNt) e = 32ull * (idx - kNtP32 + 1);         // H^(32b)
     else e = 32;                                                    // G
@@ -621,9 +635,14 @@ void launch_shape_small(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &g
     // under an SM budget the grid stays within `sms` CTAs (the scheduler
     // may place co-resident CTAs on different SMs)
     const uint64_t per_cta = kThreadsSmall / 32, ctas_per_sm = sms < (uint64_t)ctx->num_sms ? 1 : 4;
-    const uint64_t want_warps = std::max<uint64_t>(
-        1, std::min<uint64_t>(std::max(rows / small_rows_per_warp(), std::min(nmsgs, rows)),
-                              sms * ctas_per_sm * per_cta));
+    // one-row messages (NOP pads) get one warp each; longer ones split
+    // small_rows_per_warp() rows per warp (SPGCM_SMALL_SINGLE_ROWS=k keeps
+    // messages of up to k rows on one warp: measured slower for k = 8 on
+    // 2 KiB tokens, 9.8 vs 7.9 us per launch, profiles/r2_launch_latency.txt)
+    static const uint64_t single = env_u64("SPGCM_SMALL_SINGLE_ROWS", 1);  // >1: measured slower (r2)
+    const uint64_t spread = rows <= single * nmsgs ? std::min(nmsgs, rows)
+                                              : std::max(rows / small_rows_per_warp(), std::min(nmsgs, rows));
+    const uint64_t want_warps = std::max<uint64_t>(1, std::min<uint64_t>(spread, sms * ctas_per_sm * per_cta));
     warps_used = (uint32_t)std::min<uint64_t>(per_cta, (want_warps + sms * ctas_per_sm - 1) / (sms * ctas_per_sm));
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }

@@ -35,10 +35,10 @@ constexpr int kWarpsPerCta = kThreads / 32;
 constexpr uint64_t kMaxMsg = 32ull << 20;
 constexpr uint32_t kMaxRows = (uint32_t)((kMaxMsg / 16 + 31) / 32);  // 65536
 constexpr uint32_t kNumF = (kMaxRows + 15) / 16;                     // 4096
-// nibble-table index layout (each table: 32 positions x 16 values x uint4)
-constexpr uint32_t kNtLane = 0;          // H^e, e = 1..32  -> index e-1
-constexpr uint32_t kNtF = 32;            // F_a = H^(512a+1), a < kNumF
-constexpr uint32_t kNtP32 = 32 + kNumF;  // H^(32b), b = 1..15 -> kNtP32 + b - 1
+// nibble-table index layout (each table: 32 positions x 16 values x uint4 = 8 KiB)
+constexpr uint32_t kNtLane = 0;          // H^e, e = 1..33 -> index e-1 (H^(33-l): runs ending at their message's end)
+constexpr uint32_t kNtF = 33;            // F_a = H^(512a+1), a < kNumF
+constexpr uint32_t kNtP32 = kNtF + kNumF;  // H^(32b), b = 1..15 -> kNtP32 + b - 1
 constexpr uint32_t kNumNt = kNtP32 + 15;
 constexpr uint32_t kNtEntries = 32 * 16;
 

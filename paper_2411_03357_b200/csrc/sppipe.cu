@@ -61,14 +61,17 @@ __global__ void k_bytes(uint8_t *__restrict__ dst, const uint8_t *__restrict__ s
 
 // Model compute of a trace's ComputeEvent (the reference charges it to the
 // GPU timeline, simulator.py:431-434): a fixed amount of FMA work per
-// launch, calibrated to the event's duration on an idle GPU, over every SM
-// (4 CTAs x 256 threads each).  Fixed work, not a timed spin, so SM
-// contention with the crypto kernels slows it down measurably.  Each launch
+// launch, calibrated to the event's duration on an idle GPU, in 16 waves of
+// 4 CTAs x 256 threads per SM (tiles, like a GEMM: CTAs flow to whichever
+// SMs are free).  Fixed work, not a timed spin, so SM contention with the
+// crypto kernels slows it down measurably.  The app stream has the highest
+// stream priority: its CTAs are dispatched ahead of queued crypto CTAs.  Each launch
 // stamps its first-CTA start and last-CTA end (globaltimer) into its span
 // slot: slot[0] = min start, slot[1] = ~max end (both atomicMin on a slot
 // initialised to all ones).
 constexpr int kComputeThreads = 256;
 constexpr int kComputeCtasPerSm = 4;
+constexpr int kComputeWaves = 16;
 __global__ void __launch_bounds__(kComputeThreads) k_layer_compute(uint64_t iters, unsigned long long *slot) {
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -580,8 +583,11 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[9] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2, &s.app};
+    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
     for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
+    int lo = 0, hi = 0;  // the model's compute outranks the crypto launches
+    ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+    ck(cudaStreamCreateWithPriority(&s.app, cudaStreamNonBlocking, hi), "cudaStreamCreate(app)");
     g_streams[dev] = s;
     return s;
 }
@@ -1993,7 +1999,7 @@ class Plane {
         double best = 1e30;
         for (int r = 0; r < 4; ++r) {
             ck(cudaEventRecord(a, st), "event");
-            k_layer_compute<<<sms * kComputeCtasPerSm, kComputeThreads, 0, st>>>(iters, nullptr);
+            k_layer_compute<<<sms * kComputeCtasPerSm * kComputeWaves, kComputeThreads, 0, st>>>(iters, nullptr);
             ck(cudaEventRecord(b, st), "event");
             ck(cudaEventSynchronize(b), "calibration");
             float ms = 0;
@@ -2035,7 +2041,7 @@ class Plane {
             if (deps[k]) wait(s.app, deps[k]);
         unsigned long long *slot = d_spans + 2 * span_used++;
         const cudaStream_t st = s.app;
-        const unsigned grid = (unsigned)(sms * kComputeCtasPerSm);
+        const unsigned grid = (unsigned)(sms * kComputeCtasPerSm * kComputeWaves);
         iss.post([iters, slot, st, grid] {
             k_layer_compute<<<grid, kComputeThreads, 0, st>>>(iters, slot);
             ck(cudaGetLastError(), "k_layer_compute launch");
@@ -2879,13 +2885,15 @@ class Engine {
             std::vector<size_t> n;
             std::vector<BufP> keep;
             std::unordered_set<int64_t> blocks;
+            std::vector<std::pair<uint8_t *, uint64_t>> ring;  // token slots of the pinned ring it copies
+            uint64_t ring_bytes = 0;
             uint64_t bytes = 0;
             void add(void *d, void *s, size_t k, const BufP &b, int64_t blk) {
                 dst.push_back(d);
                 src.push_back(s);
                 n.push_back(k);
                 keep.push_back(b);
-                blocks.insert(blk);
+                if (blk >= 0) blocks.insert(blk);
                 bytes += k;
             }
         };
@@ -2901,6 +2909,7 @@ class Engine {
             FenceP f = pl.record_new(st);
             ++pl.tick;
             for (auto &b : q.keep) b->use(st, f, pl.tick);
+            for (auto &r : q.ring) pl.ring_commit(r.first, r.second, f);
             return f;
         };
         auto flush_in = [&] {
@@ -2961,21 +2970,21 @@ class Engine {
                 pl.enqueue_host_write(b, e.base, payloads + e.payload, e.len, last_in);
                 landed[e.block] = pl.host_ready[e.block];
             } else if (e.kind == SP_EV_SMALL_IO_H2D || e.kind == SP_EV_SMALL_IO_D2H) {
+                // token copies ride in the batch of their direction (one
+                // cudaMemcpyBatchAsync per sync), through the pinned ring
                 const bool h2d = e.kind == SP_EV_SMALL_IO_H2D;
                 cudaStream_t st = h2d ? pl.s.h2d : pl.s.d2h;
                 View v{pl.alloc(e.len, st), 0, e.len};
                 uint8_t *h = pl.ring_reserve(e.len);
                 if (h2d && payloads) memcpy(h, payloads + e.payload, e.len);
-                void *cd = h2d ? (void *)v.ptr() : (void *)h;
-                const void *cs = h2d ? (const void *)h : (const void *)v.ptr();
-                const uint64_t cn = e.len;
-                pl.iss.post([cd, cs, cn, h2d, st] {
-                    ck(cudaMemcpyAsync(cd, cs, cn, h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
-                       "plain token copy");
-                });
-                FenceP f = pl.record_new(st);
-                pl.ring_commit(h, e.len, f);
-                v.buf->use(st, f, ++pl.tick);
+                Pend &q = h2d ? pin : pout;
+                if (h2d) q.add(v.ptr(), h, e.len, v.buf, -1);
+                else q.add(h, v.ptr(), e.len, v.buf, -1);
+                q.ring.push_back({h, e.len});
+                // ring slots are reserved against committed fences only:
+                // issue long token runs before the ring could wrap onto them
+                q.ring_bytes += (e.len + 63u) & ~uint64_t(63);
+                if (q.ring_bytes >= (8ull << 20)) h2d ? flush_in() : flush_out();
             }
         }
         flush_in();

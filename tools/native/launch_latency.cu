@@ -5,6 +5,7 @@
 //        -L paper_2411_03357_b200/lib -lspgcm -Xlinker -rpath,$PWD/paper_2411_03357_b200/lib -o /tmp/ll
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <vector>
 
@@ -53,10 +54,35 @@ int main() {
         for (int i = 0; i < c.n; ++i) {
             d[i] = sp_desc{SP_DIR_H2D, 0u, (uint64_t)i, c.size, buf + i * c.size, buf + i * c.size, tags + 16 * i, nullptr};
         }
+        {  // device time alone: the same launches captured once in a CUDA graph, replayed
+            const int reps = 200;
+            cudaGraph_t g;
+            cudaGraphExec_t ge;
+            cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+            for (int r = 0; r < reps; ++r) sp_seal_batch(ctx, d.data(), c.n, s);
+            cudaStreamEndCapture(s, &g);
+            if (cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) {
+                cudaGraphLaunch(ge, s);
+                cudaStreamSynchronize(s);
+                cudaEventRecord(a, s);
+                for (int k = 0; k < 5; ++k) cudaGraphLaunch(ge, s);
+                cudaEventRecord(b, s);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                printf("%-18s %-16s %7.2f us/launch\n", c.name, "graph (device)", ms * 1e3 / (5 * reps));
+                cudaGraphExecDestroy(ge);
+            } else {
+                printf("%-18s %-16s   n/a (capture failed: %s)\n", c.name, "graph (device)", cudaGetErrorString(cudaGetLastError()));
+            }
+            cudaGraphDestroy(g);
+            cudaGetLastError();
+        }
         for (int mode = 0; mode < 2; ++mode) {
             const int reps = 2000;
             for (int w = 0; w < 50; ++w) sp_seal_batch(ctx, d.data(), c.n, s);
             cudaStreamSynchronize(s);
+            const auto h0 = std::chrono::steady_clock::now();
             cudaEventRecord(a, s);
             for (int r = 0; r < reps; ++r) {
                 if (mode == 1) {  // event hop through a second stream before every launch
@@ -68,10 +94,13 @@ int main() {
                 sp_seal_batch(ctx, d.data(), c.n, s);
             }
             cudaEventRecord(b, s);
+            const double host_us =
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count() / reps;
             cudaEventSynchronize(b);
             float ms = 0;
             cudaEventElapsedTime(&ms, a, b);
-            printf("%-18s %-16s %7.2f us/launch\n", c.name, mode ? "event-hop" : "back-to-back", ms * 1e3 / reps);
+            printf("%-18s %-16s %7.2f us/launch  (host issue %.2f us/launch)\n", c.name,
+                   mode ? "event-hop" : "back-to-back", ms * 1e3 / reps, host_us);
         }
     }
     printf("launches %llu\n", (unsigned long long)sp_launch_count());
