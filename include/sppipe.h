@@ -316,6 +316,10 @@ int sp_pipe_compute(sp_pipe *p, uint64_t duration_ns);
  * device time they actually took (waits for them). */
 int sp_pipe_compute_stats(sp_pipe *p, uint64_t *launches, uint64_t *requested_ns, uint64_t *measured_ns);
 int sp_pipe_stats(sp_pipe *p, uint64_t *bytes_h2d, uint64_t *bytes_d2h, uint64_t *launches);
+/* The issuing thread: stream-ordered CUDA calls posted so far and the time
+ * spent inside them (ns); busy close to a run's wall time = issue-bound.
+ * host_queries: event queries the control plane itself made. */
+int sp_pipe_issuer_stats(sp_pipe *p, uint64_t *calls, uint64_t *busy_ns, uint64_t *host_queries);
 /* Device memory: bytes the stream-ordered pool holds from the driver, bytes
  * handed out, bytes parked in this pipe's buffer cache. */
 int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t *cached);

@@ -106,7 +106,7 @@ SPPIPE_SYMBOLS = (
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
     "sp_pipe_record_count", "sp_pipe_record_first", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
-    "sp_pipe_delivered", "sp_pipe_compute", "sp_pipe_compute_stats", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
+    "sp_pipe_delivered", "sp_pipe_compute", "sp_pipe_compute_stats", "sp_pipe_issuer_stats", "sp_pipe_stats", "sp_pipe_pool_stats", "sp_pipe_last_error",
     "sp_val_create", "sp_val_destroy", "sp_val_label", "sp_val_validate", "sp_val_commit", "sp_val_invalidate",
     "sp_val_write_fault", "sp_val_pending_at_iv", "sp_val_has_pending_range", "sp_val_invalidate_pending_below", "sp_val_pending",
     "sp_val_record_count", "sp_val_record", "sp_val_counters",
@@ -237,6 +237,7 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_stats": [vp, P(u64), P(u64), P(u64)],
             "sp_pipe_compute": [vp, u64],
             "sp_pipe_compute_stats": [vp, P(u64), P(u64), P(u64)],
+            "sp_pipe_issuer_stats": [vp, P(u64), P(u64), P(u64)],
             "sp_pipe_pool_stats": [vp, P(u64), P(u64), P(u64)],
         }
         for name, args in sig.items():

@@ -68,6 +68,7 @@ struct MsgDev {
 // blocks a deep queue of pending launches blocks the issuing thread.
 constexpr uint32_t kInline = 32;
 constexpr uint32_t kInlineBig = 256;
+constexpr uint32_t kInlineTiny = 4;  // 0.5 KiB of parameters: the common KV / NOP-run / token launch
 
 // MsgDev.dir: low byte = channel direction (nonce word 0), this bit = open
 // (verify + decrypt) instead of seal, so one launch can mix both.
@@ -89,6 +90,7 @@ struct KParamsT {
     uint32_t warps_used;   // warps per CTA that own rows (<= kWarpsPerCta)
 };
 using KParams = KParamsT<kInline>;
+using KParamsTiny = KParamsT<kInlineTiny>;
 using KParamsBig = KParamsT<kInlineBig>;
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }

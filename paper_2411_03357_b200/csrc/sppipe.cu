@@ -702,7 +702,9 @@ class Issuer {
     }
     bool on() const { return on_; }
     // Run `fn` now (inline mode) or queue it; returns its sequence number.
-    uint64_t post(std::function<void()> fn) {
+    // `tag` (a string literal) names the call kind for the per-kind
+    // profile (SPPIPE_ISSUER_PROFILE=1 prints it when the plane closes).
+    uint64_t post(std::function<void()> fn, const char *tag = "misc") {
         if (!on_ || g_forked.load(std::memory_order_relaxed)) {
             fn();
             return 0;
@@ -711,7 +713,7 @@ class Issuer {
         uint64_t seq;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            q_.push_back(std::move(fn));
+            q_.push_back(Job{std::move(fn), tag});
             seq = ++posted_;
             posted_seen_.store(seq, std::memory_order_release);
         }
@@ -737,7 +739,7 @@ class Issuer {
     }
     void run() {
         cudaSetDevice(dev_);
-        std::vector<std::function<void()>> batch;
+        std::vector<Job> batch;
         for (;;) {
             // spin ~50 us for the next post before sleeping: a flush posts a
             // burst of calls, and a futex wake-up would add its latency to
@@ -756,13 +758,23 @@ class Issuer {
                 batch.assign(std::make_move_iterator(q_.begin()), std::make_move_iterator(q_.end()));
                 q_.clear();
             }
-            for (auto &fn : batch) {
+            const auto t_batch = std::chrono::steady_clock::now();
+            calls_.fetch_add(batch.size(), std::memory_order_relaxed);
+            for (auto &job : batch) {
+                const auto t_job = profile_ ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
                 try {
-                    fn();
+                    job.fn();
                 } catch (const std::exception &e) {
                     std::lock_guard<std::mutex> lk(mu_);
                     if (err_.empty()) err_ = e.what();
                     failed_.store(true, std::memory_order_release);
+                }
+                if (profile_) {
+                    auto &k = kinds_[job.tag];
+                    k.first++;
+                    k.second += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                    std::chrono::steady_clock::now() - t_job)
+                                    .count();
                 }
                 {
                     std::lock_guard<std::mutex> lk(mu_);
@@ -770,6 +782,10 @@ class Issuer {
                 }
                 cv_done_.notify_all();
             }
+            busy_ns_.fetch_add((uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                   std::chrono::steady_clock::now() - t_batch)
+                                   .count(),
+                               std::memory_order_relaxed);
             batch.clear();
         }
     }
@@ -778,11 +794,32 @@ class Issuer {
     std::thread th_;
     std::mutex mu_;
     std::condition_variable cv_, cv_done_;
-    std::deque<std::function<void()>> q_;
+    struct Job {
+        std::function<void()> fn;
+        const char *tag;
+    };
+    std::deque<Job> q_;
     uint64_t posted_ = 0;
     std::atomic<uint64_t> done_{0}, posted_seen_{0};
     std::atomic<bool> failed_{false}, sleeping_{false}, quit_flag_{false};
     std::string err_;
+
+  public:
+    // CUDA calls issued and the time the worker spent inside them (a worker
+    // busy for most of a run's wall time means the run is issue-bound)
+    std::atomic<uint64_t> calls_{0}, busy_ns_{0};
+    const bool profile_ = [] {
+        const char *e = getenv("SPPIPE_ISSUER_PROFILE");
+        return e && e[0] == '1';
+    }();
+    std::map<std::string, std::pair<uint64_t, uint64_t>> kinds_;  // worker thread only; read after stop()
+    void print_profile() const {
+        if (!profile_) return;
+        for (auto &k : kinds_)
+            fprintf(stderr, "[issuer] %-10s n=%6llu total %8.3f ms  %6.2f us/call\n", k.first.c_str(),
+                    (unsigned long long)k.second.first, k.second.second / 1e6,
+                    k.second.first ? k.second.second / 1e3 / k.second.first : 0.0);
+    }
 };
 
 class Plane {
@@ -926,6 +963,7 @@ class Plane {
             idle = false;
         }
         iss.stop();  // everything below runs inline
+        iss.print_profile();
         ops.clear();
         landings.clear();
         host_ready.clear();
@@ -978,7 +1016,7 @@ class Plane {
     uint64_t record_seq = 0;
     void record(const FenceP &f, cudaStream_t st) {
         const cudaEvent_t ev = f->ev;
-        f->post_seq = iss.post([ev, st] { ck(cudaEventRecord(ev, st), "cudaEventRecord"); });
+        f->post_seq = iss.post([ev, st] { ck(cudaEventRecord(ev, st), "cudaEventRecord"); }, "record");
         f->stream = st;
         f->recorded = true;
         f->seq = ++record_seq;
@@ -993,7 +1031,7 @@ class Plane {
         if (!f->recorded) throw std::logic_error("wait on an unrecorded fence");
         if (f->stream == st) return;  // stream order covers it
         const cudaEvent_t ev = f->ev;
-        iss.post([st, ev] { ck(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent"); });
+        iss.post([st, ev] { ck(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent"); }, "wait");
     }
     // Size classes of the plane's buffer cache: 4 KiB steps up to 1 MiB,
     // then 1 MiB steps (staging sizes repeat: chunks, KV blocks, arenas).
@@ -1001,8 +1039,54 @@ class Plane {
         n = std::max<uint64_t>(n, 16);
         return n <= (1u << 20) ? (n + 4095u) & ~uint64_t(4095) : (n + (1u << 20) - 1) & ~uint64_t((1u << 20) - 1);
     }
+    // Fence completion without a driver call where stream order answers it:
+    // on one stream a fence recorded later completes later, so a completed
+    // fence vouches for every earlier one on its stream, and a pending one
+    // (queried in the last few microseconds) for every later one.  A stale
+    // "pending" only delays a buffer's reuse; it never reports a fence done
+    // early.  cudaEventQuery takes the driver lock the issuing thread needs
+    // for every launch and copy (~1.5 us each).
+    struct StreamDone {
+        cudaStream_t st;
+        uint64_t done_seq, pending_seq;
+        std::chrono::steady_clock::time_point pending_at;
+    };
+    std::vector<StreamDone> stream_done;
+    uint64_t host_queries = 0;  // cudaEventQuery calls of the control plane (diagnostics)
+    StreamDone &stream_state(cudaStream_t st) {
+        for (auto &d : stream_done)
+            if (d.st == st) return d;
+        stream_done.push_back(StreamDone{st, 0, UINT64_MAX, {}});
+        return stream_done.back();
+    }
+    static bool infer_enabled() {  // SPPIPE_INFER_FENCES=0: query every fence (A/B)
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_INFER_FENCES");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
     bool passed(Fence &f) {
-        if (!f.complete && iss.done(f.post_seq) && cudaEventQuery(f.ev) == cudaSuccess) f.complete = true;
+        if (f.complete) return true;
+        if (!f.recorded || !iss.done(f.post_seq)) return false;
+        if (!infer_enabled()) {
+            ++host_queries;
+            if (cudaEventQuery(f.ev) == cudaSuccess) f.complete = true;
+            return f.complete;
+        }
+        StreamDone &sd = stream_state(f.stream);
+        if (f.seq <= sd.done_seq) return f.complete = true;
+        const auto now = std::chrono::steady_clock::now();
+        if (f.seq >= sd.pending_seq && now - sd.pending_at < std::chrono::microseconds(20)) return false;
+        ++host_queries;
+        if (cudaEventQuery(f.ev) == cudaSuccess) {
+            f.complete = true;
+            sd.done_seq = std::max(sd.done_seq, f.seq);
+            if (sd.pending_seq <= f.seq) sd.pending_seq = UINT64_MAX;
+        } else if (f.seq < sd.pending_seq || now - sd.pending_at >= std::chrono::microseconds(20)) {
+            sd.pending_seq = f.seq;
+            sd.pending_at = now;
+        }
         return f.complete;
     }
     // A retired buffer is reusable on stream st without any wait when every
@@ -1126,7 +1210,7 @@ class Plane {
                 if (idle) {
                     void *ptr = v[k].ptr;
                     const cudaStream_t st = s.comp;
-                    iss.post([ptr, st] { ck(cudaFreeAsync(ptr, st), "cudaFreeAsync(trim)"); });
+                    iss.post([ptr, st] { ck(cudaFreeAsync(ptr, st), "cudaFreeAsync(trim)"); }, "free");
                     pool_bytes -= std::min(pool_bytes, kv.first);
                     cached_bytes -= kv.first;
                 } else {
@@ -1159,11 +1243,11 @@ class Plane {
             for (auto &u : x.uses) {
                 if (u.first == fs) continue;
                 const cudaEvent_t ev = (u.second && u.second->recorded) ? u.second->ev : record_new(u.first)->ev;
-                iss.post([fs, ev] { ck(cudaStreamWaitEvent(fs, ev, 0), "cudaStreamWaitEvent(free)"); });
+                iss.post([fs, ev] { ck(cudaStreamWaitEvent(fs, ev, 0), "cudaStreamWaitEvent(free)"); }, "wait");
             }
             x.uses.clear();
             void *ptr = x.ptr;
-            iss.post([ptr, fs] { ck(cudaFreeAsync(ptr, fs), "cudaFreeAsync"); });
+            iss.post([ptr, fs] { ck(cudaFreeAsync(ptr, fs), "cudaFreeAsync"); }, "free");
             pool_bytes -= std::min(pool_bytes, x.size);
         }
         collecting = false;
@@ -1512,7 +1596,7 @@ class Plane {
         const int device = dev;
         iss.post([st, h2d, device, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes)]() mutable {
             issue_copies(st, h2d, device, dsts, srcs, sizes);
-        });
+        }, h2d ? "copy_h2d" : "copy_d2h");
     }
     // Runs on the issuing thread (or inline).
     static void issue_copies(cudaStream_t st, bool h2d, int device, std::vector<void *> &dsts, std::vector<void *> &srcs,
@@ -1571,7 +1655,7 @@ class Plane {
                                          : (kind == 1 ? sp_seal_batch(c, p, n, st) : sp_open_batch(c, p, n, st));
                 ck_sp(rc, what);
             }
-        });
+        }, "launch");
     }
 
     void before_host_read_of(int64_t block_id) {
@@ -1949,7 +2033,7 @@ class Plane {
             iss.post([blocks, st, dst, h, n] {
                 k_bytes<<<blocks, 256, 0, st>>>(dst, h, n);
                 ck(cudaGetLastError(), "k_bytes(app write)");
-            });
+            }, "app_write");
             f = record_new(s.host);
         } else {
             BufP tmp = alloc(n, s.host);
@@ -1957,7 +2041,7 @@ class Plane {
             iss.post([st, t, dst, h, n] {
                 ck(cudaMemcpyAsync(t, h, n, cudaMemcpyHostToDevice, st), "app write H2D");
                 ck(cudaMemcpyAsync(dst, t, n, cudaMemcpyDeviceToHost, st), "app write D2H");
-            });
+            }, "app_write");
             f = record_new(s.host);
             tmp->use(s.host, f, ++tick);
         }
@@ -2045,7 +2129,7 @@ class Plane {
         iss.post([iters, slot, st, grid] {
             k_layer_compute<<<grid, kComputeThreads, 0, st>>>(iters, slot);
             ck(cudaGetLastError(), "k_layer_compute launch");
-        });
+        }, "compute");
         app_fence = record_new(s.app);
         ++compute_launches;
         compute_ns_requested += ns;
@@ -3437,6 +3521,12 @@ int sp_pipe_pool_stats(sp_pipe *p, uint64_t *reserved, uint64_t *used, uint64_t 
     if (reserved) *reserved = r;
     if (used) *used = u;
     if (cached) *cached = pl.cached_bytes;
+    return SP_OK;
+}
+int sp_pipe_issuer_stats(sp_pipe *p, uint64_t *calls, uint64_t *busy_ns, uint64_t *host_queries) {
+    if (calls) *calls = p->e->plane.iss.calls_.load();
+    if (busy_ns) *busy_ns = p->e->plane.iss.busy_ns_.load();
+    if (host_queries) *host_queries = p->e->plane.host_queries;
     return SP_OK;
 }
 int sp_pipe_compute(sp_pipe *p, uint64_t duration_ns) {

@@ -32,8 +32,11 @@ for _ in range(reps):
     if S:
         S.sampler_enable(0)
     pl.append(run_plain_native(kv, cfg, memory=mem).swap_gbs)
-env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("SPPIPE_")) or "default"
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("SPPIPE_", "SPGCM_"))) or "default"
 print(f"{env}: enc {max(enc):.2f} plain {max(pl):.2f} ratio {max(enc) / max(pl):.3f} "
       f"enc runs {[round(x, 1) for x in enc]}", flush=True)
 r = run_engine(kv, cfg, memory=mem)
+print("wall ms", round(r.wall_s * 1e3, 3))
 print("plane stats", r.engine.plane_stats(), {k: v for k, v in r.engine.report().items() if k in ("syncs", "nops", "small_io_h2d", "small_io_d2h", "on_the_fly", "committed_sends", "deferred_decrypts")})
+p = run_plain_native(kv, cfg, memory=mem)
+print("plain wall ms", round(p.wall_s * 1e3, 3), "plain plane stats", p.engine.plane_stats())
