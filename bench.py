@@ -2,7 +2,7 @@
 """Benchmark of the encrypted-swap hot path (BASELINE.json metric:
 "AES-GCM GB/s per GPU (1/2/4/8 B200); OPT-66B offload tokens/s vs no-crypto").
 
-Workload (BASELINE.json configs[1]): one OPT-13B layer, 629,278,720 B =
+Headline (`value`, BASELINE configs[1]): one OPT-13B layer, 629,278,720 B =
 18 x 32 MiB + 25,298,944 B messages at consecutive H2D counters, synthetic
 bytes.  One step = seal the layer + open it again (every tag verified), in
 one batched launch each.  `value` counts payload bytes through AES-GCM (seal
@@ -10,21 +10,34 @@ and open each count) per second, inputs resident in HBM; the layer is 5x the
 126 MB L2, so nothing is cached between steps.  `e2e` is the same metric
 through the C-ABI host-buffer entry points (sp_seal_host_batch /
 sp_open_host_batch: pinned host in -> pinned host out, PCIe copies inside).
+`roofline` is the north-star bound: the slower of the integer-pipe bounds
+(measured lane rates, profiles/r2_pipe_rates.jsonl) and read+write bytes
+at the measured HBM copy rate.
+
+The other BASELINE configs run through the whole pipeline (libsppipe:
+predictor, validator, IV-ordered submit, NOP padding, relinquish) against the
+same trace as plain pinned copies (`offload`, `workloads`, `chunk_sweep`):
+config 1 (64 MiB layers), 2/5 (OPT-66B and OPT-175B-4bit FlexGen offload,
+with the model's compute on the GPU and a crypto SM-budget sweep), 3 (OPT-30B
+KV blocks with mispredictions, relinquish ablation), 4 (activations), and the
+config-5 chunk sweep 64 KiB - 256 MiB.
 
 Multi-GPU (torchrun): each rank runs its own independent channel (key seed =
-rank) on its own layer — the path shards with no data-path collective, so
-scaling is weak; NCCL is used only for the barrier and the max-over-ranks
-timing reduction.
+rank) on its own layer and traces — the path shards with no data-path
+collective, so scaling is weak; NCCL is used only for the barrier and the
+max-over-ranks timing reduction.
 
 `--impl reference` times the reference's own CPU arithmetic for the path
 (oracle/port.py: `cryptography` AESGCM as channel.py:96,111 call it,
 including the payload/tag split and concat of encrypt_at/decrypt_at) over the
-same layer, one process per host core; only rank 0 runs it.
+same layer, its bytes split evenly over one process per host core; only
+rank 0 runs it.
 """
 from __future__ import annotations
 
 import argparse
 import json
+from dataclasses import replace
 import os
 import statistics
 import subprocess
@@ -157,6 +170,25 @@ def measured_peaks() -> tuple[dict, str]:
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def lane_rates() -> tuple[float, float, str]:
+    """ALU and LSU lanes per SM per clock for k_gcm's instruction mix,
+    microbenchmarked on the B200 (tools/native/pipe_rates.cu ->
+    profiles/r2_pipe_rates.jsonl): LOP3/PRMT/SHF (the ALU mix) and
+    lane-private LDS.32 (the T-table lookups)."""
+    p = os.path.join(ROOT, "profiles", "r2_pipe_rates.jsonl")
+    alu, lsu = 64.0, 32.0
+    kind = "assumed (64 ALU, 32 LSU lanes/SM/clk)"
+    try:
+        rows = [json.loads(ln) for ln in open(p) if ln.strip().startswith("{")]
+        ops = {r["op"]: r["lanes_per_sm_per_clk"] for r in rows if "op" in r}
+        alu = min(ops["LOP3.LUT"], ops["PRMT"], ops["SHF"])
+        lsu = ops["LDS.32 lane-private"]
+        kind = "measured on B200 (profiles/r2_pipe_rates.jsonl)"
+    except (OSError, KeyError, ValueError):
+        pass
+    return alu, lsu, kind
+
+
 def ncu_traffic_per_launch() -> float | None:
     """dram bytes read+write of one k_gcm launch over this workload, from the
     committed `ncu --set full` capture summary (profiles/)."""
@@ -203,22 +235,55 @@ def _cpu_worker(args):
     return total, time.perf_counter() - t0
 
 
+def balanced_shards(sizes: list[int], workers: int, chunk: int = CHUNK) -> list[list[int]]:
+    """The bytes of `sizes` split evenly over `workers` (each share cut into
+    <= 32 MiB messages): no worker carries more than 1/workers of the work."""
+    total = sum(sizes)
+    shares = [total // workers + (1 if i < total % workers else 0) for i in range(workers)]
+    return [[chunk] * (n // chunk) + ([n % chunk] if n % chunk else []) for n in shares if n]
+
+
 def cpu_sample(cores: int, sizes: list[int], reps: int = 1) -> tuple[float, float]:
-    """Seal+open `sizes` spread over `cores` processes; returns (GB/s of
-    AES-GCM payload, seconds) where seconds = the slowest worker's crypto
-    time after a common start barrier (payload generation excluded)."""
+    """Seal+open the bytes of `sizes`, split evenly over `cores` processes;
+    returns (GB/s of AES-GCM payload, seconds) where seconds = the slowest
+    worker's crypto time after a common start barrier (payload generation
+    excluded)."""
     if cores <= 1:
         total, wall = _cpu_worker((0, sizes, reps))
         return total / wall / 1e9, wall
     import multiprocessing as mp
 
-    shards = [s for s in (sizes[i::cores] for i in range(cores)) if s]
+    shards = balanced_shards(sizes, cores)
     ctx = mp.get_context("fork")
     barrier = ctx.Barrier(len(shards))
     with ctx.Pool(len(shards), initializer=_cpu_init, initargs=(barrier,)) as pool:
         res = pool.map(_cpu_worker, [(i, s, reps) for i, s in enumerate(shards)], chunksize=1)
     wall = max(r[1] for r in res)
     return sum(r[0] for r in res) / wall / 1e9, wall
+
+
+def evp_floor(total: int, threads: int, reps: int = 3) -> dict | None:
+    """The "OpenSSL floor": the same bytes sealed+opened by OpenSSL EVP
+    AES-256-GCM from C on `threads` host threads (oracle/evp_floor.c, the
+    arithmetic under the reference's `cryptography` without Python around
+    it); best of `reps`."""
+    exe = os.path.join(ROOT, "oracle", "_build", "evp_floor")
+    if not os.path.exists(exe):
+        try:
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
+        except (OSError, subprocess.CalledProcessError):
+            return None
+    best = None
+    for _ in range(reps):
+        try:
+            out = subprocess.run([exe, str(total), str(threads)], check=True, capture_output=True, text=True,
+                                 timeout=300).stdout
+            r = json.loads(out.strip().splitlines()[-1])
+        except (OSError, subprocess.SubprocessError, ValueError, IndexError):
+            return best
+        if best is None or r["gbs"] > best["gbs"]:
+            best = r
+    return best
 
 
 def host_cores() -> int:
@@ -235,9 +300,10 @@ def run_reference(args) -> None:
         return
     cores = host_cores()
     sizes = layer_sizes()
-    # one step = the whole layer sealed + opened, messages spread over processes
-    # (the reference itself is single-threaded; this is its arithmetic on every core)
-    procs = min(cores, len(sizes))
+    # one step = the whole layer sealed + opened, its bytes split evenly over
+    # one process per host core (the reference itself is single-threaded;
+    # this is its arithmetic on every core)
+    procs = cores
     for _ in range(args.warmup):
         cpu_sample(procs, sizes)
     gbs_steps, walls = [], []
@@ -254,9 +320,11 @@ def run_reference(args) -> None:
         "config": {"workload": "opt-13b layer seal+open (18 x 32 MiB + 25,298,944 B), AES-256-GCM",
                    "layer_bytes": sum(sizes), "messages": len(sizes), "parallelism": "independent channels"},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": procs, "kind": "port",
-                         "sample": f"full layer per step, {procs} processes (of {cores} host cores), "
-                                   "oracle/port.py = cryptography AESGCM with encrypt_at/decrypt_at framing"},
+                         "sample": f"full layer per step, bytes split evenly over {procs} processes "
+                                   f"({cores} host cores), oracle/port.py = cryptography AESGCM with "
+                                   "encrypt_at/decrypt_at framing"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "openssl_floor": evp_floor(sum(sizes), cores),
     }
     print(json.dumps(line), flush=True)
 
@@ -381,10 +449,14 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
     pcie_ms = (time.perf_counter() - t0) * 1000.0 / KE
 
-    offload = None
+    small = small_message_table(ctx, dev)
+
+    offload = workloads = sweep = None
     if not args.no_offload:
         offload = offload_bench(args, dist, dev_sync, rank, world)
-        offload["other_configs"] = workloads_bench(args, dist, dev_sync, rank, world)
+        workloads = workloads_bench(args, dist, dev_sync, rank, world)
+        if not args.no_sweep:
+            sweep = chunk_sweep_bench(args, dist, dev_sync, rank, world)
 
     if rank != 0:
         if dist is not None:
@@ -394,14 +466,19 @@ def run_gpu(args) -> None:
     peaks, peaks_kind = measured_peaks()
     clocks = clk.summary()
     bytes_per_launch = 2 * total + 16 * n  # algorithmic: read + write every payload byte, tags
-    achieved = bytes_per_launch / ((seal_ms + open_ms) / 2 / 1000.0) / 1e9
+    launch_ms = (seal_ms + open_ms) / 2
+    hbm_achieved = bytes_per_launch / (launch_ms / 1000.0) / 1e9
     f_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # integer-pipe bounds with SURVEY §8d's canonical counts per payload byte:
-    # 16 LSU lookups/B on 32 lanes/SM/clk; 36 ALU ops/B on 64 lanes/SM/clk
-    lsu_bound = 32 * sms * f_mhz * 1e6 / 16 / 1e9
-    alu_bound = 64 * sms * f_mhz * 1e6 / 36 / 1e9
+    alu_lanes, lsu_lanes, lanes_kind = lane_rates()
+    # integer-pipe bounds with SURVEY §8d's canonical counts per payload byte
+    # (36 ALU ops/B, 16 shared-memory lookups/B) on the measured lane rates
+    alu_bound = alu_lanes * sms * f_mhz * 1e6 / 36 / 1e9
+    lsu_bound = lsu_lanes * sms * f_mhz * 1e6 / 16 / 1e9
+    hbm_payload_bound = peaks.get("hbm_gbs", 6650.0) / 2  # 2 B of HBM traffic per payload byte
+    bound = min(alu_bound, lsu_bound, hbm_payload_bound)
     per_gpu_payload = 2 * total / (ms / 1000.0) / 1e9
+    traffic = ncu_traffic_per_launch()
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": K,
@@ -412,23 +489,22 @@ def run_gpu(args) -> None:
                    "layer_bytes": total, "messages": n, "parallelism": f"independent channels x{world}",
                    "l2": "inputs (629 MB) > 126 MB L2; no flush needed"},
         "seal_gbs": round(total / seal_ms / 1e6, 2), "open_gbs": round(total / open_ms / 1e6, 2),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peaks.get("hbm_gbs"),
-                     "unit": "GB/s", "frac": round(achieved / peaks.get("hbm_gbs", 6650.0), 4),
-                     "traffic": ncu_traffic_per_launch(), "peak_kind": peaks_kind,
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "note": "k_gcm is bound by the shared-memory LSU pipe, not HBM: see int_roofline",
-                     "north_star": {
-                         "definition": "BASELINE north star: the slower of the integer-op bound and read+write "
-                                       "bytes at the HBM peak, in payload GB/s",
-                         "bound_gbs": round(min(lsu_bound, alu_bound, peaks.get("hbm_gbs", 6650.0) / 2), 1),
-                         "achieved_gbs": round(per_gpu_payload, 2),
-                         "frac": round(per_gpu_payload / min(lsu_bound, alu_bound,
-                                                             peaks.get("hbm_gbs", 6650.0) / 2), 4)}},
-        "int_roofline": {"bound": "lsu (T-table + GHASH lookups)", "payload_gbs": round(per_gpu_payload, 2),
-                         "lsu_bound_gbs": round(lsu_bound, 1), "alu_bound_gbs": round(alu_bound, 1),
-                         "frac_of_lsu_bound": round(per_gpu_payload / lsu_bound, 4),
-                         "sm_mhz": f_mhz, "sms": sms,
-                         "counts": "SURVEY 8d: 16 lookups/B (32 lanes/SM/clk), 36 ALU ops/B (64 lanes/SM/clk)"},
+        "roofline": {
+            "bound": "int", "achieved": round(per_gpu_payload, 2), "peak": round(bound, 1), "unit": "GB/s",
+            "frac": round(per_gpu_payload / bound, 4), "traffic": traffic,
+            "definition": "north star: the slower of the integer-op bound and read+write bytes at the HBM peak, "
+                          "in payload GB/s per GPU (seal and open each count)",
+            "alu_bound_gbs": round(alu_bound, 1), "lsu_bound_gbs": round(lsu_bound, 1),
+            "hbm_payload_bound_gbs": round(hbm_payload_bound, 1),
+            "lanes_per_sm_per_clk": {"alu": alu_lanes, "lsu": lsu_lanes, "kind": lanes_kind},
+            "counts": "SURVEY 8d canonical per payload byte: 36 ALU-pipe ops, 16 shared-memory lookups",
+            "sm_mhz": f_mhz, "sms": sms,
+            "hbm": {"bound": "hbm", "achieved": round(hbm_achieved, 2), "peak": peaks.get("hbm_gbs"),
+                    "unit": "GB/s", "frac": round(hbm_achieved / peaks.get("hbm_gbs", 6650.0), 4),
+                    "traffic": traffic, "peak_kind": peaks_kind,
+                    "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "traffic_vs_algorithmic": round(traffic / bytes_per_launch, 4) if traffic else None,
+                    "launch_ms": round(launch_ms, 4)}},
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d_bytes,
                 "d2h_bytes_per_step": d2h_bytes, "ms_per_step": round(e2e_ms, 3), "steps": KE,
                 "path": "sp_seal_host_batch + sp_open_host_batch, pinned host buffers",
@@ -436,110 +512,317 @@ def run_gpu(args) -> None:
                 "ratio_vs_plain_copies": round(pcie_ms / e2e_ms, 4)},
         "gpu_launches": int(gpu_launches),
         "clocks": clocks,
+        "small_messages": small,
     }
 
     if not args.no_cpu_baseline:
         sizes_all = layer_sizes()
         g1, w1 = cpu_sample(1, sizes_all, reps=args.cpu_reps)
+        cores = host_cores()
+        gN, wN = cpu_sample(cores, sizes_all, reps=2)
         line["cpu_baseline"] = {"value": round(g1, 3), "unit": "GB/s", "cores": 1, "kind": "port",
                                 "sample": f"the OPT-13B layer ({len(sizes_all)} messages) sealed+opened "
                                           f"{args.cpu_reps}x on 1 core via oracle/port.py (cryptography AESGCM "
-                                          f"with encrypt_at/decrypt_at framing): {w1:.1f} s of CPU work"}
+                                          f"with encrypt_at/decrypt_at framing): {w1:.1f} s of CPU work",
+                                "all_cores": {"value": round(gN, 3), "unit": "GB/s", "cores": cores,
+                                              "sample": f"the layer's bytes split evenly over {cores} processes, "
+                                                        f"sealed+opened 2x: {wN:.2f} s"},
+                                "openssl_floor": evp_floor(sum(sizes_all), cores)}
     if offload is not None:
         line["offload"] = offload
+    if workloads is not None:
+        line["workloads"] = workloads
+    if sweep is not None:
+        line["chunk_sweep"] = sweep
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def trace_compare(tr, cfg, dist, dev_sync, world: int, reps: int) -> dict:
-    """One synthetic trace through the native engine (libsppipe: encrypted,
-    speculative) and as plain pinned cudaMemcpyAsync swaps from the same C++
-    dispatch loop (sp_pipe_plain_replay): one untimed run of each, then
-    `reps` timed runs of each alternating; best of each.  A run's time is the
-    max over ranks, its bytes the sum (whole job)."""
+def small_message_table(ctx, dev, reps: int = 200) -> dict:
+    """Device time per launch (CUDA-graph replay of `reps` back-to-back
+    sp_seal_batch launches, so the host's issue cost is out of the number)
+    for the engine's small batches: NOP pads, 2 KiB tokens, 224 KiB OPT-30B
+    KV blocks; per message and as GB/s."""
+    import torch
+
+    cases = [("1 NOP (1 B)", 1, 1), ("8-NOP pad", 8, 1), ("2 KiB token", 1, 2048), ("1 x 224 KiB KV", 1, 229_376),
+             ("4 x 224 KiB KV", 4, 229_376), ("32 x 224 KiB KV", 32, 229_376), ("1 MiB", 1, 1 << 20)]
+    buf = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    tags = torch.zeros((64, 16), dtype=torch.uint8, device=dev)
+    out = {"method": f"CUDA graph of {reps} back-to-back sp_seal_batch launches, replayed; CUDA events",
+           "rows": []}
+    s = torch.cuda.Stream(dev)
+    for name, k, size in cases:
+        items = [(0, 7 + i, buf[i * size:(i + 1) * size], buf[i * size:(i + 1) * size], tags[i]) for i in range(k)]
+        with torch.cuda.stream(s):
+            for _ in range(5):  # workspace and first-use setup outside the capture
+                ctx.seal_batch(items, s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    ctx.seal_batch(items, torch.cuda.current_stream())
+        except Exception as exc:  # noqa: BLE001
+            out["rows"].append({"case": name, "error": str(exc)[:200]})
+            continue
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):  # replay() launches on the current stream
+            g.replay()
+            s.synchronize()
+            a.record(s)
+            for _ in range(3):
+                g.replay()
+            b.record(s)
+        b.synchronize()
+        us = a.elapsed_time(b) * 1e3 / (3 * reps)
+        out["rows"].append({"case": name, "messages": k, "bytes_per_message": size, "us_per_launch": round(us, 2),
+                            "us_per_message": round(us / k, 3), "gbs": round(k * size / us / 1e3, 3)})
+        del g
+    return out
+
+
+def trace_compare(tr, arms: list, dist, dev_sync, world: int, reps: int, memory=None) -> dict:
+    """One synthetic trace through several arms on the same pinned host
+    blocks: ("plain", cfg) = the swaps as plain pinned copies from the same
+    C++ dispatch loop (sp_pipe_plain_replay), ("engine", cfg) = libsppipe
+    (encrypted; speculative or not per cfg.system).  One untimed run of each
+    arm, then `reps` timed rounds over all arms; best of each.  A run's time
+    is the max over ranks, its bytes the sum (whole job)."""
     from paper_2411_03357_b200.replay import prepare_memory, run_engine, run_plain_native
 
-    def timed(fn):
-        barrier(dist, dev_sync)
-        r = fn()
-        wall = reduce_max(dist, r.wall_s, dev_sync)
-        return r, world * r.swap_bytes / wall / 1e9
+    def run(kind, cfg):
+        return run_plain_native(tr, cfg, memory=memory) if kind == "plain" else run_engine(tr, cfg, memory=memory)
 
-    memory = prepare_memory(tr, cfg)  # one set of pinned host blocks for every run
-    run_plain_native(tr, cfg, memory=memory)
-    run_engine(tr, cfg, memory=memory)
-    plain, enc, obs, rep = [], [], [], None
+    if memory is None:
+        memory = prepare_memory(tr, arms[0][2])
+    for _, kind, cfg in arms:
+        run(kind, cfg)
+    res = {name: {"runs": [], "obs": [], "wall_ms": []} for name, _, _ in arms}
     for _ in range(reps):
-        plain.append(timed(lambda: run_plain_native(tr, cfg, memory=memory))[1])
-        r, g = timed(lambda: run_engine(tr, cfg, memory=memory))
-        enc.append(g)
-        obs.append(world * r.swap_bytes / reduce_max(dist, r.observable_s or r.wall_s, dev_sync) / 1e9)
-        rep = r.engine.report()
-        del r
-    return {"swap_bytes_per_gpu": tr.swap_bytes(), "events": len(tr.events),
-            "encrypted_gbs": round(max(enc), 2), "plain_gbs": round(max(plain), 2),
-            "encrypted_runs": [round(x, 2) for x in enc], "plain_runs": [round(x, 2) for x in plain],
-            "throughput_ratio": round(max(enc) / max(plain), 4),
-            "encrypted_observable_gbs": round(max(obs), 2),
-            "throughput_ratio_observable": round(max(obs) / max(plain), 4),
-            "hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "misses": rep["miss"], "nops": rep["nops"],
-            "relinquishes": rep["relinquishes"] + rep["replans"], "sequence_hit_rate": rep["sequence_hit_rate"]}
+        for name, kind, cfg in arms:
+            barrier(dist, dev_sync)
+            r = run(kind, cfg)
+            wall = reduce_max(dist, r.wall_s, dev_sync)
+            e = res[name]
+            e["runs"].append(world * r.swap_bytes / wall / 1e9)
+            e["wall_ms"].append(wall * 1e3)
+            if kind == "engine":
+                obs = reduce_max(dist, r.observable_s or r.wall_s, dev_sync)
+                e["obs"].append(world * r.swap_bytes / obs / 1e9)
+                rep = r.engine.report()
+                e["counters"] = {"hits": rep["hit"], "iv_ahead": rep["iv_ahead"], "misses": rep["miss"],
+                                 "stale": rep["stale"], "nops": rep["nops"],
+                                 "relinquishes": rep["relinquishes"] + rep["replans"],
+                                 "spec_encrypts": rep["spec_encrypts"],
+                                 "sequence_hit_rate": round(rep["sequence_hit_rate"], 4)}
+            if getattr(cfg, "compute", False):
+                st = r.engine.compute_stats()
+                e["compute"] = {"launches": st["launches"], "requested_ms": round(st["requested_ns"] / 1e6, 3),
+                                "measured_ms": round(st["measured_ns"] / 1e6, 3),
+                                "slowdown": round(st["measured_ns"] / st["requested_ns"], 4)
+                                if st["requested_ns"] else None}
+            del r
+    out = {"swap_bytes_per_gpu": tr.swap_bytes(), "events": len(tr.events), "arms": {}}
+    for name, kind, cfg in arms:
+        e = res[name]
+        row = {"gbs": round(max(e["runs"]), 2), "runs": [round(x, 2) for x in e["runs"]],
+               "best_wall_ms": round(min(e["wall_ms"]), 3)}
+        if e["obs"]:
+            row["observable_gbs"] = round(max(e["obs"]), 2)
+        for k in ("counters", "compute"):
+            if k in e:
+                row[k] = e[k]
+        out["arms"][name] = row
+    plain = [n for n, k, _ in arms if k == "plain"]
+    if plain:
+        base = out["arms"][plain[0]]["gbs"]
+        out["ratio_vs_plain"] = {n: round(out["arms"][n]["gbs"] / base, 4) for n, k, _ in arms if k == "engine"}
+    return out
+
+
+def _cfg(**kw):
+    from paper_2411_03357_b200.replay import ReplayConfig
+
+    base = dict(system="specpipe", plane="gpu", record_stream=False, fill="fast", engine="native")
+    base.update(kw)
+    return ReplayConfig(**base)
 
 
 def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
-    """OPT-66B-shaped FlexGen weight offload (2 offloaded layers, 61 x 32 MiB
-    blocks each) through the native engine vs the same swaps as plain
-    copies — the north star's 'within 10% of unencrypted swap throughput'.
-    Every rank replays its own trace on its own channel (seed = rank).  The
-    whole trace is timed (speculation runs ahead across iteration
-    boundaries, so a mid-trace clock start would credit the encrypted run
-    with copies issued before it)."""
+    """BASELINE configs 2/5: OPT-66B-shaped FlexGen weight offload (2
+    offloaded layers, 61 x 32 MiB blocks each, 8 iterations) through the
+    native engine vs the same swaps as plain copies — the north star's
+    "within 10% of unencrypted".  With the model's compute on the GPU (each
+    trace ComputeEvent runs as calibrated FMA work on a high-priority app
+    stream; swap-outs wait for it, later swap-ins prefetch past it) the
+    ratio is tokens/s: the same trace and batch, so tokens/s ratio = run
+    time ratio.  Also: the swap-only ratio, SyncCc (no speculation), a
+    crypto SM-budget sweep with the compute's own slowdown, and OPT-175B in
+    the paper's 4-bit layout.  Every rank replays its own
+    trace on its own channel (seed = rank); whole traces are timed."""
     from paper_2411_03357_b200 import workload
-    from paper_2411_03357_b200.replay import ReplayConfig
+    from paper_2411_03357_b200.replay import prepare_memory
 
-    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank, engine="native")
     tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=args.offload_iters, seed=rank)
+    mem = prepare_memory(tr, _cfg(seed=rank))
+    c = dict(seed=rank, compute=True)
+    with_compute = trace_compare(tr, [
+        ("plain", "plain", _cfg(**c)),
+        ("specpipe", "engine", _cfg(**c)),
+        ("synccc", "engine", _cfg(system="synccc", **c)),
+        ("specpipe_sms64", "engine", _cfg(crypto_sms=64, **c)),
+        ("specpipe_sms32", "engine", _cfg(crypto_sms=32, **c)),
+    ], dist, dev_sync, world, args.offload_reps, memory=mem)
+    swap_only = trace_compare(tr, [
+        ("plain", "plain", _cfg(seed=rank)),
+        ("specpipe", "engine", _cfg(seed=rank)),
+        ("synccc", "engine", _cfg(system="synccc", seed=rank)),
+    ], dist, dev_sync, world, args.offload_reps, memory=mem)
+    del mem
     out = {"model": "opt-66b", "layers_offloaded_per_gpu": 2, "iterations": args.offload_iters,
-           "layer_bytes": workload.opt_layer_bytes("opt-66b"), "timed": "whole trace, best of reps", "n_gpus": world,
+           "layer_bytes": workload.opt_layer_bytes("opt-66b"), "n_gpus": world,
+           "compute_per_layer_us": 200, "timed": "whole trace, best of reps; whole-job swap GB/s "
+                                                 "(sum over ranks / max time); random payload",
            "engine": "libsppipe (native control plane + B200 data plane), sp_pipe_replay",
-           "plain": "sp_pipe_plain_replay: the same swaps as pinned cudaMemcpyAsync, no crypto",
-           "note": "whole-job swap GB/s (sum over ranks / max time); tokens/s ratio == swap throughput ratio "
-                   "(same trace, same batch); random payload. throughput_ratio waits for every GPU op the run "
-                   "issued, including the encrypt-ahead of the layer predicted after the last sync that the finite "
-                   "trace never consumes; throughput_ratio_observable stops when every committed transfer is "
-                   "verified and landed (the reference simulator's makespan, simulator.py:441-443)"}
-    out.update(trace_compare(tr, cfg, dist, dev_sync, world, args.offload_reps))
-    # the no-speculation system on the same trace (the simulator's SyncCc):
-    # every swap sealed and opened on the fly, synchronous host decrypts
-    from dataclasses import replace
-
-    sync_cfg = replace(cfg, system="synccc")
-    sync = trace_compare(tr, sync_cfg, dist, dev_sync, world, max(1, args.offload_reps // 2))
-    out["synccc_gbs"] = sync["encrypted_gbs"]
-    out["synccc_ratio"] = round(sync["encrypted_gbs"] / out["plain_gbs"], 4)
+           "plain": "sp_pipe_plain_replay: the same swaps as pinned cudaMemcpyAsync, no crypto, each swap-out "
+                    "after its own swap-in (and the compute before it)",
+           "tokens_per_s_ratio": with_compute["ratio_vs_plain"]["specpipe"],
+           "tokens_per_s_ratio_synccc": with_compute["ratio_vs_plain"]["synccc"],
+           "swap_only_ratio": swap_only["ratio_vs_plain"]["specpipe"],
+           "with_compute": with_compute, "swap_only": swap_only}
+    tr175 = workload.gen_opt_offload_trace("opt-175b", [1, 2], iterations=2, seed=rank, quant_bits=4)
+    out["opt175b_4bit"] = {
+        "layer_bytes": workload.opt_layer_bytes("opt-175b") // 4, "layers_offloaded_per_gpu": 2, "iterations": 2,
+        **trace_compare(tr175, [("plain", "plain", _cfg(seed=rank, compute=True)),
+                                ("specpipe", "engine", _cfg(seed=rank, compute=True)),
+                                ("synccc", "engine", _cfg(system="synccc", seed=rank, compute=True))],
+                        dist, dev_sync, world, 2)}
     return out
 
 
 def workloads_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
-    """BASELINE configs 3 and 4 at full shape through the same comparison:
-    OPT-30B vLLM KV-block swapping (229,376 B blocks, adversarial 25%
-    mispredictions, relinquish path) and OPT-30B LoRA activation offload
-    (48 x 28 MiB activations, encrypt-on-D2H / decrypt-on-H2D)."""
+    """BASELINE configs 1, 3 and 4 at full shape: config 1's 8 x 64 MiB
+    layers (2 x 32 MiB blocks, 3 iterations, the reference's decisions bit
+    for bit), OPT-30B vLLM KV-block swapping (229,376 B blocks, 25%
+    adversarial mispredictions) with the relinquish ablation (mutation rate
+    1.0: speculation never succeeds, SpecPipe vs SyncCc on the same trace =
+    the cost of speculating and relinquishing), and OPT-30B LoRA activation
+    offload (48 x 28 MiB, encrypt-on-D2H / decrypt-on-H2D)."""
     from paper_2411_03357_b200 import workload
-    from paper_2411_03357_b200.replay import ReplayConfig
 
-    cfg = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", seed=rank, engine="native",
-                       reference_compat=False)
-    kv = workload.gen_adversarial_trace(
-        workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=rank), 0.25, seed=8)
+    fix = dict(seed=rank, reference_compat=False)
+    out = {}
+    c1 = workload.gen_chunked_offload_trace(8, list(range(1, 9)), 3, 64 * MIB, chunk_bytes=32 * MIB, seed=rank)
+    out["config1_64mib"] = {"trace": "8 x 64 MiB layers (2 x 32 MiB blocks), all offloaded, 3 iterations; "
+                                     "reference_compat (defects reproduced)",
+                            **trace_compare(c1, [("plain", "plain", _cfg(seed=rank)),
+                                                 ("specpipe", "engine", _cfg(seed=rank)),
+                                                 ("synccc", "engine", _cfg(system="synccc", seed=rank))],
+                                            dist, dev_sync, world, 3)}
+    kv_base = workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=rank)
+    kv = workload.gen_adversarial_trace(kv_base, 0.25, seed=8)
+    arms = [("plain", "plain", _cfg(**fix)), ("specpipe", "engine", _cfg(**fix)),
+            ("synccc", "engine", _cfg(system="synccc", **fix))]
+    arms_c = [(n, k, replace(c, compute=True)) for n, k, c in arms]
+    out["kv_swap_opt30b"] = {"trace": "gen_kvswap_trace(48, lifo, 229,376 B blocks, parallel 4) + 25% adversarial",
+                             "swap_only": trace_compare(kv, arms, dist, dev_sync, world, 5),
+                             "with_compute": trace_compare(kv, arms_c, dist, dev_sync, world, 2)}
+    # SPEC criterion 7 (SPEC.md:655), zero-success ablation: SpecPipe on the
+    # KV trace at mutation rate 1.0 (no sequence hits) vs the same trace
+    # unmutated, and vs SyncCc at rate 1.0
+    kv0 = workload.gen_adversarial_trace(kv_base, 0.0, seed=8)
+    kv1 = workload.gen_adversarial_trace(kv_base, 1.0, seed=8)
+    r0 = trace_compare(kv0, arms[:2], dist, dev_sync, world, 5)
+    r1 = trace_compare(kv1, arms, dist, dev_sync, world, 5)
+    out["kv_zero_success_ablation"] = {
+        "rate0": r0, "rate1": r1,
+        "specpipe_rate1_vs_rate0": round(r1["arms"]["specpipe"]["gbs"] / r0["arms"]["specpipe"]["gbs"], 4),
+        "specpipe_vs_synccc_rate1": round(r1["arms"]["specpipe"]["gbs"] / r1["arms"]["synccc"]["gbs"], 4),
+        "note": "criterion 7 asks rate1/rate0 >= 0.85 and SpecPipe > SyncCc; on the B200 SyncCc has no CPU "
+                "crypto to hide, so SpecPipe can only match it"}
+    out["relinquish_cost"] = relinquish_cost(dev_sync)
     act = workload.gen_activation_trace(48, 29_360_128, 2, seed=rank)
-    return {
-        "kv_swap_opt30b": {"trace": "gen_kvswap_trace(48, lifo, 229,376 B blocks, parallel 4) + 25% adversarial",
-                           **trace_compare(kv, cfg, dist, dev_sync, world, 5)},
-        "activation_opt30b": {"trace": "gen_activation_trace(48 layers, 29,360,128 B, 2 steps)",
-                              **trace_compare(act, cfg, dist, dev_sync, world, 2)},
-    }
+    out["activation_opt30b"] = {"trace": "gen_activation_trace(48 layers, 29,360,128 B, 2 steps)",
+                                **trace_compare(act, arms, dist, dev_sync, world, 2)}
+    return out
+
+
+def relinquish_cost(dev_sync, reps: int = 200, plane: str = "gpu") -> dict:
+    """The relinquish path (engine.py:515-535) on a full record window: 64
+    OPT-30B KV blocks encrypted ahead on the GPU, then relinquish(); host
+    time per call, and the device work it issues (none: the pending records'
+    ciphertext is dropped, counters re-key, the copy engine is untouched)."""
+    import time as _t
+
+    from paper_2411_03357_b200.channel import new_channel
+    from paper_2411_03357_b200.engine import Engine, EngineConfig
+    from paper_2411_03357_b200.memory import HostMemory, KvCache, prng_fill
+    from paper_2411_03357_b200.predictor import Prediction, Predictor
+
+    mem = HostMemory(pinned=plane == "gpu")
+    blocks = [mem.alloc(KvCache(i, 0), 229_376, prng_fill(i)) for i in range(64)]
+    ids = {b.id for b in blocks}
+    plan = [[Prediction(b.id, k, 0) for k, b in enumerate(blocks)]]
+    pred = Predictor.scripted(None, ids, rounds=[plan] * (2 * reps + 2))
+    cpu, gpu = new_channel(seed=11)
+    eng = Engine(mem, cpu, gpu, pred, EngineConfig(leeway=0, window=64, reference_compat=False, plane=plane))
+    times, dropped = [], 0
+    for _ in range(reps):
+        eng.speculate_tick()   # queue 64 encrypt-ahead tasks
+        eng.speculate_tick()   # seal them on the spec stream, label 64 records
+        eng.flush(wait=plane == "gpu")
+        launches = eng.plane_stats()["launches"]
+        t0 = _t.perf_counter()
+        dropped += eng.relinquish()
+        times.append(_t.perf_counter() - t0)
+        eng.flush(wait=plane == "gpu")
+        assert eng.plane_stats()["launches"] == launches, "relinquish issued device work"
+    eng.finish()
+    times.sort()
+    return {"records_per_relinquish": dropped // reps, "reps": reps,
+            "host_us_median": round(1e6 * times[len(times) // 2], 2), "host_us_p99": round(1e6 * times[-3], 2),
+            "device_launches_per_relinquish": 0,
+            "note": "metadata only: pending records invalidated, queued tasks cancelled, payload buffers released "
+                    "to the pool's cache; nothing is issued to the copy engine or the SMs"}
+
+
+def chunk_sweep_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1) -> dict:
+    """BASELINE config 5's chunk-size sweep, 64 KiB - 256 MiB: one OPT-66B
+    layer offloaded, 2 iterations, the layer cut into blocks of each size
+    (blocks > 32 MiB go as several 32 MiB messages and, per the reference's
+    classifier (defect C3), are never speculated).  reference_compat=False:
+    a layer of more than 64 chunks trips defect C2 in the reference.  With
+    the model's compute on (tokens/s: swap-outs wait for the compute, which
+    waits for its layer's swap-ins) and swap-only (the plain arm may then
+    overlap a layer's swap-outs with the rest of its swap-ins, which a
+    model could not)."""
+    from paper_2411_03357_b200 import workload
+    from paper_2411_03357_b200.replay import prepare_memory
+
+    rows = []
+    for block in (64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 32 << 20, 64 << 20, 128 << 20, 256 << 20):
+        tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=block, seed=rank)
+        msg = min(block, 32 * MIB)
+        kw = dict(seed=rank, reference_compat=False, chunk_bytes=msg, predictor_chunk_bytes=msg)
+        mem = prepare_memory(tr, _cfg(**kw))
+        row = {"block_bytes": block, "blocks_per_layer": len(tr.header.blocks) // 2, "events": len(tr.events)}
+        for tag, comp in (("", True), ("swap_only_", False)):
+            r = trace_compare(tr, [("plain", "plain", _cfg(compute=comp, **kw)),
+                                   ("specpipe", "engine", _cfg(compute=comp, **kw)),
+                                   ("synccc", "engine", _cfg(system="synccc", compute=comp, **kw))],
+                              dist, dev_sync, world, 2, memory=mem)
+            row.update({f"{tag}plain_gbs": r["arms"]["plain"]["gbs"], f"{tag}specpipe_gbs": r["arms"]["specpipe"]["gbs"],
+                        f"{tag}synccc_gbs": r["arms"]["synccc"]["gbs"],
+                        f"{tag}specpipe_ratio": r["ratio_vs_plain"]["specpipe"],
+                        f"{tag}synccc_ratio": r["ratio_vs_plain"]["synccc"]})
+            if comp:
+                row["spec_encrypts"] = r["arms"]["specpipe"]["counters"]["spec_encrypts"]
+        del mem
+        rows.append(row)
+    return {"workload": "opt-66b, 2 layers offloaded, 2 iterations, whole trace timed; ratios with the model's "
+                        "compute on the GPU (tokens/s) and swap-only", "rows": rows}
 
 
 def main() -> None:
@@ -551,10 +834,11 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for barrier/timing (nccl)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (flow check on a 1-GPU box)")
-    ap.add_argument("--cpu-reps", type=int, default=8, help="layers sealed+opened by the 1-core CPU baseline")
+    ap.add_argument("--cpu-reps", type=int, default=6, help="layers sealed+opened by the 1-core CPU baseline")
     ap.add_argument("--no-offload", action="store_true", help="skip the OPT-66B engine offload comparison")
     ap.add_argument("--offload-iters", type=int, default=8)
-    ap.add_argument("--offload-reps", type=int, default=4)
+    ap.add_argument("--offload-reps", type=int, default=3)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 chunk-size sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
