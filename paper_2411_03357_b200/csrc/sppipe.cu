@@ -812,11 +812,11 @@ class Issuer {
         const char *e = getenv("SPPIPE_ISSUER_PROFILE");
         return e && e[0] == '1';
     }();
-    std::map<std::string, std::pair<uint64_t, uint64_t>> kinds_;  // worker thread only; read after stop()
+    std::map<const char *, std::pair<uint64_t, uint64_t>> kinds_;  // tags are literals; worker thread only
     void print_profile() const {
         if (!profile_) return;
         for (auto &k : kinds_)
-            fprintf(stderr, "[issuer] %-10s n=%6llu total %8.3f ms  %6.2f us/call\n", k.first.c_str(),
+            fprintf(stderr, "[issuer] %-16s n=%6llu total %8.3f ms  %6.2f us/call\n", k.first,
                     (unsigned long long)k.second.first, k.second.second / 1e6,
                     k.second.first ? k.second.second / 1e3 / k.second.first : 0.0);
     }
@@ -1014,16 +1014,16 @@ class Plane {
         return f;
     }
     uint64_t record_seq = 0;
-    void record(const FenceP &f, cudaStream_t st) {
+    void record(const FenceP &f, cudaStream_t st, const char *tag = "record") {
         const cudaEvent_t ev = f->ev;
-        f->post_seq = iss.post([ev, st] { ck(cudaEventRecord(ev, st), "cudaEventRecord"); }, "record");
+        f->post_seq = iss.post([ev, st] { ck(cudaEventRecord(ev, st), "cudaEventRecord"); }, tag);
         f->stream = st;
         f->recorded = true;
         f->seq = ++record_seq;
     }
-    FenceP record_new(cudaStream_t st) {
+    FenceP record_new(cudaStream_t st, const char *tag = "record") {
         FenceP f = new_fence();
-        record(f, st);
+        record(f, st, tag);
         return f;
     }
     void wait(cudaStream_t st, const FenceP &f) {
@@ -1116,7 +1116,7 @@ class Plane {
             if (!sl || sl->off + need > sl->big->size) {
                 sl = pmake<Slab>();
                 sl->big = alloc_whole(kSlabBytes, st);
-                sl->born = record_new(st);
+                sl->born = record_new(st, "rec_slab");
             }
             auto b = pmake<Buf>();
             b->plane = this;
@@ -1242,7 +1242,7 @@ class Plane {
             cudaStream_t fs = x.last;
             for (auto &u : x.uses) {
                 if (u.first == fs) continue;
-                const cudaEvent_t ev = (u.second && u.second->recorded) ? u.second->ev : record_new(u.first)->ev;
+                const cudaEvent_t ev = (u.second && u.second->recorded) ? u.second->ev : record_new(u.first, "rec_free")->ev;
                 iss.post([fs, ev] { ck(cudaStreamWaitEvent(fs, ev, 0), "cudaStreamWaitEvent(free)"); }, "wait");
             }
             x.uses.clear();
@@ -1393,7 +1393,7 @@ class Plane {
                                 u.second->mark = mk;
                             }
                         } else {
-                            if (!alloc_point) alloc_point = record_new(other);
+                            if (!alloc_point) alloc_point = record_new(other, "rec_alloc_point");
                             if (alloc_point->mark != mk) {
                                 wait(cs, alloc_point);
                                 alloc_point->mark = mk;
@@ -1421,7 +1421,7 @@ class Plane {
                 post_batch(0, descs, cs, "sp_crypt_batch");
                 ++launches;
             }
-            record(window, cs);
+            record(window, cs, "rec_flush");
             ++tick;
             for (auto &op : q) {
                 if (op.a) {
@@ -1527,7 +1527,7 @@ class Plane {
             }
         post_batch(2, descs, s.land, "sp_open_batch(landing)");
         ++launches;
-        FenceP opened = record_new(s.land);
+        FenceP opened = record_new(s.land, "rec_land");
         ++tick;
         buf->use(s.land, opened, tick);
         for (auto &l : ls)
@@ -1548,7 +1548,7 @@ class Plane {
             src = buf->ptr + places[i].off;
             n = places[i].n;
         });
-        FenceP ev = record_new(s.d2h);
+        FenceP ev = record_new(s.d2h, "rec_d2h");
         buf->use(s.d2h, ev, ++tick);
         for (auto &l : ls) host_ready[l.block->id] = ev;
         bytes_d2h += total;
@@ -1565,7 +1565,7 @@ class Plane {
             src = cb.src[i];
             n = cb.n[i];
         });
-        record(cb.fence, s.h2d);
+        record(cb.fence, s.h2d, "rec_copy");
         ++tick;
         for (auto &b : cb.keep) b->use(s.h2d, cb.fence, tick);
         cb.dst.clear();
@@ -1779,7 +1779,7 @@ class Plane {
             p->wait(p->s.spec, last_copy);
             p->post_batch(1, items, p->s.spec, "sp_seal_batch(spec)");
             ++p->launches;
-            p->record(ready, p->s.spec);
+            p->record(ready, p->s.spec, "rec_spec");
             ++p->tick;
             for (auto &b : bufs) b->use(p->s.spec, ready, p->tick);
             items.clear();
@@ -1879,7 +1879,7 @@ class Plane {
             if (seen.insert(f.get()).second) wait(s.out, f);
         post_batch(1, outb.items, s.out, "sp_seal_batch(swap-out)");
         ++launches;
-        record(outb.ready, s.out);
+        record(outb.ready, s.out, "rec_out");
         ++tick;
         for (auto &b : outb.bufs) {
             b->use(s.out, outb.ready, tick);
@@ -2034,7 +2034,7 @@ class Plane {
                 k_bytes<<<blocks, 256, 0, st>>>(dst, h, n);
                 ck(cudaGetLastError(), "k_bytes(app write)");
             }, "app_write");
-            f = record_new(s.host);
+            f = record_new(s.host, "rec_host");
         } else {
             BufP tmp = alloc(n, s.host);
             uint8_t *t = tmp->ptr, *dst = b.host + offset;
@@ -2042,7 +2042,7 @@ class Plane {
                 ck(cudaMemcpyAsync(t, h, n, cudaMemcpyHostToDevice, st), "app write H2D");
                 ck(cudaMemcpyAsync(dst, t, n, cudaMemcpyDeviceToHost, st), "app write D2H");
             }, "app_write");
-            f = record_new(s.host);
+            f = record_new(s.host, "rec_host");
             tmp->use(s.host, f, ++tick);
         }
         ring_commit(h, n, f);
@@ -2095,13 +2095,18 @@ class Plane {
         cudaStreamDestroy(st);
         return cal[dev] = best / (double)iters;
     }
-    void mark_compute_inputs() {
-        if (dry) return;
-        compute_inputs[0] = record_new(s.comp);
-        compute_inputs[1] = record_new(s.comp2);
-    }
+    // Marked at every sync, recorded lazily by the next compute: everything
+    // issued on the compute streams by then includes the batch's swap-ins
+    // (a trace without compute costs no event records).
+    bool compute_inputs_dirty = false;
+    void mark_compute_inputs() { compute_inputs_dirty = true; }
     void compute(uint64_t ns, const FenceP *deps, int ndeps) {
         if (dry || !ns) return;
+        if (deps == compute_inputs && compute_inputs_dirty) {
+            compute_inputs[0] = record_new(s.comp, "rec_compute");
+            compute_inputs[1] = record_new(s.comp2, "rec_compute");
+            compute_inputs_dirty = false;
+        }
         int sms = 148;
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
         const double per_iter = compute_ns_per_iter(dev, sms);
@@ -2130,7 +2135,7 @@ class Plane {
             k_layer_compute<<<grid, kComputeThreads, 0, st>>>(iters, slot);
             ck(cudaGetLastError(), "k_layer_compute launch");
         }, "compute");
-        app_fence = record_new(s.app);
+        app_fence = record_new(s.app, "rec_compute");
         ++compute_launches;
         compute_ns_requested += ns;
     }
@@ -2990,7 +2995,7 @@ class Engine {
                 src = q.src[i];
                 k = q.n[i];
             });
-            FenceP f = pl.record_new(st);
+            FenceP f = pl.record_new(st, "rec_plain");
             ++pl.tick;
             for (auto &b : q.keep) b->use(st, f, pl.tick);
             for (auto &r : q.ring) pl.ring_commit(r.first, r.second, f);
