@@ -44,6 +44,8 @@
 #include <unordered_set>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "spgcm.h"
 #include "spguard.h"
 #include "sppipe.h"
@@ -93,6 +95,38 @@ __global__ void __launch_bounds__(kComputeThreads) k_layer_compute(uint64_t iter
         atomicMin(slot + 1, ~t1);
         if (acc == -1.0f) slot[0] = 0;  // never: keeps the FMA chains live
     }
+}
+
+// ---- NVTX (SURVEY §5 tracing) ----------------------------------------------------
+// Domain "sppipe": a range per engine entry point (payload = the channel's
+// H2D send counter at entry) and a mark per message put on the wire (name =
+// direction and kind, payload = its counter), so nsys / ncu timelines line
+// the control plane up with the kernels and copies.  NVTX3 is header-only:
+// without an attached tool every call is a null check.
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("sppipe");
+    return d;
+}
+inline nvtxEventAttributes_t nvtx_attr(const char *msg, uint64_t payload) {
+    nvtxEventAttributes_t a{};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = msg;
+    a.payloadType = NVTX_PAYLOAD_TYPE_UNSIGNED_INT64;
+    a.payload.ullValue = payload;
+    return a;
+}
+struct NvtxRange {
+    NvtxRange(const char *msg, uint64_t payload) {
+        nvtxEventAttributes_t a = nvtx_attr(msg, payload);
+        nvtxDomainRangePushEx(nvtx_domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
+inline void nvtx_mark(const char *msg, uint64_t payload) {
+    nvtxEventAttributes_t a = nvtx_attr(msg, payload);
+    nvtxDomainMarkEx(nvtx_domain(), &a);
 }
 
 // ---- error classes (Python exception names) -----------------------------------
@@ -2382,6 +2416,7 @@ class Engine {
 
     // -- channel (channel.py:146-215) --
     void send(int dir, const MsgP &m) {
+        nvtx_mark(dir == H2D ? (m->nop ? "h2d nop" : "h2d msg") : (m->nop ? "d2h nop" : "d2h msg"), send_iv[dir]);
         lanes[dir].log.push_back({send_iv[dir], m->len, m->nop ? 1 : 0, 0});
         lanes[dir].queue.push_back(m);
         send_iv[dir] += 1;
@@ -2532,6 +2567,7 @@ class Engine {
 
     // -- host-to-device (engine.py:295-349) --
     int submit_h2d(const Req &r, uint64_t &sq) {
+        NvtxRange nvtx_("submit_h2d", send_iv[H2D]);
         complete_spec_tasks();
         sq = seq();
         if (r.cls == TC_SMALL) {
@@ -2597,6 +2633,7 @@ class Engine {
 
     // -- device-to-host (engine.py:353-393) --
     uint64_t submit_d2h(const Req &r) {
+        NvtxRange nvtx_("submit_d2h", send_iv[H2D]);
         complete_spec_tasks();
         if (pending(H2D)) drain_gpu();
         uint64_t sq = seq();
@@ -2641,6 +2678,7 @@ class Engine {
 
     // -- token-sized transfers (engine.py:397-416) --
     void small_io(int dir, const uint8_t *payload, uint64_t size) {
+        NvtxRange nvtx_("small_io", send_iv[H2D]);
         complete_spec_tasks();
         uint64_t sq = seq();
         if (dir == H2D) {
@@ -2705,6 +2743,7 @@ class Engine {
 
     // -- pipeline control (engine.py:442-535) --
     void speculate_tick() {
+        NvtxRange nvtx_("speculate_tick", send_iv[H2D]);
         complete_spec_tasks();
         if (!cfg.speculate) return;
         auto flat = pred->predict_batches(send_iv[H2D], cfg.leeway, (int)cfg.depth);
@@ -2787,6 +2826,7 @@ class Engine {
     }
 
     void complete_spec_tasks() {
+        NvtxRange nvtx_("complete_spec_tasks", send_iv[H2D]);
         if (mem.hw) poll_hw_faults();
         if (spec_queue.empty()) return;
         Plane::SpecBatch batch(&plane);
@@ -2835,6 +2875,7 @@ class Engine {
     }
 
     int64_t relinquish() {
+        NvtxRange nvtx_("relinquish", send_iv[H2D]);
         int64_t n = discard_pipeline();
         counters[C_RELINQUISHES]++;
         counters[C_RELINQUISHED_RECORDS] += n;
@@ -2843,6 +2884,7 @@ class Engine {
     }
 
     void pad_to(uint64_t target, int64_t keep_id) {
+        NvtxRange nvtx_("pad_to (NOPs)", send_iv[H2D]);
         if (target <= send_iv[H2D]) return;
         uint64_t gap = target - send_iv[H2D];
         std::vector<std::pair<const uint8_t *, uint64_t>> pads(gap, {nullptr, (uint64_t)cfg.nop_bytes});
@@ -2865,6 +2907,7 @@ class Engine {
 
     // -- batch boundary (engine.py:537-577) --
     void sync() {
+        NvtxRange nvtx_("sync", send_iv[H2D]);
         complete_spec_tasks();
         std::vector<Suspended> susp(suspended);
         std::stable_sort(susp.begin(), susp.end(),
@@ -3087,6 +3130,7 @@ class Engine {
     // A trace ComputeEvent (duration in ns): model work on the app stream
     // after the last sync's swap-ins; later swap-outs wait for it.
     void compute(uint64_t ns) {
+        NvtxRange nvtx_("compute", send_iv[H2D]);
         complete_spec_tasks();
         plane.compute(ns, plane.compute_inputs, 2);
     }

@@ -502,3 +502,17 @@ def test_sm_budget_keeps_results_gpu():
         outs.append(([bytes(d.cpu().numpy()) for d in dst], bytes(tags.cpu().numpy())))
     assert outs[0] == outs[1] == outs[2]
     ctx.set_max_sms(0)
+
+
+def test_libsppipe_carries_nvtx_ranges():
+    """SURVEY §5 tracing: libsppipe (the product path) annotates its entry
+    points and every message it puts on the wire in the NVTX domain
+    "sppipe" (header-only NVTX3: free without an attached tool)."""
+    import os
+    import re
+
+    data = open(os.path.join(os.path.dirname(_native.SPGCM_PATH), "libsppipe.so"), "rb").read()
+    for name in (b"sppipe", b"submit_h2d", b"submit_d2h", b"sync", b"speculate_tick", b"relinquish",
+                 b"pad_to (NOPs)", b"h2d msg", b"h2d nop", b"d2h msg"):
+        assert re.search(re.escape(name) + b"\\x00", data), name  # (string tails may be merged)
+    assert b"nvtxDomainRangePushEx" in data or b"NVTX_INJECTION64_PATH" in data
