@@ -1012,13 +1012,23 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
         if (rc) return rc;
         SP_CUDA(cudaEventRecord(hp->ev_k[k], hp->s_k), "event record");
         SP_CUDA(cudaStreamWaitEvent(hp->s_out, hp->ev_k[k], 0), "wait");
-        // D2H of the same slices
+        // D2H of the same slices.  An open releases a message's plaintext
+        // only once its tag is verified: its bytes cross to the caller in
+        // one copy after the piece that holds its last row (where the
+        // finisher checks the tag and, on a mismatch, zeroes the device
+        // copy), so unverified plaintext never reaches host memory
+        // (channel.py:110-115 returns none on failure).
         gg = g;
         while (gg < g_end) {
             const MsgDev &m = msgs[(size_t)mi];
             const uint64_t t0 = gg - m.row_begin, t1 = std::min<uint64_t>(m.rows, g_end - m.row_begin);
             uint64_t lo, hi;
-            rows_to_bytes(m.len, m.rows, t0, t1, lo, hi);
+            if (open) {
+                lo = 0;
+                hi = t1 == m.rows ? m.len : 0;
+            } else {
+                rows_to_bytes(m.len, m.rows, t0, t1, lo, hi);
+            }
             if (hi > lo)
                 SP_CUDA(cudaMemcpyAsync(static_cast<uint8_t *>(d[mi].dst) + lo, hp->d_out + off[(size_t)mi] + lo,
                                         hi - lo, cudaMemcpyDeviceToHost, hp->s_out),
@@ -1046,12 +1056,7 @@ int run_host_batch(sp_ctx *ctx, const sp_desc *d, int n, bool open) {
         int bad = 0;
         for (int i = 0; i < n; ++i) {
             if (d[i].status) *d[i].status = st[(size_t)i];
-            if (st[(size_t)i]) {
-                // the device zeroed its copy, but the D2H of early pieces may
-                // have raced ahead of the verdict: scrub the host copy too
-                memset(d[i].dst, 0, d[i].len);
-                bad = 1;
-            }
+            if (st[(size_t)i]) bad = 1;  // the device zeroed the message before it crossed
         }
         if (bad) return fail(SP_EAUTH, "authentication failed");
     }

@@ -322,9 +322,15 @@ def test_host_batch_pieces_split_messages(ctx_for, torch_cuda):
     from paper_2411_03357_b200.gcm import GcmAuthError
 
     dst[3][5] ^= 1
+    for b in back:
+        b.fill_(0xAB)
     with pytest.raises(GcmAuthError):
         ctx.open_host_batch([(0, 900 + i, d, b, t) for i, (d, b, t) in enumerate(zip(dst, back, tags))])
+    # the tampered message crossed PCIe once, after its verdict: all zeros
+    # (no unverified plaintext, no stale sentinel); the others are verified
     assert int(back[3].sum()) == 0
+    for i in (0, 1, 2, 4):
+        assert torch.equal(src[i], back[i]), i
 
 
 def test_mixed_seal_open_batch(ctx_for, torch_cuda):
