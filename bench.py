@@ -340,6 +340,11 @@ def run_gpu(args) -> None:
     if args.same_device:  # multi-rank flow check on a 1-GPU box (with --dist-backend gloo)
         local = 0
     torch.cuda.set_device(local)
+    # this rank's CPUs and pinned memory on its GPU's NUMA node, before any
+    # host allocation (paper_2411_03357_b200/affinity.py)
+    from paper_2411_03357_b200.affinity import bind_to_gpu
+
+    placement = bind_to_gpu(local) if not args.no_bind else {"bound": False, "why": "--no-bind"}
     dev = torch.device("cuda", local)
     dist = init_dist(world, args.dist_backend)
     if args.dist_backend != "nccl":
@@ -487,7 +492,7 @@ def run_gpu(args) -> None:
         "config": {"workload": "opt-13b layer seal+open per GPU (18 x 32 MiB + 25,298,944 B messages, "
                                "consecutive H2D counters), AES-256-GCM, one batched launch each",
                    "layer_bytes": total, "messages": n, "parallelism": f"independent channels x{world}",
-                   "l2": "inputs (629 MB) > 126 MB L2; no flush needed"},
+                   "l2": "inputs (629 MB) > 126 MB L2; no flush needed", "host_placement": placement},
         "seal_gbs": round(total / seal_ms / 1e6, 2), "open_gbs": round(total / open_ms / 1e6, 2),
         "roofline": {
             "bound": "int", "achieved": round(per_gpu_payload, 2), "peak": round(bound, 1), "unit": "GB/s",
@@ -692,6 +697,8 @@ def offload_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 1)
            "tokens_per_s_ratio_synccc": with_compute["ratio_vs_plain"]["synccc"],
            "swap_only_ratio": swap_only["ratio_vs_plain"]["specpipe"],
            "with_compute": with_compute, "swap_only": swap_only}
+    if args.quick:
+        return out
     tr175 = workload.gen_opt_offload_trace("opt-175b", [1, 2], iterations=2, seed=rank, quant_bits=4)
     out["opt175b_4bit"] = {
         "layer_bytes": workload.opt_layer_bytes("opt-175b") // 4, "layers_offloaded_per_gpu": 2, "iterations": 2,
@@ -714,6 +721,12 @@ def workloads_bench(args, dist=None, dev_sync=None, rank: int = 0, world: int = 
 
     fix = dict(seed=rank, reference_compat=False)
     out = {}
+    if args.quick:
+        kv = workload.gen_adversarial_trace(
+            workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=rank), 0.25, seed=8)
+        out["kv_swap_opt30b"] = {"swap_only": trace_compare(kv, [
+            ("plain", "plain", _cfg(**fix)), ("specpipe", "engine", _cfg(**fix))], dist, dev_sync, world, 1)}
+        return out
     c1 = workload.gen_chunked_offload_trace(8, list(range(1, 9)), 3, 64 * MIB, chunk_bytes=32 * MIB, seed=rank)
     out["config1_64mib"] = {"trace": "8 x 64 MiB layers (2 x 32 MiB blocks), all offloaded, 3 iterations; "
                                      "reference_compat (defects reproduced)",
@@ -839,9 +852,14 @@ def main() -> None:
     ap.add_argument("--offload-iters", type=int, default=8)
     ap.add_argument("--offload-reps", type=int, default=3)
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-5 chunk-size sweep")
+    ap.add_argument("--no-bind", action="store_true", help="do not bind the rank to its GPU's NUMA-local CPUs")
+    ap.add_argument("--quick", action="store_true",
+                    help="flow check: 2 offload iterations, 1 rep, no OPT-175B / sweep / config-1 / ablation legs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.quick:
+        args.offload_iters, args.offload_reps, args.no_sweep = 2, 1, True
     if args.impl == "reference":
         run_reference(args)
     else:
