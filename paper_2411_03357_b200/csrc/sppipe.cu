@@ -669,7 +669,7 @@ struct Op {
 };
 
 // Host->device staging copies gathered and issued as one batch (one
-// cudaMemcpyBatchAsync) with one shared fence, recorded at issue.
+// issuing-thread closure of per-copy calls) with one shared fence, recorded at issue.
 struct CopyBatch {
     std::vector<void *> dst;
     std::vector<void *> src;
@@ -1618,54 +1618,23 @@ class Plane {
     void copy_batch_d2h(size_t count, F &&get) {
         copy_batch(s.d2h, false, count, get);
     }
-    // Copies of one flush / batch: one cudaMemcpyBatchAsync (CUDA 12.8+)
-    // instead of a call per copy; plain cudaMemcpyAsync where unsupported.
-    static constexpr size_t kMaxBatchCopies = 128;
+    // Copies of one flush / batch are posted as one closure: one issuing-
+    // thread hop, then one cudaMemcpyAsync per copy.  (The driver's batched
+    // copy entry points are not used: on this pool they faulted the GPU.)
     template <class F>
     void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
         if (!count) return;
         std::vector<void *> dsts(count), srcs(count);
         std::vector<size_t> sizes(count);
         for (size_t i = 0; i < count; ++i) get(i, dsts[i], srcs[i], sizes[i]);
-        const int device = dev;
-        iss.post([st, h2d, device, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes)]() mutable {
-            issue_copies(st, h2d, device, dsts, srcs, sizes);
+        iss.post([st, h2d, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes)]() mutable {
+            issue_copies(st, h2d, dsts, srcs, sizes);
         }, h2d ? "copy_h2d" : "copy_d2h");
     }
     // Runs on the issuing thread (or inline).
-    static void issue_copies(cudaStream_t st, bool h2d, int device, std::vector<void *> &dsts, std::vector<void *> &srcs,
+    static void issue_copies(cudaStream_t st, bool h2d, std::vector<void *> &dsts, std::vector<void *> &srcs,
                              std::vector<size_t> &sizes) {
-        static bool batch_ok = [] {  // SPPIPE_BATCH_COPY=0: per-copy calls (profilers show each copy)
-            const char *e = getenv("SPPIPE_BATCH_COPY");
-            return !(e && e[0] == '0');
-        }();
-        const size_t count = sizes.size();
-        size_t done = 0;
-        // At most kMaxBatchCopies copies per cudaMemcpyBatchAsync call: on
-        // driver 580 / B200 a call carrying many H2D copies can fault the
-        // GPU (Xid 32, B200_PROFILING.md), so long flushes go out in chunks.
-        while (count - done > 1 && batch_ok) {
-            const size_t n = std::min(kMaxBatchCopies, count - done);
-            cudaMemcpyAttributes attr;
-            memset(&attr, 0, sizeof attr);
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.srcLocHint.type = h2d ? cudaMemLocationTypeHost : cudaMemLocationTypeDevice;
-            attr.srcLocHint.id = h2d ? 0 : device;
-            attr.dstLocHint.type = h2d ? cudaMemLocationTypeDevice : cudaMemLocationTypeHost;
-            attr.dstLocHint.id = h2d ? device : 0;
-            size_t idx = 0, fail_idx = SIZE_MAX;
-            cudaError_t e = cudaMemcpyBatchAsync(dsts.data() + done, srcs.data() + done, sizes.data() + done, n,
-                                                 &attr, &idx, 1, &fail_idx, st);
-            if (e == cudaSuccess) {
-                done += n;
-                continue;
-            }
-            if (fail_idx != SIZE_MAX || (e != cudaErrorNotSupported && e != cudaErrorInvalidValue))
-                ck(e, "cudaMemcpyBatchAsync");
-            cudaGetLastError();
-            batch_ok = false;  // driver without batch copies: per-copy path from now on
-        }
-        for (size_t i = done; i < count; ++i)
+        for (size_t i = 0; i < sizes.size(); ++i)
             ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
                "batched copy");
     }
@@ -3103,7 +3072,7 @@ class Engine {
                 landed[e.block] = pl.host_ready[e.block];
             } else if (e.kind == SP_EV_SMALL_IO_H2D || e.kind == SP_EV_SMALL_IO_D2H) {
                 // token copies ride in the batch of their direction (one
-                // cudaMemcpyBatchAsync per sync), through the pinned ring
+                // batched copy closure per sync), through the pinned ring
                 const bool h2d = e.kind == SP_EV_SMALL_IO_H2D;
                 cudaStream_t st = h2d ? pl.s.h2d : pl.s.d2h;
                 View v{pl.alloc(e.len, st), 0, e.len};

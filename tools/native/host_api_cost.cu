@@ -58,22 +58,6 @@ int main() {
             [&](int i) { cudaMemcpyAsync(dbuf + i * 229376, hbuf + i * 229376, 229376, cudaMemcpyHostToDevice, s); });
     measure("cudaMemcpyAsync D2H 224 KiB pinned", N, s,
             [&](int i) { cudaMemcpyAsync(hbuf + i * 229376, dbuf + i * 229376, 229376, cudaMemcpyDeviceToHost, s); });
-    {
-        std::vector<void *> d(4), src(4);
-        std::vector<size_t> sz(4, 229376);
-        measure("cudaMemcpyBatchAsync 4 x 224 KiB H2D", N / 4, s, [&](int i) {
-            for (int k = 0; k < 4; ++k) {
-                d[k] = dbuf + (4 * i + k) * 229376;
-                src[k] = hbuf + (4 * i + k) * 229376;
-            }
-            cudaMemcpyAttributes attr = {};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.srcLocHint.type = cudaMemLocationTypeHost;
-            attr.dstLocHint.type = cudaMemLocationTypeDevice;
-            size_t idx = 0, fail = 0;
-            cudaMemcpyBatchAsync(d.data(), src.data(), sz.data(), 4, &attr, &idx, 1, &fail, s);
-        });
-    }
     auto seal = [&](int n, size_t len, int i) {
         std::vector<sp_desc> d(n);
         for (int k = 0; k < n; ++k)
