@@ -272,6 +272,11 @@ int sp_pipe_handle_done(sp_pipe *p, uint64_t seq, int32_t *done);
  * message still in flight on the `dir` lane (sent, not yet received),
  * stream-ordered after its seal.  The receiver's open must then fail. */
 int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_index, uint8_t mask);
+/* Test hook: one k_xfer launch (the plane's SM-driven transfer of small
+ * copies) over n jobs dst[i] <- src[i] (len[i] bytes; device or UVA-mapped
+ * pinned host pointers, any alignment), on a private stream; returns when
+ * the copy is done.  n <= 128. */
+int sp_test_xfer(int32_t n, void *const *dst, const void *const *src, const uint64_t *len);
 
 /* report(): counters in the order of sp_pipe_counter_name(i); n = count. */
 int sp_pipe_report(sp_pipe *p, int64_t *out, int32_t cap, int32_t *n);

@@ -102,7 +102,7 @@ SPPIPE_SYMBOLS = (
     "sp_pipe_create", "sp_pipe_destroy", "sp_pipe_register_block", "sp_pipe_seed_device", "sp_pipe_submit_h2d",
     "sp_pipe_submit_d2h", "sp_pipe_small_io", "sp_pipe_sync", "sp_pipe_speculate", "sp_pipe_relinquish",
     "sp_pipe_drain_decrypts", "sp_pipe_finish", "sp_pipe_audit", "sp_pipe_finish_observable", "sp_pipe_flush", "sp_pipe_app_write", "sp_pipe_app_read", "sp_pipe_replay", "sp_pipe_plain_replay",
-    "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
+    "sp_pipe_handle_done", "sp_pipe_test_corrupt", "sp_test_xfer", "sp_pipe_report", "sp_pipe_counter_name", "sp_pipe_send_iv",
     "sp_pipe_recv_iv",
     "sp_pipe_action_count", "sp_pipe_actions", "sp_pipe_sent_count", "sp_pipe_sent_log",
     "sp_pipe_record_count", "sp_pipe_record_first", "sp_pipe_record", "sp_pipe_pending", "sp_pipe_pending_at_iv", "sp_pipe_delivered_count",
@@ -229,6 +229,7 @@ def load_sppipe() -> ctypes.CDLL:
             "sp_pipe_plain_replay": [vp, P(SpEvent), u64, vp],
             "sp_pipe_handle_done": [vp, u64, P(i32)],
             "sp_pipe_test_corrupt": [vp, i32, u64, u64, ctypes.c_uint8],
+            "sp_test_xfer": [i32, P(vp), P(vp), P(u64)],
             "sp_pipe_report": [vp, P(i64), i32, P(i32)],
             "sp_pipe_actions": [vp, i64, P(SpAction), i64, P(i64)],
             "sp_pipe_sent_log": [vp, i32, i64, P(SpSent), i64, P(i64)],

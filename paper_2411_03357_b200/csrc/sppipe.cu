@@ -61,6 +61,66 @@ __global__ void k_bytes(uint8_t *__restrict__ dst, const uint8_t *__restrict__ s
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
 }
 
+// ---- SM-driven host<->device transfers ----------------------------------------------
+// The copy engine pays ~4.5 us of device time per cudaMemcpyAsync whatever its
+// size (B200, pinned, profiles/r2_copy_probe.txt: 64 KiB copies move at 12.7
+// GB/s, 224 KiB at 29 GB/s), so the many small copies of one flush (KV blocks,
+// 64 KiB chunks, landings) are moved instead by ONE launch of k_xfer: warps
+// stream 16 KiB pieces of every job straight over PCIe between HBM and the
+// UVA-mapped pinned host block (~50 GB/s per direction from 16 CTAs, the same
+// probe).  Large copies (> kXferMax) stay on the copy engine, which needs no
+// SMs and is as fast there.
+struct XferJob {
+    const uint8_t *src;
+    uint8_t *dst;
+    uint64_t n;
+};
+constexpr int kXferInline = 128;           // jobs per launch, inside the kernel parameters (3 KiB)
+constexpr uint64_t kXferPiece = 16384;     // bytes per warp step
+constexpr int kXferThreads = 512;
+struct XferParams {
+    XferJob j[kXferInline];
+    uint32_t n;
+};
+
+__device__ __forceinline__ void xfer_piece(const uint8_t *s, uint8_t *d, uint64_t lo, uint64_t hi, int lane) {
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15u) == 0) {
+        // 16-byte words, four loads in flight per lane before their stores
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(s);
+        uint4 *d4 = reinterpret_cast<uint4 *>(d);
+        const uint64_t w_lo = lo >> 4, w_hi = hi >> 4;
+        for (uint64_t i = w_lo + lane; i < w_hi; i += 128) {
+            uint4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (i + 32 * k < w_hi) v[k] = __ldcv(s4 + i + 32 * k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (i + 32 * k < w_hi) __stcs(d4 + i + 32 * k, v[k]);
+        }
+        for (uint64_t i = (w_hi << 4) + lane; i < hi; i += 32) d[i] = s[i];  // tail of the job
+    } else {
+        for (uint64_t i = lo + lane; i < hi; i += 32) d[i] = s[i];
+    }
+}
+
+__global__ void __launch_bounds__(kXferThreads) k_xfer(const __grid_constant__ XferParams p) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t j = 0;
+    uint64_t base = 0;  // global index of job j's first piece
+    for (uint64_t q = warp;; q += nwarps) {
+        while (j < p.n && q >= base + (p.j[j].n + kXferPiece - 1) / kXferPiece) {
+            base += (p.j[j].n + kXferPiece - 1) / kXferPiece;
+            ++j;
+        }
+        if (j >= p.n) return;
+        const uint64_t lo = (q - base) * kXferPiece;
+        xfer_piece(p.j[j].src, p.j[j].dst, lo, min(p.j[j].n, lo + kXferPiece), lane);
+    }
+}
+
 // Model compute of a trace's ComputeEvent (the reference charges it to the
 // GPU timeline, simulator.py:431-434): a fixed amount of FMA work per
 // launch, calibrated to the event's duration on an idle GPU, in 16 waves of
@@ -1480,6 +1540,7 @@ class Plane {
         collect();
     }
 
+    bool ring_aliased = false;
     uint8_t *ring_reserve(uint64_t n) {
         if (!ring.ptr) {
             {
@@ -1497,6 +1558,12 @@ class Plane {
                 ck(cudaHostAlloc(reinterpret_cast<void **>(&ring.ptr), ring.cap,
                                  cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc(ring)");
             }
+        }
+        if (!ring_aliased) {
+            void *dp = nullptr;
+            if (cudaHostGetDevicePointer(&dp, ring.ptr, 0) == cudaSuccess) add_alias(ring.ptr, ring.cap, dp);
+            cudaGetLastError();
+            ring_aliased = true;
         }
         if (n > ring.cap) throw ValueErr("small payload larger than the staging ring");
         n = (n + 63u) & ~uint64_t(63);  // 64-byte slots: vectorised kernel reads straight from the ring
@@ -1618,16 +1685,65 @@ class Plane {
     void copy_batch_d2h(size_t count, F &&get) {
         copy_batch(s.d2h, false, count, get);
     }
-    // Copies of one flush / batch are posted as one closure: one issuing-
-    // thread hop, then one cudaMemcpyAsync per copy.  (The driver's batched
-    // copy entry points are not used: on this pool they faulted the GPU.)
+    // Device aliases of pinned host memory the plane copies to or from
+    // (registered blocks, the token ring): host lo -> (host hi, device lo).
+    std::map<uintptr_t, std::pair<uintptr_t, uintptr_t>> host_alias;
+    void add_alias(const void *host, uint64_t len, const void *dev) {
+        if (!host || !dev || !len) return;
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(host);
+        host_alias[lo] = {lo + len, reinterpret_cast<uintptr_t>(dev)};
+    }
+    // device address of [host, host + n), or null when not inside one mapped range
+    void *dev_alias(const void *host, uint64_t n) const {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(host);
+        auto it = host_alias.upper_bound(a);
+        if (it == host_alias.begin()) return nullptr;
+        --it;
+        if (a + n > it->second.first) return nullptr;
+        return reinterpret_cast<void *>(it->second.second + (a - it->first));
+    }
+    // Copies of one flush / batch are posted as one closure.  Copies of <=
+    // xfer_max() bytes whose host side is mapped go out as k_xfer launches
+    // (<= kXferInline jobs each); the rest as one cudaMemcpyAsync per copy.
+    // (The driver's batched copy entry points are not used: on this pool
+    // they faulted the GPU.)  SPPIPE_XFER_MAX=0 sends everything to the copy
+    // engine (A/B).
+    static uint64_t xfer_max() {
+        static const uint64_t v = [] {
+            const char *e = getenv("SPPIPE_XFER_MAX");
+            return e ? (uint64_t)atoll(e) : (uint64_t)(2u << 20);
+        }();
+        return v;
+    }
+    uint64_t xfer_launches = 0, xfer_jobs = 0, ce_copies = 0;  // diagnostics
     template <class F>
     void copy_batch(cudaStream_t st, bool h2d, size_t count, F &&get) {
         if (!count) return;
-        std::vector<void *> dsts(count), srcs(count);
-        std::vector<size_t> sizes(count);
-        for (size_t i = 0; i < count; ++i) get(i, dsts[i], srcs[i], sizes[i]);
-        iss.post([st, h2d, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes)]() mutable {
+        std::vector<void *> dsts, srcs;
+        std::vector<size_t> sizes;
+        std::vector<XferJob> jobs;
+        const uint64_t xmax = xfer_max();
+        for (size_t i = 0; i < count; ++i) {
+            void *d = nullptr, *s0 = nullptr;
+            size_t n = 0;
+            get(i, d, s0, n);
+            if (!n) continue;
+            void *alias = n <= xmax ? dev_alias(h2d ? s0 : d, n) : nullptr;
+            if (alias) {
+                jobs.push_back(h2d ? XferJob{static_cast<const uint8_t *>(alias), static_cast<uint8_t *>(d), n}
+                                   : XferJob{static_cast<const uint8_t *>(s0), static_cast<uint8_t *>(alias), n});
+            } else {
+                dsts.push_back(d);
+                srcs.push_back(s0);
+                sizes.push_back(n);
+            }
+        }
+        xfer_jobs += jobs.size();
+        xfer_launches += (jobs.size() + kXferInline - 1) / kXferInline;
+        ce_copies += sizes.size();
+        iss.post([st, h2d, dsts = std::move(dsts), srcs = std::move(srcs), sizes = std::move(sizes),
+                  jobs = std::move(jobs)]() mutable {
+            issue_xfers(st, jobs);
             issue_copies(st, h2d, dsts, srcs, sizes);
         }, h2d ? "copy_h2d" : "copy_d2h");
     }
@@ -1637,6 +1753,22 @@ class Plane {
         for (size_t i = 0; i < sizes.size(); ++i)
             ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
                "batched copy");
+    }
+    // One CTA per 64 KiB of a launch's bytes, 1..32 CTAs (16-32 CTAs keep
+    // ~50 GB/s in flight over PCIe; more only add SM occupancy).
+    static void issue_xfers(cudaStream_t st, const std::vector<XferJob> &jobs) {
+        for (size_t i = 0; i < jobs.size(); i += kXferInline) {
+            XferParams p;
+            p.n = (uint32_t)std::min<size_t>(kXferInline, jobs.size() - i);
+            uint64_t bytes = 0;
+            for (uint32_t k = 0; k < p.n; ++k) {
+                p.j[k] = jobs[i + k];
+                bytes += p.j[k].n;
+            }
+            const unsigned ctas = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(32, (bytes + 65535) >> 16));
+            k_xfer<<<ctas, kXferThreads, 0, st>>>(p);
+            ck(cudaGetLastError(), "k_xfer launch");
+        }
     }
     // One seal / open / mixed launch of libspgcm, issued in order.
     // kind: 0 sp_crypt_batch (per-message op), 1 sp_seal_batch, 2 sp_open_batch
@@ -3350,6 +3482,7 @@ int sp_pipe_register_block(sp_pipe *p, int64_t id, uint64_t base, uint64_t len, 
             if (cudaPointerGetAttributes(&a, host) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
                 b.host_dev = static_cast<uint8_t *>(a.devicePointer);
             cudaGetLastError();  // pageable memory: clear the sticky query error
+            p->e->plane.add_alias(b.host, len, b.host_dev);
         }
         p->e->mem.add_block(b);
     });
@@ -3425,6 +3558,23 @@ int sp_pipe_plain_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8
 int sp_pipe_replay(sp_pipe *p, const sp_event *ev, uint64_t n, const uint8_t *payloads, uint64_t *done) {
     if (done) *done = 0;
     return guarded([&] { p->e->replay(ev, n, payloads, done); });
+}
+int sp_test_xfer(int32_t n, void *const *dst, const void *const *src, const uint64_t *len) {
+    if (n < 0 || n > kXferInline || (n && (!dst || !src || !len))) {
+        g_err = "sp_test_xfer: 0 <= n <= 128 jobs with non-null arrays";
+        return SP_EINVAL;
+    }
+    return guarded([&] {
+        std::vector<XferJob> jobs;
+        for (int32_t i = 0; i < n; ++i)
+            jobs.push_back(XferJob{static_cast<const uint8_t *>(src[i]), static_cast<uint8_t *>(dst[i]), len[i]});
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        Plane::issue_xfers(st, jobs);
+        const cudaError_t e = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        ck(e, "sp_test_xfer");
+    });
 }
 int sp_pipe_test_corrupt(sp_pipe *p, int32_t dir, uint64_t index, uint64_t byte_index, uint8_t mask) {
     return guarded([&] {

@@ -1,9 +1,9 @@
 """Device timeline of the bench's OPT-30B KV-swap trace (config 3) through
 the native engine and the plain baseline: every GPU op (stream, start, end,
 kind, bytes) as text, for reading dependency chains.  Run with
-SPPIPE_BATCH_COPY=0 so each copy is its own profiler event.
+SPPIPE_XFER_MAX=0 so each copy is its own (copy-engine) profiler event.
 
-    SPPIPE_BATCH_COPY=0 python tools/kv_timeline.py gpurun_out/kv_tl
+    SPPIPE_XFER_MAX=0 python tools/kv_timeline.py gpurun_out/kv_tl
 """
 import json
 import os
