@@ -75,11 +75,12 @@ struct XferJob {
     uint8_t *dst;
     uint64_t n;
 };
-constexpr int kXferInline = 128;           // jobs per launch, inside the kernel parameters (3 KiB)
+constexpr int kXferInline = 128;           // jobs per launch, inside the kernel parameters (<= 3 KiB)
 constexpr uint64_t kXferPiece = 16384;     // bytes per warp step
-constexpr int kXferThreads = 512;
+constexpr int kXferThreads = 256;          // fits beside a k_gcm CTA (104 registers x 512 threads)
+template <int N>
 struct XferParams {
-    XferJob j[kXferInline];
+    XferJob j[N];
     uint32_t n;
 };
 
@@ -104,7 +105,8 @@ __device__ __forceinline__ void xfer_piece(const uint8_t *s, uint8_t *d, uint64_
     }
 }
 
-__global__ void __launch_bounds__(kXferThreads) k_xfer(const __grid_constant__ XferParams p) {
+template <int N>
+__global__ void __launch_bounds__(kXferThreads) k_xfer(const __grid_constant__ XferParams<N> p) {
     const int lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -1754,20 +1756,29 @@ class Plane {
             ck(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st),
                "batched copy");
     }
-    // One CTA per 64 KiB of a launch's bytes, 1..32 CTAs (16-32 CTAs keep
-    // ~50 GB/s in flight over PCIe; more only add SM occupancy).
+    // One 256-thread CTA per 32 KiB of a launch's bytes, 1..64 CTAs (~1 MiB
+    // in flight keeps ~50 GB/s over PCIe; more only add SM occupancy).  The
+    // parameter block is sized to the job count (the driver copies every
+    // parameter byte per launch: 8 jobs 0.2 KiB, 32 0.8 KiB, 128 3 KiB).
+    template <int N>
+    static void launch_xfer(cudaStream_t st, const XferJob *jobs, uint32_t n) {
+        XferParams<N> p;
+        p.n = n;
+        uint64_t bytes = 0;
+        for (uint32_t k = 0; k < n; ++k) {
+            p.j[k] = jobs[k];
+            bytes += jobs[k].n;
+        }
+        const unsigned ctas = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(64, (bytes + 32767) >> 15));
+        k_xfer<N><<<ctas, kXferThreads, 0, st>>>(p);
+        ck(cudaGetLastError(), "k_xfer launch");
+    }
     static void issue_xfers(cudaStream_t st, const std::vector<XferJob> &jobs) {
         for (size_t i = 0; i < jobs.size(); i += kXferInline) {
-            XferParams p;
-            p.n = (uint32_t)std::min<size_t>(kXferInline, jobs.size() - i);
-            uint64_t bytes = 0;
-            for (uint32_t k = 0; k < p.n; ++k) {
-                p.j[k] = jobs[i + k];
-                bytes += p.j[k].n;
-            }
-            const unsigned ctas = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(32, (bytes + 65535) >> 16));
-            k_xfer<<<ctas, kXferThreads, 0, st>>>(p);
-            ck(cudaGetLastError(), "k_xfer launch");
+            const uint32_t n = (uint32_t)std::min<size_t>(kXferInline, jobs.size() - i);
+            if (n <= 8) launch_xfer<8>(st, jobs.data() + i, n);
+            else if (n <= 32) launch_xfer<32>(st, jobs.data() + i, n);
+            else launch_xfer<kXferInline>(st, jobs.data() + i, n);
         }
     }
     // One seal / open / mixed launch of libspgcm, issued in order.

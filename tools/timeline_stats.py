@@ -58,6 +58,21 @@ def main(path: str) -> None:
         if c - b > 200:
             gaps.append((round((b - t0) / 1e3, 2), round((c - b) / 1e3, 2)))
     print("H2D gaps >0.2ms (at ms, len ms):", gaps[:40], "total", round(sum(g[1] for g in gaps), 1))
+    gaps = []
+    s = sorted(d2h)
+    for (a, b), (c, d) in zip(s, s[1:]):
+        if c - b > 50:
+            gaps.append((round((b - t0) / 1e3, 2), round((c - b) / 1e3, 3)))
+    print("D2H gaps >0.05ms (at ms, len ms):", gaps[:40], "n", len(gaps), "total", round(sum(g[1] for g in gaps), 2))
+    gaps = []
+    s = sorted(h2d)
+    for (a, b), (c, d) in zip(s, s[1:]):
+        if c - b > 50:
+            gaps.append((round((b - t0) / 1e3, 2), round((c - b) / 1e3, 3)))
+    print("H2D gaps >0.05ms: n", len(gaps), "total", round(sum(g[1] for g in gaps), 2), gaps[:20])
+    if h2d and d2h:
+        print(f"H2D first {(min(a for a, _ in h2d) - t0) / 1e3:.2f} last {(max(b for _, b in h2d) - t0) / 1e3:.2f} ms; "
+              f"D2H first {(min(a for a, _ in d2h) - t0) / 1e3:.2f} last {(max(b for _, b in d2h) - t0) / 1e3:.2f} ms")
     # host-side runtime calls: where does the host thread block?
     rt = defaultdict(lambda: [0, 0.0, 0.0])
     for e in ev:
