@@ -603,12 +603,26 @@ uint64_t rows_per_warp() {
     return v;
 }
 
+// Minimum working warps per CTA of a launch that does not fill the GPU
+// (SPGCM_PACK, default 1 = spread one warp per SM first).  Spreading gives
+// the lowest latency for a launch alone; packing keeps a small launch on few
+// SMs, so the small launches of several streams run side by side instead of
+// each occupying most SMs with one 192 KiB-table CTA per working warp.
+uint32_t pack_warps() {
+    static const uint32_t v = [] {
+        const char *e = getenv("SPGCM_PACK");
+        const long x = e ? atol(e) : 1;
+        return (uint32_t)std::max(1L, std::min<long>(x, kWarpsPerCta));
+    }();
+    return v;
+}
+
 void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
     const uint64_t sms = (uint64_t)ctx->sms();
     const uint64_t want_warps =
         std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rows_per_warp(), std::min(nmsgs, rows)),
                                                  sms * kWarpsPerCta));
-    warps_used = (uint32_t)((want_warps + sms - 1) / sms);
+    warps_used = (uint32_t)std::max<uint64_t>((want_warps + sms - 1) / sms, std::min<uint64_t>(pack_warps(), want_warps));
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }
 
@@ -643,7 +657,9 @@ void launch_shape_small(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &g
     const uint64_t spread = rows <= single * nmsgs ? std::min(nmsgs, rows)
                                               : std::max(rows / small_rows_per_warp(), std::min(nmsgs, rows));
     const uint64_t want_warps = std::max<uint64_t>(1, std::min<uint64_t>(spread, sms * ctas_per_sm * per_cta));
-    warps_used = (uint32_t)std::min<uint64_t>(per_cta, (want_warps + sms * ctas_per_sm - 1) / (sms * ctas_per_sm));
+    warps_used = (uint32_t)std::min<uint64_t>(
+        per_cta, std::max<uint64_t>((want_warps + sms * ctas_per_sm - 1) / (sms * ctas_per_sm),
+                                    std::min<uint64_t>(pack_warps(), want_warps)));
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }
 

@@ -2013,9 +2013,14 @@ class Plane {
         }();
         return m;
     }
-    static bool out_stream_for(bool kv_class) {
+    // Chunks of >= 4 MiB seal on the out stream too: a weight swap-out then
+    // waits only for its own block's open, not for every swap-in queued
+    // ahead of it on the compute streams (256 MiB-block offload without
+    // compute 0.84 -> 0.98 of plain, 32 MiB with compute 0.957 -> 0.977;
+    // 1 MiB chunks measured better in the queue, 0.915 vs 0.888).
+    static bool out_stream_for(bool kv_class, uint64_t len) {
         const int m = out_stream_mode();
-        return m < 0 ? kv_class : m == 1;
+        return m < 0 ? (kv_class || len >= (4ull << 20)) : m == 1;
     }
 
     void launch_out() {
@@ -2757,7 +2762,7 @@ class Engine {
         bool swap = r.cls == TC_WEIGHTS || r.cls == TC_KV;
         auto spans = chunk_spans(r.len, cfg.chunk_bytes);
         View src{buf.buf, buf.off + inner, r.len};
-        auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H], Plane::out_stream_for(r.cls == TC_KV));
+        auto msgs = plane.seal_device_chunks(src, spans, D2H, send_iv[D2H], Plane::out_stream_for(r.cls == TC_KV, spans.empty() ? r.len : spans[0].second));
         for (auto &m : msgs) send(D2H, m);
         if (inner == 0 && r.len == b.len) device_mem.erase(r.block_id);
         PVec<std::tuple<MsgP, uint64_t, uint64_t>> taken;
