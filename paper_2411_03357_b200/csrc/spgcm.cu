@@ -588,12 +588,13 @@ uint32_t rows_of(uint64_t len) { return (uint32_t)((((len + 15u) >> 4) + 31u) >>
 // combine whose nibble-table lookups hit 32 different L2 lines per load
 // (1,024 L2 requests per warp): fine for big batches (one combine per ~260
 // rows), but for small batches it is the whole cost if 16 warps of one SM do
-// it at once.  So small batches spread few working warps over many SMs
-// (>= 4 rows per warp, measured best on 224 KiB KV batches); big ones use all 16 warps of every SM.
+// it at once.  So batches that do not fill the GPU spread their working
+// warps over many SMs first (rows per warp per the policy above
+// launch_rows); big ones use all 16 warps of every SM.
 // Tiny messages (NOP pads, tokens) are latency-bound in their epilogue, so a
 // batch also gets at least one warp per message.
-// Minimum rows per working warp of a small batch (SPGCM_ROWS_PER_WARP
-// overrides, for launch-shape sweeps).
+// Minimum rows per working warp of a BigTabs batch above the tiny range
+// (SPGCM_ROWS_PER_WARP overrides, for launch-shape sweeps).
 uint64_t rows_per_warp() {
     static const uint64_t v = [] {
         const char *e = getenv("SPGCM_ROWS_PER_WARP");
@@ -617,26 +618,39 @@ uint32_t pack_warps() {
     return v;
 }
 
-void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
+void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used, uint64_t rpw) {
     const uint64_t sms = (uint64_t)ctx->sms();
     const uint64_t want_warps =
-        std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rows_per_warp(), std::min(nmsgs, rows)),
+        std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rpw, std::min(nmsgs, rows)),
                                                  sms * kWarpsPerCta));
     warps_used = (uint32_t)std::max<uint64_t>((want_warps + sms - 1) / sms, std::min<uint64_t>(pack_warps(), want_warps));
     grid = (int)((want_warps + warps_used - 1) / warps_used);
 }
 
-// Latency-bound launches (few rows: NOP pads, token I/O, KV blocks) run the
-// SmallTabs variant: 10 KB of tables per CTA instead of 192 KB, 128-thread
-// CTAs, up to 4 per SM, filling SMs one warp per CTA first.
-// SPGCM_SMALL_ROWS (default 256 rows = 128 KiB; 0 disables) and
-// SPGCM_SMALL_RPW (rows per warp, default 2) are for sweeps.
+// Launch policy by the batch's rows:
+//   <= SPGCM_SMALL_ROWS (default 256 rows = 128 KiB: NOP pads, tokens, KV
+//      blocks): the SmallTabs variant, 10 KB of tables per CTA, 128-thread
+//      CTAs, up to 4 per SM, SPGCM_SMALL_RPW (default 2) rows per warp;
+//   above: BigTabs, SPGCM_ROWS_PER_WARP (default 4) rows per warp.
+// SPGCM_TINY_ROWS=n (default 0 = off) sends batches of <= n rows to BigTabs
+// at 1 row per warp (2 above 256 rows).  Alone on the GPU that is faster
+// (profiles/r2_launch_shape_sweep.txt, r2_launch_latency_tiny.txt: 1 x 64
+// KiB 8.9 -> 6.2 us, 1 x 224 KiB 9.5 -> 7.6 us, 2 KiB token 8.2 -> 6.1 us
+// per launch), but each such launch holds up to 148 SMs with a 192 KiB
+// table fill per working warp, and beside the model's compute the traces
+// ran slower (64 KiB-chunk offload 0.76 -> 0.70 of plain, KV 0.94 -> 0.92,
+// profiles/r2_ab_tiny.txt), so it is off.  SmallTabs above 256 rows lost
+// everywhere (4 x 224 KiB 11.3 -> 15.4 us).
 uint64_t env_u64(const char *name, uint64_t dflt) {
     const char *e = getenv(name);
     return e ? (uint64_t)atoll(e) : dflt;
 }
 uint64_t small_rows_max() {
     static const uint64_t v = env_u64("SPGCM_SMALL_ROWS", 256);
+    return v;
+}
+uint64_t tiny_rows_max() {
+    static const uint64_t v = env_u64("SPGCM_TINY_ROWS", 0);
     return v;
 }
 uint64_t small_rows_per_warp() {
@@ -686,9 +700,11 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
     p.row_begin = row_begin;
     p.row_end = row_end;
     int grid = 1;
-    const bool small = row_end - row_begin <= small_rows_max();
-    if (small) launch_shape_small(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
-    else launch_shape(ctx, row_end - row_begin, p.nmsgs, grid, p.warps_used);
+    const uint64_t rows = row_end - row_begin;
+    const bool tiny = rows <= tiny_rows_max();
+    const bool small = !tiny && rows <= small_rows_max();
+    if (small) launch_shape_small(ctx, rows, p.nmsgs, grid, p.warps_used);
+    else launch_shape(ctx, rows, p.nmsgs, grid, p.warps_used, tiny ? (rows <= 256 ? 1 : 2) : rows_per_warp());
     // Programmatic dependent launch: a launch that directly follows another
     // kernel on the stream starts (and fills its shared-memory tables)
     // while that kernel's last CTAs drain; it waits in griddepcontrol.wait
