@@ -62,13 +62,13 @@ typedef void *sp_stream_t;
  * src/dst take the vectorised path. */
 typedef struct sp_desc {
     uint32_t dir;       /* SP_DIR_H2D or SP_DIR_D2H */
-    uint32_t reserved;  /* sp_crypt_batch only: SP_OP_SEAL or SP_OP_OPEN; ignored elsewhere */
+    uint32_t reserved;  /* sp_crypt_batch: SP_OP_SEAL or SP_OP_OPEN (else ignored); | SP_STATUS_ON_FAILURE */
     uint64_t iv;        /* 64-bit channel counter, any value in [0, 2^64) */
     uint64_t len;       /* 1 .. SP_MAX_MESSAGE_BYTES */
     const void *src;
     void *dst;
     void *tag;          /* 16 bytes, device */
-    int32_t *status;    /* open only, device; may be NULL for seal */
+    int32_t *status;    /* open only, device (or UVA-mapped pinned); may be NULL for seal */
 } sp_desc;
 
 /* Replaces the per-call `AESGCM(key)` construction (channel.py:96,111): key
@@ -96,6 +96,11 @@ int sp_open_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
  * opens of one flush.  Messages of one call must not overlap in memory. */
 #define SP_OP_SEAL 0u
 #define SP_OP_OPEN 1u
+/* Or-ed into desc.reserved of an open (any batch call): *status is written
+ * only on a tag mismatch (1), never on success, so many opens may share one
+ * status word (a sticky "some open failed" flag; the pipeline keeps one per
+ * pipe in mapped pinned memory and reads it at finish). */
+#define SP_STATUS_ON_FAILURE 0x100u
 int sp_crypt_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
 
 /* Host-buffer entry points: the exact call shape of encrypt_at / decrypt_at

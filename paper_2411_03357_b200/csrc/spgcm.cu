@@ -112,7 +112,7 @@ __device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int 
     if (lane == 0) {
         if (!have_want) want = load_tag(md.tag);
         bad = (want.x ^ tag.x) | (want.y ^ tag.y) | (want.z ^ tag.z) | (want.w ^ tag.w);
-        if (md.status) *md.status = bad ? 1 : 0;
+        if (md.status && (bad || !(md.dir & kStickyBit))) *md.status = bad ? 1 : 0;
     }
     bad = __shfl_sync(0xffffffffu, bad, 0);
     if (bad) {
@@ -760,8 +760,9 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
     for (int i = 0; i < n; ++i) {
         int rc = check_desc(d[i]);
         if (rc) return rc;
-        if (mode == 2 && d[i].reserved > SP_OP_OPEN) return fail(SP_EINVAL, "op must be SP_OP_SEAL or SP_OP_OPEN");
-        const bool open = mode == 1 || (mode == 2 && d[i].reserved == SP_OP_OPEN);
+        const uint32_t op = d[i].reserved & ~SP_STATUS_ON_FAILURE;
+        if (mode == 2 && op > SP_OP_OPEN) return fail(SP_EINVAL, "op must be SP_OP_SEAL or SP_OP_OPEN");
+        const bool open = mode == 1 || (mode == 2 && op == SP_OP_OPEN);
         if (open && !d[i].status) return fail(SP_EINVAL, "open needs a status pointer");
         MsgDev &m = ws->h_msgs[(size_t)i];
         m.src = static_cast<const uint8_t *>(d[i].src);
@@ -770,7 +771,7 @@ int stage_batch(const sp_ctx *ctx, const sp_desc *d, int n, cudaStream_t s, Work
         m.status = d[i].status;
         m.len = d[i].len;
         m.iv = d[i].iv;
-        m.dir = d[i].dir | (open ? kOpenBit : 0u);
+        m.dir = d[i].dir | (open ? kOpenBit : 0u) | ((d[i].reserved & SP_STATUS_ON_FAILURE) ? kStickyBit : 0u);
         m.rows = rows_of(d[i].len);
         m.row_begin = rows;
         rows += m.rows;

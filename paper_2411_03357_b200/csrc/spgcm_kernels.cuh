@@ -73,6 +73,8 @@ constexpr uint32_t kInlineTiny = 4;  // 0.5 KiB of parameters: the common KV / N
 // MsgDev.dir: low byte = channel direction (nonce word 0), this bit = open
 // (verify + decrypt) instead of seal, so one launch can mix both.
 constexpr uint32_t kOpenBit = 0x100u;
+// MsgDev.dir: this bit = write *status only on failure (SP_STATUS_ON_FAILURE)
+constexpr uint32_t kStickyBit = 0x200u;
 
 template <uint32_t INL>
 struct KParamsT {

@@ -1019,9 +1019,14 @@ class Plane {
         FenceP ready;
     } outb;
     CopyBatch *spec_copies = nullptr;                 // copies of the SpecBatch being built
-    // status words of opens
-    int32_t *status = nullptr;
-    uint64_t status_cap = 1 << 16, status_used = 0;
+    // Open verdicts: every open of the pipe shares one sticky status word in
+    // mapped pinned memory (SP_STATUS_ON_FAILURE: k_gcm writes it only on a
+    // tag mismatch), read by the host at finish / strict checks.  (A status
+    // word per open needed a full-device sync to recycle the words every
+    // 64K opens: four pipeline drains per 64 KiB-chunk OPT-66B run.)
+    volatile int32_t *auth_h = nullptr;  // host view
+    int32_t *auth_d = nullptr;           // device alias
+    uint64_t opens_unchecked = 0;
     uint64_t bytes_h2d = 0, bytes_d2h = 0, launches = 0;
 
     Plane(bool dry_, const uint8_t key[32], uint64_t batch, uint64_t reserve) : dry(dry_), batch_bytes(batch) {
@@ -1030,10 +1035,13 @@ class Plane {
         s = streams_for(dev);
         pool = pool_for(dev, reserve, s.comp);
         ctx = ctx_for(dev, key);
-        ck(cudaMalloc(&status, status_cap * sizeof(int32_t)), "cudaMalloc(status)");
+        ck(cudaHostAlloc(reinterpret_cast<void **>(const_cast<int32_t **>(&auth_h)), 64, cudaHostAllocMapped),
+           "cudaHostAlloc(auth flag)");
+        *auth_h = 0;
+        ck(cudaHostGetDevicePointer(reinterpret_cast<void **>(&auth_d), const_cast<int32_t *>(auth_h), 0),
+           "cudaHostGetDevicePointer(auth flag)");
         ck(cudaMalloc(&zero_dev, kZeroBytes), "cudaMalloc(zero page)");
         ck(cudaMemset(zero_dev, 0, kZeroBytes), "cudaMemset(zero page)");
-        ck(cudaMemset(status, 0, status_cap * sizeof(int32_t)), "cudaMemset(status)");
         window = new_fence();
         if (Issuer::enabled_by_env()) iss.start(dev);
     }
@@ -1092,7 +1100,7 @@ class Plane {
             g_rings.push_back({ring.ptr, ring.cap});
         }
         for (cudaEvent_t e : free_events) cudaEventDestroy(e);
-        if (status) cudaFree(status);
+        if (auth_h) cudaFreeHost(const_cast<int32_t *>(auth_h));
         if (zero_dev) cudaFree(zero_dev);
         if (d_spans) cudaFree(d_spans);
     }
@@ -1351,25 +1359,23 @@ class Plane {
 
     // -- status slots -------------------------------------------------------------------
     int32_t *status_slot() {
-        if (status_used + 1 > status_cap) check_auth();
-        return status + status_used++;
+        ++opens_unchecked;
+        return auth_d;
     }
     void check_auth() {
         if (dry) return;
         flush();
-        if (!status_used) return;
+        if (!opens_unchecked) return;
         iss.drain();
         ck(cudaStreamSynchronize(s.comp), "sync comp");
         ck(cudaStreamSynchronize(s.comp2), "sync comp2");
         ck(cudaStreamSynchronize(s.land), "sync land");
         ck(cudaStreamSynchronize(s.d2h), "sync d2h");
-        std::vector<int32_t> h(status_used);
-        ck(cudaMemcpy(h.data(), status, status_used * sizeof(int32_t), cudaMemcpyDeviceToHost), "status read");
-        int64_t bad = 0;
-        for (int32_t v : h) bad += v != 0;
-        ck(cudaMemset(status, 0, status_used * sizeof(int32_t)), "status clear");
-        status_used = 0;
-        if (bad) throw AuthErr("authentication failed on the device");
+        opens_unchecked = 0;
+        if (*auth_h) {
+            *auth_h = 0;
+            throw AuthErr("authentication failed on the device");
+        }
     }
 
     // -- compute queue ------------------------------------------------------------------
@@ -1393,7 +1399,7 @@ class Plane {
                       const BufP &tagbuf, uint64_t tag_off, int32_t *status) {
         Op op;
         op.d.dir = dir;
-        op.d.reserved = opkind;
+        op.d.reserved = opkind == SP_OP_OPEN ? (SP_OP_OPEN | SP_STATUS_ON_FAILURE) : opkind;
         op.d.iv = iv;
         op.d.len = len;
         op.d.src = src.ptr();
@@ -1624,6 +1630,7 @@ class Plane {
                 d.dst = buf->ptr + off;
                 d.tag = m->buf->ptr + m->tag_off;
                 d.status = status_slot();
+                d.reserved = SP_STATUS_ON_FAILURE;
                 descs.push_back(d);
                 places.push_back({l.block, off, std::get<2>(j), m->len});
                 off += m->len;

@@ -386,3 +386,49 @@ def test_mixed_seal_open_batch(ctx_for, torch_cuda):
         else:
             assert (_host(dsts[i]), _host(tags[i])) == refs[i], i
             assert st[i] == 7  # seals leave status alone
+
+
+@pytest.mark.parametrize("tamper", [None, 3])
+def test_status_on_failure_shared_word(ctx_for, torch_cuda, tamper):
+    """SP_STATUS_ON_FAILURE (include/spgcm.h): opens that share one status
+    word write it only on a tag mismatch — an all-authentic batch leaves the
+    word untouched, one tampered message sets it to 1 (its output zeroed,
+    the others' plaintext intact).  The pipeline keeps one such word per pipe
+    in mapped pinned memory; here it is host-mapped too."""
+    import ctypes
+
+    from paper_2411_03357_b200 import _native
+
+    torch = torch_cuda
+    rng = random.Random(5)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    lib = _native.load_spgcm()
+    n = 8
+    sizes = [rng.choice([1, 100, 229_376, 65536]) for _ in range(n)]
+    plains = [rng.randbytes(s) for s in sizes]
+    refs = [oracle_port.seal(key, 0, 40 + i, p) for i, p in enumerate(plains)]
+    word = torch.full((16,), 7, dtype=torch.int32).pin_memory()  # UVA-mapped pinned
+    tags = torch.zeros((n, 16), dtype=torch.uint8, device="cuda")
+    descs = (_native.SpDesc * n)()
+    srcs, dsts = [], []
+    for i in range(n):
+        c, t = refs[i]
+        if i == tamper:
+            c = bytes([c[0] ^ 0x80]) + c[1:]
+        src = _dev(torch, c)
+        tags[i] = torch.tensor(list(t), dtype=torch.uint8)
+        dst = torch.full_like(src, 0xAB)
+        srcs.append(src)
+        dsts.append(dst)
+        d = descs[i]
+        d.dir, d.reserved, d.iv, d.len = 0, 0x100, 40 + i, sizes[i]
+        d.src, d.dst, d.tag = src.data_ptr(), dst.data_ptr(), tags[i].data_ptr()
+        d.status = word.data_ptr()
+    rc = lib.sp_open_batch(ctx._h, descs, n, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0, _native.last_error()
+    torch.cuda.synchronize()
+    assert int(word[0]) == (7 if tamper is None else 1)
+    for i in range(n):
+        want = bytes(sizes[i]) if i == tamper else plains[i]
+        assert _host(dsts[i]) == want, i

@@ -25,6 +25,8 @@ def sampler():
         if "sampler" in name:
             lib = ctypes.CDLL(name)
             lib.sampler_start()
+            if os.environ.get("SAMPLER_WALL_US"):  # wall-clock samples of this (the control) thread only
+                lib.sampler_start_thread(int(os.environ["SAMPLER_WALL_US"]))
             lib.sampler_enable(0)
             return lib
     return None
@@ -70,8 +72,11 @@ def main() -> None:
             S.sampler_enable(0)
         times.append((t_issue, dt))
         if reps <= 10:
+            ps = engine.plane_stats() if plane == "gpu" else {}
             print(f"{system} {blk} {plane}: issue {t_issue * 1e3:.2f} ms, total {dt * 1e3:.2f} ms, "
-                  f"{tr.swap_bytes() / dt / 1e9:.2f} GB/s, {len(tr.events)} events", flush=True)
+                  f"{tr.swap_bytes() / dt / 1e9:.2f} GB/s, {len(tr.events)} events, issuer calls "
+                  f"{ps.get('issuer_calls')} busy {ps.get('issuer_busy_ms', 0):.2f} ms, launches {ps.get('launches')}",
+                  flush=True)
         del engine
     if reps > 10:
         times.sort(key=lambda x: x[1])

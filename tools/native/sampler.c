@@ -10,7 +10,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <sys/syscall.h>
 #include <sys/time.h>
+#include <time.h>
 #include <ucontext.h>
 #include <unistd.h>
 
@@ -52,6 +54,28 @@ void sampler_start(void) {
 }
 
 __attribute__((constructor)) static void start(void) { sampler_start(); }
+
+// Wall-clock sampling of the CALLING thread only (a CLOCK_MONOTONIC hrtimer
+// aimed at this thread): microsecond resolution, blocked time included.
+// ITIMER_PROF fires at scheduler-tick granularity and on whichever thread
+// burns CPU (e.g. a spinning worker), which blurs a ~1 us/event control plane.
+void sampler_start_thread(int us) {
+    if (!getenv("SAMPLER_OUT")) return;
+    struct itimerval off = {{0, 0}, {0, 0}};
+    setitimer(ITIMER_PROF, &off, NULL);
+    struct sigevent sev;
+    memset(&sev, 0, sizeof sev);
+    sev.sigev_notify = SIGEV_THREAD_ID;
+    sev.sigev_signo = SIGPROF;
+    sev._sigev_un._tid = (pid_t)syscall(SYS_gettid);
+    timer_t t;
+    if (timer_create(CLOCK_MONOTONIC, &sev, &t) != 0) return;
+    struct itimerspec its;
+    its.it_interval.tv_sec = 0;
+    its.it_interval.tv_nsec = (long)us * 1000;
+    its.it_value = its.it_interval;
+    timer_settime(t, 0, &its, NULL);
+}
 
 // pause (0) / resume (1) recording without disarming the timer
 void sampler_enable(int on) { g_on = on; }
