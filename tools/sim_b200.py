@@ -23,7 +23,10 @@ timelines:
     its committed H2D_DATA costs only the receiver's open;
   * on-the-fly H2D_DATA = wire, then seal + open;  D2H_DATA = seal + open,
     then wire; deferred decrypts are ready when the D2H copy lands;
-  * SYNC_POINT waits for the batch's wires and opens, as in the reference.
+  * SYNC_POINT waits for the batch's wires and opens, as in the reference;
+    RESOLVE_DECRYPT is not a host wait (the open ran on the GPU): it holds
+    back the later H2D copies (one in-order stream) until that landing;
+  * a swap-out's landing never blocks the host; token D2H does.
 
 NoCc keeps the reference's own plain costing.  Parameters come from
 measured B200 numbers (see PARAMS); predictions go next to the bench's
@@ -70,7 +73,15 @@ def b200_replay_class():
         def __init__(self, trace, config, params):
             self.p = params
             self.gpu_crypto = 0
+            self.h2d_floor = 0  # host bytes a later H2D copy reads land first (stream order, not a host wait)
+            self._small_io = False
             super().__init__(trace, config)
+
+        def _dispatch_engine(self, ev) -> None:
+            # token D2H is the only transfer whose bytes the application
+            # waits for; a swap-out's landing never blocks the host here
+            self._small_io = isinstance(ev, sim.SmallIoEvent)
+            super()._dispatch_engine(ev)
 
         def _ns(self, us: float) -> int:
             return int(round(us * 1000))
@@ -92,7 +103,7 @@ def b200_replay_class():
                 kind = action.kind
                 if kind is ActionKind.SPEC_ENCRYPT:
                     # staging H2D copy of the predicted bytes, then the seal
-                    self.pcie_h2d = max(self.pcie_h2d, self.t_app) + self._wire(action.nbytes)
+                    self.pcie_h2d = max(self.pcie_h2d, self.t_app, self.h2d_floor) + self._wire(action.nbytes)
                     self.ready[action.record_id] = self._crypto(action.nbytes, 1, self.pcie_h2d)
                 elif kind is ActionKind.H2D_DATA:
                     self.t_app += issue
@@ -100,7 +111,7 @@ def b200_replay_class():
                         # ciphertext already on the device: the receiver's open
                         done = self._crypto(action.nbytes, 1, max(self.t_app, self.ready.get(action.record_id, 0)))
                     else:
-                        self.pcie_h2d = max(self.pcie_h2d, self.t_app) + self._wire(action.nbytes)
+                        self.pcie_h2d = max(self.pcie_h2d, self.t_app, self.h2d_floor) + self._wire(action.nbytes)
                         done = self._crypto(action.nbytes, 2, self.pcie_h2d)
                     self.batch_wires.append(done)
                 elif kind is ActionKind.NOP:
@@ -114,11 +125,16 @@ def b200_replay_class():
                     if action.task_id is not None:
                         self.dec_ready[action.task_id] = self.pcie_d2h
                         self.dec_tail = max(self.dec_tail, self.pcie_d2h)
-                    else:
+                    elif self._small_io:
                         self.t_app = max(self.t_app, self.pcie_d2h)
+                    else:
+                        self.dec_tail = max(self.dec_tail, self.pcie_d2h)
                 elif kind is ActionKind.RESOLVE_DECRYPT:
+                    # the host endpoint's open already ran on the GPU; the
+                    # swap-in that re-reads the block waits for the landing on
+                    # the (in-order) H2D stream, the host thread does not
                     if action.task_id in self.dec_ready:
-                        self.t_app = max(self.t_app, self.dec_ready.pop(action.task_id))
+                        self.h2d_floor = max(self.h2d_floor, self.dec_ready.pop(action.task_id))
                 elif kind is ActionKind.SYNC_POINT:
                     self.t_app = max(self.t_app, self.gpu_free, *self.batch_wires) \
                         if self.batch_wires else max(self.t_app, self.gpu_free)
@@ -161,7 +177,13 @@ def main(out_path: str) -> None:
     from paper_2411_03357_b200 import workload
 
     def ref_trace(tr):
-        return ref_workload.parse_trace_lines(list(workload.trace_to_lines(tr)))
+        # the replay here (like sp_pipe_replay) runs events back to back:
+        # arrival times are dropped so the reference measures the same thing
+        import dataclasses
+
+        rt = ref_workload.parse_trace_lines(list(workload.trace_to_lines(tr)))
+        evs = [dataclasses.replace(e, t=0) if hasattr(e, "t") else e for e in rt.events]
+        return dataclasses.replace(rt, events=evs)
 
     report = {"params": PARAMS, "model": __doc__.split("\n\n")[1]}
     # the bench's OPT-66B shape (61 x 32 MiB chunks per layer, the model's
