@@ -642,6 +642,12 @@ std::map<int, Streams> g_streams;
 std::map<int, DevicePool> g_pools;
 std::map<std::pair<int, std::string>, sp_ctx *> g_ctx;  // key setup once per (device, key)
 std::vector<std::pair<uint8_t *, uint64_t>> g_rings;    // idle pinned staging rings (process-wide)
+// Idle CUDA events per device, handed from destroyed planes to new ones:
+// cudaEventCreate takes the driver's write lock (~2-5 us beside a busy
+// issuing thread) and a fresh pipe creates hundreds of fences in its first
+// milliseconds (20% of the KV trace's control thread, sampled).
+std::map<int, std::vector<cudaEvent_t>> g_events;
+constexpr size_t kEventsWarm = 256, kEventsKeep = 8192;
 // Device buffers of destroyed pipes, idle (their streams were drained):
 // the next pipe on the device takes them without a pool call (a pipe per
 // replay / bench repetition would otherwise re-carve its whole working set).
@@ -1042,6 +1048,16 @@ class Plane {
            "cudaHostGetDevicePointer(auth flag)");
         ck(cudaMalloc(&zero_dev, kZeroBytes), "cudaMalloc(zero page)");
         ck(cudaMemset(zero_dev, 0, kZeroBytes), "cudaMemset(zero page)");
+        {
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            auto &pool = g_events[dev];
+            free_events.swap(pool);
+        }
+        while (free_events.size() < kEventsWarm) {
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            free_events.push_back(e);
+        }
         window = new_fence();
         if (Issuer::enabled_by_env()) iss.start(dev);
     }
@@ -1099,7 +1115,15 @@ class Plane {
             std::lock_guard<std::mutex> lk(g_dev_mu);
             g_rings.push_back({ring.ptr, ring.cap});
         }
-        for (cudaEvent_t e : free_events) cudaEventDestroy(e);
+        {
+            std::lock_guard<std::mutex> lk(g_dev_mu);
+            auto &pool = g_events[dev];
+            for (cudaEvent_t e : free_events) {
+                if (pool.size() < kEventsKeep) pool.push_back(e);
+                else cudaEventDestroy(e);
+            }
+            free_events.clear();
+        }
         if (auth_h) cudaFreeHost(const_cast<int32_t *>(auth_h));
         if (zero_dev) cudaFree(zero_dev);
         if (d_spans) cudaFree(d_spans);
@@ -1601,14 +1625,14 @@ class Plane {
         ls.swap(landings);
         landing_blocks.clear();
         uint64_t total = 0;
-        std::unordered_set<Fence *> waited;
+        const uint64_t mk_ready = ++mark_seq;
         for (auto &l : ls)
             for (auto &j : l.jobs) {
                 const MsgP &m = std::get<0>(j);
                 total += m->len;
-                if (m->ready && !waited.count(m->ready.get())) {
+                if (m->ready && m->ready->mark != mk_ready) {
                     wait(s.land, m->ready);
-                    waited.insert(m->ready.get());
+                    m->ready->mark = mk_ready;
                 }
             }
         BufP buf = alloc(total, s.land);
@@ -1644,12 +1668,19 @@ class Plane {
             for (auto &j : l.jobs) std::get<0>(j)->buf->use(s.land, opened, tick);
         wait(s.d2h, opened);
         Block *last = nullptr;
+        const uint64_t mk = ++mark_seq;  // one wait per distinct fence (staging copies share a batch fence)
+        auto wait_once = [&](const FenceP &f) {
+            if (f && f->mark != mk) {
+                wait(s.d2h, f);
+                f->mark = mk;
+            }
+        };
         for (auto &p : places) {
             if (p.block != last) {
                 auto it = h2d_done.find(p.block->id);
-                if (it != h2d_done.end() && it->second) wait(s.d2h, it->second);
+                if (it != h2d_done.end()) wait_once(it->second);
                 auto hr = host_ready.find(p.block->id);  // an ordered app write (same stream: no-op otherwise)
-                if (hr != host_ready.end() && hr->second) wait(s.d2h, hr->second);
+                if (hr != host_ready.end()) wait_once(hr->second);
                 last = p.block;
             }
         }
@@ -2592,9 +2623,11 @@ class Engine {
     void land(Deferred &t) {
         Block &b = mem.block(t.block_id);
         uint64_t inner = t.base - b.base;
-        PVec<std::tuple<MsgP, uint64_t, uint64_t>> jobs;
-        for (auto &c : t.chunks) jobs.emplace_back(std::get<0>(c), std::get<1>(c), inner + std::get<2>(c));
-        plane.land_on_host(b, std::move(jobs), D2H);
+        // the task's chunk list becomes the landing's job list (offsets
+        // rebased to the block): nothing reads t.chunks after its landing
+        for (auto &c : t.chunks) std::get<2>(c) += inner;
+        plane.land_on_host(b, std::move(t.chunks), D2H);
+        t.chunks.clear();
         t.landing = true;
     }
 
