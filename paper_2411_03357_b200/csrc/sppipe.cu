@@ -1870,8 +1870,20 @@ class Plane {
         return buf;
     }
 
+    // KV blocks sealed on the fly read their plaintext straight from the
+    // mapped pinned host block (k_gcm's loads cross PCIe): no staging copy,
+    // no copy fence, one link less on the swap-in chain of a decode step.
+    // Only small on-the-fly KV transfers: a big fused seal would hold every
+    // SM for the whole PCIe transfer.  SPPIPE_FUSE_H2D=0 stages as before.
+    static bool fuse_h2d_enabled() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_FUSE_H2D");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
     PVec<MsgP> seal_host_chunks(Block &b, uint64_t inner, const Spans &spans,
-                                       int dir, uint64_t iv0) {
+                                       int dir, uint64_t iv0, bool fuse = false) {
         PVec<MsgP> msgs;
         if (dry) {
             for (auto &sp : spans) {
@@ -1881,6 +1893,43 @@ class Plane {
                 bytes_h2d += sp.second;
             }
             return msgs;
+        }
+        if (fuse && b.host_dev && fuse_h2d_enabled()) {
+            before_host_read_of(b.id);
+            uint64_t first = spans[0].first, total = 0;
+            for (auto &sp : spans) total += sp.second;
+            if (total <= (1u << 20)) {
+                FenceP landed;
+                auto it = host_ready.find(b.id);
+                if (it != host_ready.end() && it->second && it->second->recorded) landed = it->second;
+                BufP buf = alloc(round16(total) + kTag * spans.size(), s.comp);
+                for (size_t i = 0; i < spans.size(); ++i) {
+                    auto m = pmake<Msg>();
+                    m->buf = buf;
+                    m->off = spans[i].first - first;
+                    m->len = spans[i].second;
+                    m->tag_off = round16(total) + kTag * i;
+                    Op op;
+                    op.d.dir = (uint32_t)dir;
+                    op.d.reserved = SP_OP_SEAL;
+                    op.d.iv = iv0 + i;
+                    op.d.len = m->len;
+                    op.d.src = b.host_dev + inner + spans[i].first;
+                    op.d.dst = buf->ptr + m->off;
+                    op.d.tag = buf->ptr + m->tag_off;
+                    op.d.status = nullptr;
+                    op.b = buf;
+                    op.w[op.nw++] = Region{buf.get(), m->off, m->off + m->len};
+                    op.w[op.nw++] = Region{buf.get(), m->tag_off, m->tag_off + kTag};
+                    op.wait = landed;  // the block's last landing lands before we read it
+                    m->ready = window;
+                    queue(std::move(op), m->len);
+                    msgs.push_back(m);
+                }
+                h2d_done[b.id] = window;  // recorded by the flush that issues these seals
+                bytes_h2d += total;
+                return msgs;
+            }
         }
         FenceP done;
         BufP buf = stage_h2d(b, inner, spans, done, otf_copies);
@@ -2758,7 +2807,7 @@ class Engine {
         resolve_decrypts_over(r.base, r.len, true);
         auto bi = mem.block_at(r.base, r.len);
         auto spans = chunk_spans(r.len, cfg.chunk_bytes);
-        auto msgs = plane.seal_host_chunks(*bi.first, bi.second, spans, H2D, send_iv[H2D]);
+        auto msgs = plane.seal_host_chunks(*bi.first, bi.second, spans, H2D, send_iv[H2D], r.cls == TC_KV);
         for (size_t i = 0; i < spans.size(); ++i)
             send_h2d(msgs[i], NONE, Meta{0, sq, r.block_id, r.base, spans[i].first, spans[i].second}, sq);
         drain_soon();
