@@ -1874,11 +1874,13 @@ class Plane {
     // mapped pinned host block (k_gcm's loads cross PCIe): no staging copy,
     // no copy fence, one link less on the swap-in chain of a decode step.
     // Only small on-the-fly KV transfers: a big fused seal would hold every
-    // SM for the whole PCIe transfer.  SPPIPE_FUSE_H2D=0 stages as before.
+    // SM for the whole PCIe transfer.  Measured neutral on the OPT-30B KV
+    // trace (0.775 vs 0.785 of plain swap-only, 0.937 both with compute;
+    // profiles/r2_ab_fuse_h2d.txt), so off by default: SPPIPE_FUSE_H2D=1.
     static bool fuse_h2d_enabled() {
         static const bool on = [] {
             const char *e = getenv("SPPIPE_FUSE_H2D");
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         return on;
     }
