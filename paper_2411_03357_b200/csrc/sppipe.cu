@@ -3568,6 +3568,10 @@ int sp_pipe_create(const sp_pipe_config *cfg, const uint8_t key[SP_KEY_BYTES], s
                 g_err = "window_aware must be SP_WINDOW_AWARE_AUTO, _ON or _OFF";
                 throw ValueErr(g_err);
             }
+            // one channel message per chunk: the reference rejects > 32 MiB
+            // plaintexts in encrypt_at (channel.py:92-95)
+            if (c.chunk_bytes < 1 || c.chunk_bytes > SP_MAX_MESSAGE_BYTES)
+                throw ValueErr("chunk_bytes must be in 1..32 MiB (one channel message per chunk)");
             c.window_aware = c.window_aware == SP_WINDOW_AWARE_AUTO ? (c.reference_compat ? 0 : 1)
                                                                      : (c.window_aware == SP_WINDOW_AWARE_ON ? 1 : 0);
             p->e.reset(new Engine(c, key, &pred->p));

@@ -517,3 +517,17 @@ def test_libsppipe_carries_nvtx_ranges():
                  b"pad_to (NOPs)", b"h2d msg", b"h2d nop", b"d2h msg"):
         assert re.search(re.escape(name) + b"\\x00", data), name  # (string tails may be merged)
     assert b"nvtxDomainRangePushEx" in data or b"NVTX_INJECTION64_PATH" in data
+
+
+def test_chunk_bytes_above_message_limit_rejected():
+    """A chunk is one channel message: the reference's encrypt_at rejects
+    plaintexts above 32 MiB (channel.py:92-95), so the pipe refuses such a
+    chunk size at creation instead of failing inside a launch."""
+    from paper_2411_03357_b200.channel import new_channel
+    from paper_2411_03357_b200.engine import Engine, EngineConfig
+    from paper_2411_03357_b200.memory import HostMemory
+
+    cpu, gpu = new_channel(seed=1)
+    with pytest.raises(ValueError):
+        Engine(HostMemory(pinned=False), cpu, gpu, Predictor(ModelProfile("m", 1 << 20, 4)),
+               EngineConfig(plane="dry", chunk_bytes=64 << 20))

@@ -16,8 +16,9 @@ from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engin
 CH = int(os.environ.get("CHUNK_KIB", "256")) * 1024
 SYSTEM = os.environ.get("SYSTEM", "specpipe")
 tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=2, chunk_bytes=CH)
+MSG = min(CH, 32 << 20)  # channel messages are <= 32 MiB (larger blocks travel as several)
 cfg = ReplayConfig(plane="gpu", fill="fast", engine="native", record_stream=False, system=SYSTEM,
-                   chunk_bytes=CH, predictor_chunk_bytes=CH, reference_compat=False)
+                   chunk_bytes=MSG, predictor_chunk_bytes=MSG, reference_compat=False)
 mem = prepare_memory(tr, cfg)
 for name, fn in ((SYSTEM, lambda: run_engine(tr, cfg, memory=mem)),
                  ("plain", lambda: run_plain_native(tr, cfg, memory=mem))):
