@@ -245,7 +245,7 @@ struct Buf : RcBase {
     uint8_t *ptr = nullptr;
     uint64_t size = 0;
     uint64_t alloc_size = 0;
-    PVec<std::pair<cudaStream_t, FenceP>> uses;  // latest fence per stream
+    SmallVec<std::pair<cudaStream_t, FenceP>, 4> uses;  // latest fence per stream
     uint64_t last_use = 0;
     cudaStream_t last_stream = nullptr;
     uint32_t queued = 0;       // ops in the compute queue that touch this buffer (not yet issued)
@@ -937,7 +937,7 @@ class Plane {
     std::vector<cudaEvent_t> free_events;
     struct Garbage {
         uint8_t *ptr;
-        PVec<std::pair<cudaStream_t, FenceP>> uses;
+        SmallVec<std::pair<cudaStream_t, FenceP>, 4> uses;
         cudaStream_t last;
         uint64_t size;
     };
@@ -1235,11 +1235,23 @@ class Plane {
         }();
         return on;
     }
-    std::map<std::pair<cudaStream_t, int>, Rc<Slab>> slabs;  // open slab per (stream, lane)
+    // open slab per (stream, lane): a handful of keys, searched linearly
+    struct OpenSlab {
+        cudaStream_t st;
+        int lane;
+        Rc<Slab> slab;
+    };
+    std::vector<OpenSlab> slabs;
+    Rc<Slab> &open_slab(cudaStream_t st, int lane) {
+        for (auto &o : slabs)
+            if (o.st == st && o.lane == lane) return o.slab;
+        slabs.push_back(OpenSlab{st, lane, Rc<Slab>()});
+        return slabs.back().slab;
+    }
     // lane separates lifetimes: 0 = transient staging, 1 = device copies of blocks
     BufP alloc(uint64_t n, cudaStream_t st, int lane = 0) {
         if (!dry && n <= kSlabMax && slabs_enabled()) {
-            auto &sl = slabs[{st, lane}];
+            auto &sl = open_slab(st, lane);
             const uint64_t need = (std::max<uint64_t>(n, 16) + 255u) & ~uint64_t(255);
             if (!sl || sl->off + need > sl->big->size) {
                 sl = pmake<Slab>();
@@ -2564,7 +2576,7 @@ struct Meta {
 };
 struct Lane {
     std::deque<MsgP> queue;
-    std::vector<sp_sent> log;
+    std::deque<sp_sent> log;
 };
 struct Recorded {
     uint64_t seq, addr, n;
@@ -2588,7 +2600,7 @@ class Engine {
     Validator val;
     Lane lanes[2];
     uint64_t send_iv[2], recv_iv[2];  // [H2D]: cpu send / gpu recv; [D2H]: gpu send / cpu recv
-    std::vector<sp_action> actions;
+    std::deque<sp_action> actions;  // grows without copying (a 64 KiB-chunk run logs ~0.5M actions)
     int64_t counters[C_COUNT] = {};
     bool otf_burned_present = false;
     uint64_t initial_send_iv;
