@@ -1774,6 +1774,7 @@ class Plane {
         std::vector<void *> dsts, srcs;
         std::vector<size_t> sizes;
         std::vector<XferJob> jobs;
+        jobs.reserve(count);
         const uint64_t xmax = xfer_max();
         for (size_t i = 0; i < count; ++i) {
             void *d = nullptr, *s0 = nullptr;

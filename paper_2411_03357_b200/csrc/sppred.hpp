@@ -26,6 +26,8 @@
 #include <unordered_set>
 #include <vector>
 
+#include "sppool.hpp"
+
 namespace sppipe {
 
 struct ValueErr : std::runtime_error { using std::runtime_error::runtime_error; };
@@ -157,7 +159,7 @@ class Predictor {
         }
         events_.push_back({1, (int64_t)in_batches_.size()});
         in_batches_.push_back(intern(batch));
-        std::unordered_set<int64_t> bs(batch.begin(), batch.end());
+        PUSet<int64_t> bs(batch.begin(), batch.end());
         for (int64_t b : batch) out_pos_.erase(b);
         // LIFO/FIFO streaks against the stack of all swap-outs (predictor.py:231-239)
         size_t k = batch.size(), n = stack_.size();
@@ -332,7 +334,7 @@ class Predictor {
     std::vector<std::vector<Prediction>> script_rounds_;
     size_t script_next_ = 0;
     std::unordered_set<int64_t> script_out_;
-    std::unordered_set<int64_t> out_pos_;
+    PUSet<int64_t> out_pos_;  // pooled nodes: one insert per swap-out, one erase per swap-in
     std::vector<int64_t> stack_;
     std::vector<int64_t> open_;
     std::vector<std::vector<int64_t>> groups_;
