@@ -1063,6 +1063,7 @@ class Plane {
     }
     ~Plane() {
         if (dry) return;
+        if (!g_forked.load()) dbg_print();
         if (g_forked.load()) {
             // CUDA is unusable in a forked child: no stream syncs or frees
             // (the parent still owns the device memory); members unwind
@@ -1130,9 +1131,61 @@ class Plane {
     }
 
     // -- events / buffers --------------------------------------------------------------
+    // SPPIPE_DEBUG_TIMES=1 (diagnostics): fences get timing events, and every
+    // swap-out launch logs when each of its waits and its own fence completed
+    // (ms after the plane's first record), printed when the plane closes.
+    static bool dbg_times() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_DEBUG_TIMES");
+            return e && e[0] == '1';
+        }();
+        return on;
+    }
+    cudaEvent_t dbg_base = nullptr;
+    struct DbgEntry {
+        const char *what;
+        cudaStream_t st;
+        FenceP f;
+        uint64_t batch;
+    };
+    std::vector<DbgEntry> dbg_log;
+    uint64_t dbg_batches = 0;
+    const char *stream_name(cudaStream_t st) const {
+        if (st == s.comp) return "comp";
+        if (st == s.comp2) return "comp2";
+        if (st == s.h2d) return "h2d";
+        if (st == s.d2h) return "d2h";
+        if (st == s.land) return "land";
+        if (st == s.out) return "out";
+        if (st == s.spec) return "spec";
+        if (st == s.host) return "host";
+        if (st == s.app) return "app";
+        return "?";
+    }
+    void dbg_print() {
+        if (!dbg_base) return;
+        iss.drain();
+        cudaDeviceSynchronize();
+        for (auto &d : dbg_log) {
+            float ms = -1;
+            if (d.f && d.f->recorded && cudaEventElapsedTime(&ms, dbg_base, d.f->ev) != cudaSuccess) ms = -2;
+            fprintf(stderr, "[dbg] batch %llu %-10s %-6s %9.3f ms\n", (unsigned long long)d.batch, d.what,
+                    stream_name(d.st), ms);
+        }
+        cudaGetLastError();
+        dbg_log.clear();
+    }
     FenceP new_fence() {
         auto f = pmake<Fence>();
         f->plane = this;
+        if (dbg_times()) {
+            if (!dbg_base) {
+                ck(cudaEventCreate(&dbg_base), "cudaEventCreate(dbg)");
+                ck(cudaEventRecord(dbg_base, s.comp), "cudaEventRecord(dbg)");
+            }
+            ck(cudaEventCreate(&f->ev), "cudaEventCreate(dbg)");
+            return f;
+        }
         if (!free_events.empty()) {
             f->ev = free_events.back();
             free_events.pop_back();
@@ -1560,6 +1613,7 @@ class Plane {
                 ++launches;
             }
             record(window, cs, "rec_flush");
+            if (dbg_times()) dbg_log.push_back({"flush", cs, window, flush_no});
             ++tick;
             for (auto &op : q) {
                 if (op.a) {
@@ -1674,6 +1728,7 @@ class Plane {
         post_batch(2, descs, s.land, "sp_open_batch(landing)");
         ++launches;
         FenceP opened = record_new(s.land, "rec_land");
+        if (dbg_times()) dbg_log.push_back({"landed", s.land, opened, dbg_batches});
         ++tick;
         buf->use(s.land, opened, tick);
         for (auto &l : ls)
@@ -1702,6 +1757,7 @@ class Plane {
             n = places[i].n;
         });
         FenceP ev = record_new(s.d2h, "rec_d2h");
+        if (dbg_times()) dbg_log.push_back({"d2h-done", s.d2h, ev, dbg_batches});
         buf->use(s.d2h, ev, ++tick);
         for (auto &l : ls) host_ready[l.block->id] = ev;
         bytes_d2h += total;
@@ -2128,8 +2184,13 @@ class Plane {
     void launch_out() {
         if (outb.items.empty()) return;
         std::unordered_set<Fence *> seen;
+        const uint64_t bno = ++dbg_batches;
         for (auto &f : outb.waits)
-            if (seen.insert(f.get()).second) wait(s.out, f);
+            if (seen.insert(f.get()).second) {
+                wait(s.out, f);
+                if (dbg_times()) dbg_log.push_back({"out-wait", f->stream, f, bno});
+            }
+        if (dbg_times()) dbg_log.push_back({"out-ready", s.out, outb.ready, bno});
         post_batch(1, outb.items, s.out, "sp_seal_batch(swap-out)");
         ++launches;
         record(outb.ready, s.out, "rec_out");
