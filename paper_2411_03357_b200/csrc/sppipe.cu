@@ -1383,7 +1383,15 @@ class Plane {
             }
             b->alloc_size = cls;
             b->last_stream = st;
-            b->uses.emplace_back(st, FenceP());
+            // The allocation point on st, recorded now: another stream that
+            // later orders after "st's last use" of this buffer waits only
+            // for the allocation, not for whatever st is running by then.
+            // (A null entry used to be resolved by recording a fence on st
+            // at free time, which made the freeing stream — e.g. the swap-out
+            // stream — wait for st's whole backlog: with many 16 MiB
+            // swap-ins queued on the compute streams, swap-out seals stalled
+            // until the layer's swap-in finished; profiles/r2_dbg_out_waits.)
+            b->uses.emplace_back(st, record_new(st, "rec_alloc"));
         }
         return b;
     }
