@@ -1330,6 +1330,8 @@ class Plane {
         b->plane = this;
         b->size = n;
         if (!dry) {
+            bool cache_reuse = false;  // taken from the cache with every other stream's old fence passed
+            FenceP reuse_fence;
             const uint64_t cls = size_class(n);
             auto it = cache.find(cls);
             if (it != cache.end()) {
@@ -1339,8 +1341,15 @@ class Plane {
                 for (size_t k = 0; k < lim; ++k) {
                     if (!reusable(v[k], st)) continue;
                     b->ptr = v[k].ptr;
+                    // every other stream's old use has passed; st's own old
+                    // use (if any) may still run: carry its fence, so a
+                    // stream other than st that touches the buffer first
+                    // orders after it
+                    for (auto &u : v[k].uses)
+                        if (u.first == st) reuse_fence = u.second && u.second->recorded ? u.second : record_new(st, "rec_alloc");
                     v.erase(v.begin() + (long)k);
                     cached_bytes -= cls;
+                    cache_reuse = true;
                     break;
                 }
                 // Backpressure: past the pool budget, wait for the oldest
@@ -1375,14 +1384,19 @@ class Plane {
                     pool_bytes += cls;
                 }
             }
+            bool fresh = false;
             if (!b->ptr) {
                 void *p = nullptr;
                 ck(cudaMallocFromPoolAsync(&p, cls, pool, st), "cudaMallocFromPoolAsync");
                 b->ptr = static_cast<uint8_t *>(p);
                 pool_bytes += cls;
+                fresh = true;
             }
             b->alloc_size = cls;
             b->last_stream = st;
+            // A reused cache buffer carries st's old fence (or nothing when
+            // st never touched it).  A fresh pool allocation (or a
+            // backpressure / idle-pool buffer) is ordered on st:
             // The allocation point on st, recorded now: another stream that
             // later orders after "st's last use" of this buffer waits only
             // for the allocation, not for whatever st is running by then.
@@ -1391,7 +1405,11 @@ class Plane {
             // stream — wait for st's whole backlog: with many 16 MiB
             // swap-ins queued on the compute streams, swap-out seals stalled
             // until the layer's swap-in finished; profiles/r2_dbg_out_waits.)
-            b->uses.emplace_back(st, record_new(st, "rec_alloc"));
+            if (cache_reuse && !fresh) {
+                if (reuse_fence) b->uses.emplace_back(st, reuse_fence);
+            } else {
+                b->uses.emplace_back(st, record_new(st, "rec_alloc"));
+            }
         }
         return b;
     }
