@@ -1485,6 +1485,7 @@ class Plane {
         ck(cudaStreamSynchronize(s.comp), "sync comp");
         ck(cudaStreamSynchronize(s.comp2), "sync comp2");
         ck(cudaStreamSynchronize(s.land), "sync land");
+        ck(cudaStreamSynchronize(s.out), "sync out");  // landing opens behind out-stream seals
         ck(cudaStreamSynchronize(s.d2h), "sync d2h");
         opens_unchecked = 0;
         if (*auth_h) {
@@ -1712,22 +1713,39 @@ class Plane {
         ring.busy.emplace_back(lo, lo + n, f);
     }
 
+    static bool land_on_out_enabled() {  // SPPIPE_LAND_ON_OUT=0: landings always on the land stream (A/B)
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_LAND_ON_OUT");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
     void flush_landings() {
         std::vector<Landing> ls;
         ls.swap(landings);
         landing_blocks.clear();
         uint64_t total = 0;
-        const uint64_t mk_ready = ++mark_seq;
+        // Landings of messages sealed on the out stream alone (KV evictions,
+        // >= 4 MiB swap-outs) open right behind their seals on that stream:
+        // no event hop between the seal and the host endpoint's open.
+        bool on_out = land_on_out_enabled();
         for (auto &l : ls)
             for (auto &j : l.jobs) {
                 const MsgP &m = std::get<0>(j);
                 total += m->len;
+                if (!m->ready || !m->ready->recorded || m->ready->stream != s.out) on_out = false;
+            }
+        const cudaStream_t ls_st = on_out ? s.out : s.land;
+        const uint64_t mk_ready = ++mark_seq;
+        for (auto &l : ls)
+            for (auto &j : l.jobs) {
+                const MsgP &m = std::get<0>(j);
                 if (m->ready && m->ready->mark != mk_ready) {
-                    wait(s.land, m->ready);
+                    wait(ls_st, m->ready);
                     m->ready->mark = mk_ready;
                 }
             }
-        BufP buf = alloc(total, s.land);
+        BufP buf = alloc(total, ls_st);
         std::vector<sp_desc> descs;
         struct Place {
             Block *block;
@@ -1751,14 +1769,14 @@ class Plane {
                 places.push_back({l.block, off, std::get<2>(j), m->len});
                 off += m->len;
             }
-        post_batch(2, descs, s.land, "sp_open_batch(landing)");
+        post_batch(2, descs, ls_st, "sp_open_batch(landing)");
         ++launches;
-        FenceP opened = record_new(s.land, "rec_land");
-        if (dbg_times()) dbg_log.push_back({"landed", s.land, opened, dbg_batches});
+        FenceP opened = record_new(ls_st, "rec_land");
+        if (dbg_times()) dbg_log.push_back({"landed", ls_st, opened, dbg_batches});
         ++tick;
-        buf->use(s.land, opened, tick);
+        buf->use(ls_st, opened, tick);
         for (auto &l : ls)
-            for (auto &j : l.jobs) std::get<0>(j)->buf->use(s.land, opened, tick);
+            for (auto &j : l.jobs) std::get<0>(j)->buf->use(ls_st, opened, tick);
         wait(s.d2h, opened);
         Block *last = nullptr;
         const uint64_t mk = ++mark_seq;  // one wait per distinct fence (staging copies share a batch fence)
