@@ -685,11 +685,25 @@ Streams streams_for(int dev) {
     auto it = g_streams.find(dev);
     if (it != g_streams.end()) return it->second;
     Streams s;
-    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
-    for (auto p : all) ck(cudaStreamCreateWithFlags(p, cudaStreamNonBlocking), "cudaStreamCreate");
-    int lo = 0, hi = 0;  // the model's compute outranks the crypto launches
+    // Stream priorities (SPPIPE_PRIO): "crypto" (default) — the data plane's
+    // streams outrank the model's compute, so a seal/open/transfer launched
+    // while a compute kernel fills the GPU gets SMs as soon as one of the
+    // compute's CTAs retires (~20 us) instead of after the whole kernel
+    // (~300 us): on the KV trace each decode step's swap-out landing ->
+    // D2H -> swap-in -> open chain used to wait out the compute kernel before
+    // it (profiles/r2_dbg_kv_compute).  "app": the compute outranks the data
+    // plane (r1 policy); "equal": one priority.
+    static const int mode = [] {
+        const char *e = getenv("SPPIPE_PRIO");
+        if (!e) return 0;
+        return std::string(e) == "app" ? 1 : (std::string(e) == "equal" ? 2 : 0);
+    }();
+    int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-    ck(cudaStreamCreateWithPriority(&s.app, cudaStreamNonBlocking, hi), "cudaStreamCreate(app)");
+    const int plane_prio = mode == 0 ? hi : lo, app_prio = mode == 1 ? hi : lo;
+    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
+    for (auto p : all) ck(cudaStreamCreateWithPriority(p, cudaStreamNonBlocking, plane_prio), "cudaStreamCreate");
+    ck(cudaStreamCreateWithPriority(&s.app, cudaStreamNonBlocking, app_prio), "cudaStreamCreate(app)");
     g_streams[dev] = s;
     return s;
 }
@@ -1053,6 +1067,12 @@ class Plane {
             auto &pool = g_events[dev];
             free_events.swap(pool);
         }
+        if (dbg_times())
+            for (int i = 0; i < 16384; ++i) {
+                cudaEvent_t e;
+                ck(cudaEventCreate(&e), "cudaEventCreate(dbg)");
+                dbg_events.push_back(e);
+            }
         while (free_events.size() < kEventsWarm) {
             cudaEvent_t e;
             ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -1142,6 +1162,7 @@ class Plane {
         return on;
     }
     cudaEvent_t dbg_base = nullptr;
+    std::vector<cudaEvent_t> dbg_events;
     struct DbgEntry {
         const char *what;
         cudaStream_t st;
@@ -1149,7 +1170,7 @@ class Plane {
         uint64_t batch;
     };
     std::vector<DbgEntry> dbg_log;
-    uint64_t dbg_batches = 0;
+    uint64_t dbg_batches = 0, dbg_computes = 0;
     const char *stream_name(cudaStream_t st) const {
         if (st == s.comp) return "comp";
         if (st == s.comp2) return "comp2";
@@ -1183,7 +1204,12 @@ class Plane {
                 ck(cudaEventCreate(&dbg_base), "cudaEventCreate(dbg)");
                 ck(cudaEventRecord(dbg_base, s.comp), "cudaEventRecord(dbg)");
             }
-            ck(cudaEventCreate(&f->ev), "cudaEventCreate(dbg)");
+            if (!dbg_events.empty()) {  // timing events made up front (no driver call per fence)
+                f->ev = dbg_events.back();
+                dbg_events.pop_back();
+            } else {
+                ck(cudaEventCreate(&f->ev), "cudaEventCreate(dbg)");
+            }
             return f;
         }
         if (!free_events.empty()) {
@@ -1822,6 +1848,7 @@ class Plane {
             n = cb.n[i];
         });
         record(cb.fence, s.h2d, "rec_copy");
+        if (dbg_times()) dbg_log.push_back({"h2d-copy", s.h2d, cb.fence, dbg_computes});
         ++tick;
         for (auto &b : cb.keep) b->use(s.h2d, cb.fence, tick);
         cb.dst.clear();
@@ -2131,6 +2158,7 @@ class Plane {
             p->post_batch(1, items, p->s.spec, "sp_seal_batch(spec)");
             ++p->launches;
             p->record(ready, p->s.spec, "rec_spec");
+            if (p->dbg_times()) p->dbg_log.push_back({"spec", p->s.spec, ready, p->dbg_computes});
             ++p->tick;
             for (auto &b : bufs) b->use(p->s.spec, ready, p->tick);
             items.clear();
@@ -2488,7 +2516,10 @@ class Plane {
             span_cap = cap;
         }
         for (int k = 0; k < ndeps; ++k)
-            if (deps[k]) wait(s.app, deps[k]);
+            if (deps[k]) {
+                wait(s.app, deps[k]);
+                if (dbg_times()) dbg_log.push_back({"comp-in", deps[k]->stream, deps[k], ++dbg_computes});
+            }
         unsigned long long *slot = d_spans + 2 * span_used++;
         const cudaStream_t st = s.app;
         const unsigned grid = (unsigned)(sms * kComputeCtasPerSm * kComputeWaves);
@@ -2497,6 +2528,7 @@ class Plane {
             ck(cudaGetLastError(), "k_layer_compute launch");
         }, "compute");
         app_fence = record_new(s.app, "rec_compute");
+        if (dbg_times()) dbg_log.push_back({"comp-done", s.app, app_fence, dbg_computes});
         ++compute_launches;
         compute_ns_requested += ns;
     }
@@ -2555,7 +2587,7 @@ class Plane {
 };
 
 Fence::~Fence() {
-    if (plane && ev) plane->free_events.push_back(ev);
+    if (plane && ev) (Plane::dbg_times() ? plane->dbg_events : plane->free_events).push_back(ev);
 }
 Buf::~Buf() {
     if (slab) {

@@ -12,7 +12,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_03357_b200 import workload  # noqa: E402
 from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engine, run_plain_native  # noqa: E402
 
-sizes = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [64, 1024, 32768, 262144]
+sizes = ([int(x) for x in sys.argv[1].split(",") if x and x != "none"] if len(sys.argv) > 1
+         else [64, 1024, 32768, 262144])
 env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("SPPIPE_", "SPGCM_"))) or "default"
 reps = int(os.environ.get("AB_REPS", "2"))
 
