@@ -628,19 +628,21 @@ void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, u
 }
 
 // Launch policy by the batch's rows:
-//   <= SPGCM_SMALL_ROWS (default 256 rows = 128 KiB: NOP pads, tokens, KV
-//      blocks): the SmallTabs variant, 10 KB of tables per CTA, 128-thread
-//      CTAs, up to 4 per SM, SPGCM_SMALL_RPW (default 2) rows per warp;
-//   above: BigTabs, SPGCM_ROWS_PER_WARP (default 4) rows per warp.
-// SPGCM_TINY_ROWS=n (default 0 = off) sends batches of <= n rows to BigTabs
-// at 1 row per warp (2 above 256 rows).  Alone on the GPU that is faster
-// (profiles/r2_launch_shape_sweep.txt, r2_launch_latency_tiny.txt: 1 x 64
-// KiB 8.9 -> 6.2 us, 1 x 224 KiB 9.5 -> 7.6 us, 2 KiB token 8.2 -> 6.1 us
-// per launch), but each such launch holds up to 148 SMs with a 192 KiB
-// table fill per working warp, and beside the model's compute the traces
-// ran slower (64 KiB-chunk offload 0.76 -> 0.70 of plain, KV 0.94 -> 0.92,
-// profiles/r2_ab_tiny.txt), so it is off.  SmallTabs above 256 rows lost
-// everywhere (4 x 224 KiB 11.3 -> 15.4 us).
+//   <= SPGCM_TINY_ROWS (default 512 rows = 256 KiB: NOP pads, tokens, one KV
+//      block): BigTabs at 1 row per warp (2 above 256 rows) — the shortest
+//      serial chain per warp wins despite the 192 KiB table fill
+//      (profiles/r2_launch_shape_sweep.txt, device time per launch in a CUDA
+//      graph: 1 x 64 KiB 8.9 -> 6.2 us, 1 x 224 KiB 9.5 -> 7.6 us, 2 KiB
+//      token 8.2 -> 6.1 us against SmallTabs).  Such a launch holds up to
+//      148 SMs for a few us; while the model's compute outranked the data
+//      plane that slowed the traces (r2_ab_tiny.txt), with the data plane's
+//      streams on top it is neutral to slightly faster (64 KiB chunks with
+//      compute 0.89 -> 0.91 of plain, r2_ab_tiny_prio.txt);
+//   <= SPGCM_SMALL_ROWS (default 256; only reached with SPGCM_TINY_ROWS=0):
+//      the SmallTabs variant, 10 KB of tables per CTA, 128-thread CTAs, up
+//      to 4 per SM, SPGCM_SMALL_RPW (default 2) rows per warp;
+//   above: BigTabs, SPGCM_ROWS_PER_WARP (default 4) rows per warp (SmallTabs
+//      above 256 rows lost everywhere: 4 x 224 KiB 11.3 -> 15.4 us).
 uint64_t env_u64(const char *name, uint64_t dflt) {
     const char *e = getenv(name);
     return e ? (uint64_t)atoll(e) : dflt;
@@ -650,7 +652,7 @@ uint64_t small_rows_max() {
     return v;
 }
 uint64_t tiny_rows_max() {
-    static const uint64_t v = env_u64("SPGCM_TINY_ROWS", 0);
+    static const uint64_t v = env_u64("SPGCM_TINY_ROWS", 512);
     return v;
 }
 uint64_t small_rows_per_warp() {
