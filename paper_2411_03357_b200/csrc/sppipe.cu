@@ -696,13 +696,16 @@ Streams streams_for(int dev) {
     static const int mode = [] {
         const char *e = getenv("SPPIPE_PRIO");
         if (!e) return 0;
-        return std::string(e) == "app" ? 1 : (std::string(e) == "equal" ? 2 : 0);
+        const std::string v(e);
+        return v == "app" ? 1 : (v == "equal" ? 2 : (v == "spec_low" ? 3 : 0));
     }();
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-    const int plane_prio = mode == 0 ? hi : lo, app_prio = mode == 1 ? hi : lo;
+    const int plane_prio = (mode == 0 || mode == 3) ? hi : lo, app_prio = mode == 1 ? hi : lo;
     cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
-    for (auto p : all) ck(cudaStreamCreateWithPriority(p, cudaStreamNonBlocking, plane_prio), "cudaStreamCreate");
+    for (auto p : all)
+        ck(cudaStreamCreateWithPriority(p, cudaStreamNonBlocking, (mode == 3 && p == &s.spec) ? lo : plane_prio),
+           "cudaStreamCreate");
     ck(cudaStreamCreateWithPriority(&s.app, cudaStreamNonBlocking, app_prio), "cudaStreamCreate(app)");
     g_streams[dev] = s;
     return s;

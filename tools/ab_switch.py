@@ -43,6 +43,14 @@ for kib in sizes:
     base = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", engine="native",
                         chunk_bytes=msg, predictor_chunk_bytes=msg, reference_compat=False)
     print(json.dumps({"env": env, "block_kib": kib, **arms(tr, base)}), flush=True)
+if os.environ.get("AB_175B"):  # the bench's OPT-175B 4-bit leg (2 x 906 MB layers, 2 iterations)
+    tr = workload.gen_opt_offload_trace("opt-175b", [1, 2], iterations=2, seed=0, quant_bits=4)
+    base = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", engine="native")
+    print(json.dumps({"env": env, "trace": "opt175b_4bit", **arms(tr, base)}), flush=True)
+if os.environ.get("AB_66B"):  # the bench's OPT-66B leg (8 iterations)
+    tr = workload.gen_opt_offload_trace("opt-66b", [1, 2], iterations=8, seed=0)
+    base = ReplayConfig(system="specpipe", plane="gpu", record_stream=False, fill="fast", engine="native")
+    print(json.dumps({"env": env, "trace": "opt66b_8it", **arms(tr, base)}), flush=True)
 kv = workload.gen_adversarial_trace(
     workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=0), 0.25, seed=8)
 reps = 5

@@ -10,7 +10,7 @@ from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engin
 kv = workload.gen_adversarial_trace(
     workload.gen_kvswap_trace(48, "lifo", kv_block_bytes=229_376, parallel_size=4, seed=0), 0.25, seed=8)
 cfg = ReplayConfig(system=os.environ.get("SYSTEM", "specpipe"), plane="gpu", record_stream=False, fill="fast",
-                   engine="native", reference_compat=False, compute=True)
+                   engine="native", reference_compat=False, compute=os.environ.get("COMPUTE", "1") == "1")
 mem = prepare_memory(kv, cfg)
 which = os.environ.get("ARM", "engine")
 fn = (lambda: run_engine(kv, cfg, memory=mem)) if which == "engine" else (lambda: run_plain_native(kv, cfg, memory=mem))
