@@ -1873,10 +1873,34 @@ class Plane {
     // Device aliases of pinned host memory the plane copies to or from
     // (registered blocks, the token ring): host lo -> (host hi, device lo).
     std::map<uintptr_t, std::pair<uintptr_t, uintptr_t>> host_alias;
+    // Ranges with the same host->device offset that touch or sit within 64
+    // KiB of each other (page-padded blocks of one pinned slab; under UVA the
+    // offset is 0 for all pinned memory) are merged: a 64 KiB-chunk layer
+    // registers ~31k blocks, and a lookup per copy walked a map that size.
+    // Plane copies never span two blocks, so the padding between merged
+    // blocks is never translated.
     void add_alias(const void *host, uint64_t len, const void *dev) {
         if (!host || !dev || !len) return;
-        const uintptr_t lo = reinterpret_cast<uintptr_t>(host);
-        host_alias[lo] = {lo + len, reinterpret_cast<uintptr_t>(dev)};
+        uintptr_t lo = reinterpret_cast<uintptr_t>(host), hi = lo + len;
+        const uintptr_t dlo = reinterpret_cast<uintptr_t>(dev);
+        const intptr_t delta = (intptr_t)(dlo - lo);
+        constexpr uintptr_t kGap = 64u << 10;
+        auto it = host_alias.upper_bound(lo);
+        if (it != host_alias.begin()) {  // a range starting at or before lo
+            auto pv = std::prev(it);
+            if ((intptr_t)(pv->second.second - pv->first) == delta && pv->second.first + kGap >= lo) {
+                lo = pv->first;
+                hi = std::max(hi, pv->second.first);
+                host_alias.erase(pv);
+            }
+        }
+        it = host_alias.lower_bound(lo);
+        while (it != host_alias.end() && it->first <= hi + kGap &&
+               (intptr_t)(it->second.second - it->first) == delta) {  // following ranges
+            hi = std::max(hi, it->second.first);
+            it = host_alias.erase(it);
+        }
+        host_alias[lo] = {hi, (uintptr_t)((intptr_t)lo + delta)};
     }
     // device address of [host, host + n), or null when not inside one mapped range
     void *dev_alias(const void *host, uint64_t n) const {
@@ -1953,7 +1977,12 @@ class Plane {
             p.j[k] = jobs[k];
             bytes += jobs[k].n;
         }
-        const unsigned ctas = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(64, (bytes + 32767) >> 15));
+        static const uint64_t max_ctas = [] {  // SPPIPE_XFER_CTAS: grid cap (A/B)
+            const char *e = getenv("SPPIPE_XFER_CTAS");
+            const long v = e ? atol(e) : 64;
+            return (uint64_t)std::max(1L, v);
+        }();
+        const unsigned ctas = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(max_ctas, (bytes + 32767) >> 15));
         k_xfer<N><<<ctas, kXferThreads, 0, st>>>(p);
         ck(cudaGetLastError(), "k_xfer launch");
     }
