@@ -2014,7 +2014,7 @@ class Plane {
                                          : (kind == 1 ? sp_seal_batch(c, p, n, st) : sp_open_batch(c, p, n, st));
                 ck_sp(rc, what);
             }
-        }, "launch");
+        }, what);  // profile tag: the launch kind
     }
 
     void before_host_read_of(int64_t block_id) {
