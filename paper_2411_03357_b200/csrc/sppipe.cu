@@ -1309,7 +1309,19 @@ class Plane {
         }
         return true;
     }
-    static constexpr uint64_t kSlabBytes = 32ull << 20, kSlabMax = 1ull << 20;
+    // Sub-buffers up to slab_max() come from slabs.  The cap sits above 1 MiB
+    // + tags so a 1 MiB chunk's staging / ciphertext buffer (1 MiB + 16 B)
+    // is bump-allocated too: at 1 MiB it used to take a 2 MiB pool-size
+    // class, a pool allocation, a fence and a stream-ordered free per chunk.
+    // SPPIPE_SLAB_MAX_KIB overrides (A/B).
+    static constexpr uint64_t kSlabBytes = 32ull << 20;
+    static uint64_t slab_max() {
+        static const uint64_t v = [] {
+            const char *e = getenv("SPPIPE_SLAB_MAX_KIB");
+            return e ? (uint64_t)atoll(e) << 10 : (uint64_t)((1u << 20) + (64u << 10));
+        }();
+        return v;
+    }
     static bool slabs_enabled() {  // SPPIPE_SLAB=0: every buffer from the pool / cache
         static const bool on = [] {
             const char *e = getenv("SPPIPE_SLAB");
@@ -1332,7 +1344,7 @@ class Plane {
     }
     // lane separates lifetimes: 0 = transient staging, 1 = device copies of blocks
     BufP alloc(uint64_t n, cudaStream_t st, int lane = 0) {
-        if (!dry && n <= kSlabMax && slabs_enabled()) {
+        if (!dry && n <= slab_max() && slabs_enabled()) {
             auto &sl = open_slab(st, lane);
             const uint64_t need = (std::max<uint64_t>(n, 16) + 255u) & ~uint64_t(255);
             if (!sl || sl->off + need > sl->big->size) {

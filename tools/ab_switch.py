@@ -14,7 +14,7 @@ from paper_2411_03357_b200.replay import ReplayConfig, prepare_memory, run_engin
 
 sizes = ([int(x) for x in sys.argv[1].split(",") if x and x != "none"] if len(sys.argv) > 1
          else [64, 1024, 32768, 262144])
-env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("SPPIPE_", "SPGCM_"))) or "default"
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("SPPIPE_", "SPGCM_", "AB_CRYPTO"))) or "default"
 reps = int(os.environ.get("AB_REPS", "2"))
 
 
@@ -23,6 +23,8 @@ def best(fn):
 
 
 def arms(tr, base):
+    if os.environ.get("AB_CRYPTO_SMS"):  # SM budget of the crypto launches (ReplayConfig.crypto_sms)
+        base = replace(base, crypto_sms=int(os.environ["AB_CRYPTO_SMS"]))
     out = {}
     for comp in (False, True):
         c = replace(base, compute=comp)
