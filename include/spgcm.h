@@ -102,6 +102,18 @@ int sp_open_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
  * pipe in mapped pinned memory and reads it at finish). */
 #define SP_STATUS_ON_FAILURE 0x100u
 int sp_crypt_batch(sp_ctx *ctx, const sp_desc *descs, int n, sp_stream_t stream);
+/* Dependent levels of one flush in ONE launch: descs grouped by level,
+ * level l = descs[level_start[l] .. level_start[l+1]), level_start[0] = 0,
+ * level_start[nlevels] = n.  A message of level l may read what level l-1
+ * wrote (a receiver open of a ciphertext sealed in the same flush): the
+ * kernel's warps claim work in level order and level l starts when level
+ * l-1 is complete, so the result equals nlevels sp_crypt_batch calls in
+ * stream order (what the reference's per-send drain does one message at a
+ * time, engine.py:291 and engine.py:579-581) without a launch boundary per
+ * level.  Up to 8 levels and 256 messages fuse; larger calls run one launch
+ * per level.  Stream-ordered. */
+int sp_crypt_levels(sp_ctx *ctx, const sp_desc *descs, int n, const int *level_start, int nlevels,
+                    sp_stream_t stream);
 
 /* Host-buffer entry points: the exact call shape of encrypt_at / decrypt_at
  * (bytes in, bytes out).  H2D copies, kernels and D2H copies are pipelined

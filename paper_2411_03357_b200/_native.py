@@ -22,7 +22,7 @@ SPGCM_SYMBOLS = (
     "sp_ctx_create", "sp_ctx_destroy", "sp_seal", "sp_open", "sp_seal_batch", "sp_open_batch",
     "sp_crypt_batch", "sp_seal_host", "sp_open_host", "sp_seal_host_batch", "sp_open_host_batch",
     "sp_last_error", "sp_version", "sp_launch_count", "sp_ctx_round_keys", "sp_ctx_hash_key",
-    "sp_ctx_set_max_sms", "sp_ctx_max_sms",
+    "sp_ctx_set_max_sms", "sp_ctx_max_sms", "sp_crypt_levels",
 )
 
 
@@ -67,6 +67,8 @@ def load_spgcm() -> ctypes.CDLL:
         lib.sp_open.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, vp, ctypes.c_size_t, vp, vp, vp, vp]
         for name in ("sp_seal_batch", "sp_open_batch", "sp_crypt_batch"):
             getattr(lib, name).argtypes = [vp, ctypes.POINTER(SpDesc), ctypes.c_int, vp]
+        lib.sp_crypt_levels.argtypes = [vp, ctypes.POINTER(SpDesc), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                        ctypes.c_int, vp]
         for name in ("sp_seal_host_batch", "sp_open_host_batch"):
             getattr(lib, name).argtypes = [vp, ctypes.POINTER(SpDesc), ctypes.c_int]
         lib.sp_seal_host.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint64, vp, ctypes.c_size_t, vp, u8p]

@@ -93,8 +93,10 @@ __device__ __forceinline__ uint4 len_block(uint64_t len) {
 
 // Tag finalisation for one message; T = GHASH xor E_K(J0) (the warp that
 // covered the message's first row folded E_K(J0) in).  Warp-uniform.
+template <bool COH>
 __device__ __forceinline__ uint4 load_tag(const uint8_t *t) {
-    return (reinterpret_cast<uintptr_t>(t) & 15u) == 0 ? __ldg(reinterpret_cast<const uint4 *>(t)) : load_bytes(t, 16);
+    if ((reinterpret_cast<uintptr_t>(t) & 15u) != 0) return load_bytes(t, 16);
+    return COH ? __ldcg(reinterpret_cast<const uint4 *>(t)) : __ldg(reinterpret_cast<const uint4 *>(t));
 }
 
 // want: the expected tag, already loaded by lane 0 (have_want) or loaded here.
@@ -110,7 +112,7 @@ __device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int 
     }
     uint32_t bad = 0;
     if (lane == 0) {
-        if (!have_want) want = load_tag(md.tag);
+        if (!have_want) want = load_tag<true>(md.tag);  // after the message's rows: coherent
         bad = (want.x ^ tag.x) | (want.y ^ tag.y) | (want.z ^ tag.z) | (want.w ^ tag.w);
         if (md.status && (bad || !(md.dir & kStickyBit))) *md.status = bad ? 1 : 0;
     }
@@ -129,44 +131,32 @@ __device__ __forceinline__ void finish_message(const MsgDev &md, uint4 tag, int 
     }
 }
 
-template <uint32_t INL, class TB>
-__global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSmall ? 4 : 1)
-    k_gcm(const __grid_constant__ KParamsT<INL> p) {
-    extern __shared__ __align__(16) uint8_t sm[];
-    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
-    // let a dependent launch on this stream be scheduled now: its CTAs take
-    // idle SMs and fill their tables while this grid runs (they read no data
-    // before their own griddepcontrol.wait, which waits for this grid to end)
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (TB::kSmall) fill_tables_small(sm, p);
-    else fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
-    __syncthreads();
-    // programmatic dependent launch: everything below may read what the
-    // previous kernel on this stream wrote (messages, accumulators)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-
-    const int lane = threadIdx.x & 31;
-    const uint32_t lct = (uint32_t)lane * 4u;                  // T tables
-    const uint32_t lcm = (uint32_t)(lane & 7) * 16u;           // M_G copies
-    const uint32_t lcr = 128u + (uint32_t)lane * 4u;           // R8 copies
-
-    // contiguous, balanced row range for this warp
-    const uint64_t total = p.row_end - p.row_begin;
-    const uint32_t warp = threadIdx.x >> 5;
-    if (warp >= p.warps_used) return;
-    const uint64_t gw = (uint64_t)blockIdx.x * p.warps_used + warp;
-    const uint64_t nw = (uint64_t)gridDim.x * p.warps_used;
-    uint64_t g, g_end;
-    if (total * nw <= 0xffffffffull) {  // 32-bit division (the common case; 64-bit is a long software routine)
-        const uint32_t t32 = (uint32_t)total, w32 = (uint32_t)gw, n32 = (uint32_t)nw;
-        g = p.row_begin + (t32 * w32) / n32;
-        g_end = p.row_begin + (t32 * (w32 + 1u)) / n32;
+// Unit [k, k+1) of `n` equal shares of `total` rows starting at `base`.
+__device__ __forceinline__ void share_of(uint64_t base, uint64_t total, uint64_t k, uint64_t n, uint64_t &g,
+                                         uint64_t &g_end) {
+    if (total * n <= 0xffffffffull) {  // 32-bit division (the common case; 64-bit is a long software routine)
+        const uint32_t t32 = (uint32_t)total, k32 = (uint32_t)k, n32 = (uint32_t)n;
+        g = base + (t32 * k32) / n32;
+        g_end = base + (t32 * (k32 + 1u)) / n32;
     } else {
-        g = p.row_begin + (total * gw) / nw;
-        g_end = p.row_begin + (total * (gw + 1)) / nw;
+        g = base + (total * k) / n;
+        g_end = base + (total * (k + 1)) / n;
     }
-    if (g >= g_end) return;
+}
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Rows [g, g_end) of the flattened batch: keystream + XOR, GHASH, and the
+// tags of the messages whose last row this range completes.  COH: the
+// range may read what an earlier level of the same launch wrote, so no
+// read goes through the non-coherent (read-only) path.
+template <uint32_t INL, class TB, bool COH>
+__device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, const uint64_t g_end, const int lane,
+                                         const uint32_t lct, const uint32_t lcm, const uint32_t lcr) {
     const MsgDev *msgs = p.nmsgs <= INL ? p.inl : p.msgs;
     // first message containing row g (binary search on row_begin)
     uint32_t lo = 0, hi = p.nmsgs - 1;
@@ -194,7 +184,8 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
             if (i < 0) return make_uint4(0, 0, 0, 0);
             const int nb = (i == nblk - 1 && tail) ? tail : 16;
             const uint8_t *ptr = md.src + 16 * i;
-            if (vec && nb == 16) return __ldcs(reinterpret_cast<const uint4 *>(ptr));
+            if (vec && nb == 16)
+                return COH ? __ldcg(reinterpret_cast<const uint4 *>(ptr)) : __ldcs(reinterpret_cast<const uint4 *>(ptr));
             return load_bytes(ptr, nb);
         };
 
@@ -217,7 +208,7 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
         // the expected tag of an open whose last row this run covers: read
         // now, not after the epilogue
         const bool have_want = opening && t_b == md.rows && lane == 0;
-        const uint4 want = have_want ? load_tag(md.tag) : make_uint4(0, 0, 0, 0);
+        const uint4 want = have_want ? load_tag<COH>(md.tag) : make_uint4(0, 0, 0, 0);
         const uint4 lh_part = nt_part(p.nt + (size_t)kNtLane * kNtEntries, len_block(md.len), lane);  // L x H
         const CtrConst cc = ctr_const<TB>(p.rk, lct, x0, x1, x2);
         CtrCache ck;
@@ -296,6 +287,78 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
         }
         g = md.row_begin + t_b;
         ++m;
+    }
+}
+
+template <uint32_t INL, class TB, bool LV>
+__global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSmall ? 4 : 1)
+    k_gcm(const __grid_constant__ KParamsT<INL> p) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(sm)) != kSmBase) __trap();  // absolute lookups
+    // let a dependent launch on this stream be scheduled now: its CTAs take
+    // idle SMs and fill their tables while this grid runs (they read no data
+    // before their own griddepcontrol.wait, which waits for this grid to end)
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (TB::kSmall) fill_tables_small(sm, p);
+    else fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
+    __syncthreads();
+    // programmatic dependent launch: everything below may read what the
+    // previous kernel on this stream wrote (messages, accumulators)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    const int lane = threadIdx.x & 31;
+    const uint32_t lct = (uint32_t)lane * 4u;                  // T tables
+    const uint32_t lcm = (uint32_t)(lane & 7) * 16u;           // M_G copies
+    const uint32_t lcr = 128u + (uint32_t)lane * 4u;           // R8 copies
+
+    const uint32_t warp = threadIdx.x >> 5;
+    if (warp >= p.warps_used) return;
+    if (!LV) {
+        // contiguous, balanced row range for this warp
+        uint64_t g, g_end;
+        share_of(p.row_begin, p.row_end - p.row_begin, (uint64_t)blockIdx.x * p.warps_used + warp,
+                 (uint64_t)gridDim.x * p.warps_used, g, g_end);
+        if (g < g_end) gcm_rows<INL, TB, false>(p, g, g_end, lane, lct, lcm, lcr);
+        return;
+    }
+
+    // fused levels: claim units in order (see KParamsT)
+    uint32_t *ctl = p.ctl;
+    const uint32_t units = p.lvl_unit[p.nlevels];
+    for (;;) {
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(ctl, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= units) break;
+        uint32_t lv = 0;
+        while (u >= p.lvl_unit[lv + 1]) ++lv;
+        if (lv > 0) {
+            if (lane == 0) {
+                const uint32_t need = p.lvl_unit[lv] - p.lvl_unit[lv - 1];
+                uint32_t ns = 32, spins = 0;
+                while (ld_acquire_gpu(ctl + 2 + lv - 1) < need) {
+                    __nanosleep(ns);
+                    ns = ns < 512 ? ns * 2 : ns;
+                    if (++spins > (1u << 22)) __trap();  // a lost level (bug): fail loudly, never hang
+                }
+            }
+            __syncwarp();
+        }
+        const uint32_t k = u - p.lvl_unit[lv], n = p.lvl_unit[lv + 1] - p.lvl_unit[lv];
+        uint64_t g, g_end;
+        share_of(p.lvl_row[lv], p.lvl_row[lv + 1] - p.lvl_row[lv], k, n, g, g_end);
+        if (g < g_end) gcm_rows<INL, TB, true>(p, g, g_end, lane, lct, lcm, lcr);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctl + 2 + lv) : "memory");
+    }
+    if (lane == 0) {
+        const uint32_t e = atomicAdd(ctl + 1, 1u);
+        if (e == gridDim.x * p.warps_used - 1u) {  // every warp is past its last claim
+            ctl[0] = 0;
+            ctl[1] = 0;
+            for (uint32_t l = 0; l < p.nlevels; ++l) ctl[2 + l] = 0;
+        }
     }
 }
 
@@ -525,6 +588,7 @@ struct Workspace {
     size_t cap_msgs = 0;
     uint32_t *d_acc = nullptr;
     size_t cap_acc = 0;
+    uint32_t *d_ctl = nullptr;  // fused-level launches: claim / exit / per-level done counters
     std::vector<MsgDev> h_msgs;
     // pinned staging ring for descriptor arrays larger than kInline
     MsgDev *h_pin[kPinSlots] = {};
@@ -693,6 +757,10 @@ int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
         SP_CUDA(cudaMemsetAsync(ws->d_acc, 0, cap * 8 * sizeof(uint32_t), s), "cudaMemsetAsync(acc)");
         ws->cap_acc = cap;
     }
+    if (!ws->d_ctl) {
+        SP_CUDA(cudaMalloc(&ws->d_ctl, kCtlWords * sizeof(uint32_t)), "cudaMalloc(ctl)");
+        SP_CUDA(cudaMemsetAsync(ws->d_ctl, 0, kCtlWords * sizeof(uint32_t), s), "cudaMemsetAsync(ctl)");
+    }
     return SP_OK;
 }
 
@@ -726,9 +794,54 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     if (small)
-        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, SmallTabs>, p), "k_gcm launch");
+        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, SmallTabs, false>, p), "k_gcm launch");
     else
-        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, BigTabs>, p), "k_gcm launch");
+        SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, BigTabs, false>, p), "k_gcm launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SP_OK;
+}
+
+// One launch for `nlevels` dependent levels (p.lvl_row filled, rows grouped
+// by level).  Each level gets the units its own launch would have had
+// warps (the tiny-batch policy of launch_rows); the grid covers the
+// largest level in one wave and warps loop over claimed units.
+template <uint32_t INL>
+int launch_levels(const sp_ctx *ctx, KParamsT<INL> p, uint32_t nlevels, cudaStream_t s) {
+    const uint64_t sms = (uint64_t)ctx->sms();
+    int grid = 1;
+    uint32_t wu = 1;
+    p.nlevels = nlevels;
+    p.lvl_unit[0] = 0;
+    for (uint32_t l = 0; l < nlevels; ++l) {
+        const uint64_t rows = p.lvl_row[l + 1] - p.lvl_row[l];
+        const uint64_t rpw = rows <= tiny_rows_max() ? (rows <= 256 ? 1 : 2) : rows_per_warp();
+        const uint64_t want = std::max<uint64_t>(1, std::min<uint64_t>(std::max<uint64_t>(rows / rpw, 1),
+                                                                       sms * kWarpsPerCta));
+        int g = 1;
+        uint32_t w = 1;
+        launch_shape(ctx, rows, 1, g, w, rpw);
+        grid = std::max(grid, g);
+        wu = std::max(wu, w);
+        p.lvl_unit[l + 1] = p.lvl_unit[l] + (uint32_t)want;
+    }
+    p.warps_used = wu;
+    p.row_begin = p.lvl_row[0];
+    p.row_end = p.lvl_row[nlevels];
+    static const bool pdl = [] {
+        const char *e = getenv("SPGCM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    SP_CUDA(cudaLaunchKernelEx(&cfg, k_gcm<INL, BigTabs, true>, p), "k_gcm levels launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return SP_OK;
 }
@@ -748,6 +861,15 @@ bool inline_big_enabled() {
 bool tiny_params_enabled() {
     static const bool on = [] {
         const char *e = getenv("SPGCM_TINY_PARAMS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// SPGCM_FUSE_LEVELS=0: sp_crypt_levels issues one launch per level (A/B).
+bool fuse_levels_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("SPGCM_FUSE_LEVELS");
         return !(e && e[0] == '0');
     }();
     return on;
@@ -1118,12 +1240,18 @@ int sp_ctx_create(const uint8_t key[SP_KEY_BYTES], sp_ctx **out) {
     cudaDeviceProp prop;
     SP_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
     if (prop.major != 10) return fail(SP_ENODEV, "libspgcm is built for sm_100a (B200) only");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm)");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineTiny, BigTabs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineTiny, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm tiny)");
-    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm big)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm levels)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineTiny, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm tiny levels)");
+    SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm big levels)");
     sp_ctx *c = new sp_ctx();
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;
@@ -1196,6 +1324,58 @@ int sp_open_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
 
 int sp_crypt_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
     return run_batch(ctx, d, n, static_cast<cudaStream_t>(stream), 2);
+}
+
+int sp_crypt_levels(sp_ctx *ctx, const sp_desc *d, int n, const int *level_start, int nlevels,
+                    sp_stream_t stream) {
+    if (!ctx) return fail(SP_EINVAL, "null context");
+    if (nlevels < 1 || !level_start) return fail(SP_EINVAL, "need at least one level");
+    if (level_start[0] != 0 || level_start[nlevels] != n) return fail(SP_EINVAL, "levels must cover the batch");
+    for (int l = 0; l < nlevels; ++l)
+        if (level_start[l + 1] <= level_start[l]) return fail(SP_EINVAL, "empty level");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nlevels == 1) return run_batch(ctx, d, n, s, 2);
+    if ((uint32_t)nlevels > kMaxLevels || (uint32_t)n > kInlineBig || !fuse_levels_enabled()) {
+        for (int l = 0; l < nlevels; ++l) {  // one launch per level, in stream order
+            const int rc = run_batch(ctx, d + level_start[l], level_start[l + 1] - level_start[l], s, 2);
+            if (rc) return rc;
+        }
+        return SP_OK;
+    }
+    SP_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    Workspace *ws = workspace_for(ctx->device, s);
+    std::lock_guard<std::mutex> lk(ws->mu);
+    KParams p;
+    static thread_local KParamsBig big;
+    bool use_big = false;
+    uint64_t rows = 0;
+    int rc = stage_batch(ctx, d, n, s, ws, p, rows, 2, &big, &use_big);
+    if (rc) return rc;
+    auto fill = [&](auto &q) {
+        q.ctl = ws->d_ctl;
+        for (int l = 0; l < nlevels; ++l) q.lvl_row[l] = ws->h_msgs[(size_t)level_start[l]].row_begin;
+        q.lvl_row[nlevels] = rows;
+    };
+    if (use_big) {
+        fill(big);
+        return launch_levels(ctx, big, (uint32_t)nlevels, s);
+    }
+    if ((uint32_t)n <= kInlineTiny && tiny_params_enabled()) {
+        KParamsTiny t;
+        memset(&t, 0, sizeof(t));
+        memcpy(t.inl, p.inl, (size_t)n * sizeof(MsgDev));
+        memcpy(t.rk, p.rk, sizeof(t.rk));
+        t.ttab = p.ttab;
+        t.mg = p.mg;
+        t.nt = p.nt;
+        t.msgs = p.msgs;
+        t.acc = p.acc;
+        t.nmsgs = p.nmsgs;
+        fill(t);
+        return launch_levels(ctx, t, (uint32_t)nlevels, s);
+    }
+    fill(p);
+    return launch_levels(ctx, p, (uint32_t)nlevels, s);
 }
 
 int sp_seal(sp_ctx *ctx, uint32_t dir, uint64_t iv, const void *src, size_t len, void *dst, void *tag16,

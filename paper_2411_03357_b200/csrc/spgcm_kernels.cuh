@@ -76,6 +76,16 @@ constexpr uint32_t kOpenBit = 0x100u;
 // MsgDev.dir: this bit = write *status only on failure (SP_STATUS_ON_FAILURE)
 constexpr uint32_t kStickyBit = 0x200u;
 
+// Fused levels (sp_crypt_levels): up to kMaxLevels dependent batches in ONE
+// launch.  Level L's rows split into lvl_unit[L+1]-lvl_unit[L] units; warps
+// claim units in global order from ctl[0], and a unit of level L > 0 starts
+// once every unit of level L-1 is done (ctl[2+L-1]).  Claiming in order makes
+// it deadlock-free without co-residency: every unit a waiter depends on was
+// claimed earlier by a warp that is already running.  The last warp to exit
+// (ctl[1]) resets the counters for the next launch on the stream.
+constexpr uint32_t kMaxLevels = 8;
+constexpr uint32_t kCtlWords = 2 + kMaxLevels;
+
 template <uint32_t INL>
 struct KParamsT {
     MsgDev inl[INL];
@@ -90,6 +100,10 @@ struct KParamsT {
     uint32_t nmsgs;
     uint32_t reserved;
     uint32_t warps_used;   // warps per CTA that own rows (<= kWarpsPerCta)
+    uint32_t nlevels;      // fused launches only (k_gcm<.., true>)
+    uint32_t lvl_unit[kMaxLevels + 1];
+    uint64_t lvl_row[kMaxLevels + 1];
+    uint32_t *ctl;         // claim, exit, done[kMaxLevels]
 };
 using KParams = KParamsT<kInline>;
 using KParamsTiny = KParamsT<kInlineTiny>;

@@ -1666,6 +1666,30 @@ class Plane {
                 }
             }
             auto &descs = descs_scratch;
+            if (top >= 1 && top < (int)kFuseLevels && q.size() <= kLaunchMsgs) {
+                // the flush's dependent levels in ONE launch (sp_crypt_levels):
+                // level l starts inside the kernel once level l-1 is done, no
+                // launch boundary per level.  Every op's input fence is waited
+                // for up front.
+                descs.clear();
+                std::vector<int> starts;
+                starts.reserve((size_t)top + 2);
+                for (int lv = 0; lv <= top; ++lv) {
+                    starts.push_back((int)descs.size());
+                    for (uint32_t k = level_start[(size_t)lv]; k < level_start[(size_t)lv + 1]; ++k) {
+                        const Op &op = q[by_level[k]];
+                        if (op.wait && op.wait->mark != mk) {
+                            wait(cs, op.wait);
+                            op.wait->mark = mk;
+                        }
+                        descs.push_back(op.d);
+                    }
+                }
+                starts.push_back((int)descs.size());
+                post_levels(descs, std::move(starts), cs);
+                ++launches;
+                top = -1;  // nothing left for the per-level loop below
+            }
             for (int lv = 0; lv <= top; ++lv) {
                 descs.clear();
                 for (uint32_t k = level_start[(size_t)lv]; k < level_start[(size_t)lv + 1]; ++k) {
@@ -2027,6 +2051,15 @@ class Plane {
                 ck_sp(rc, what);
             }
         }, what);  // profile tag: the launch kind
+    }
+
+    static constexpr size_t kFuseLevels = 8;
+    void post_levels(const std::vector<sp_desc> &d, std::vector<int> starts, cudaStream_t st) {
+        sp_ctx *c = ctx;
+        iss.post([c, st, d = std::vector<sp_desc>(d), starts = std::move(starts)] {
+            ck_sp(sp_crypt_levels(c, d.data(), (int)d.size(), starts.data(), (int)starts.size() - 1, st),
+                  "sp_crypt_levels");
+        }, "sp_crypt_levels");
     }
 
     void before_host_read_of(int64_t block_id) {

@@ -432,3 +432,76 @@ def test_status_on_failure_shared_word(ctx_for, torch_cuda, tamper):
     for i in range(n):
         want = bytes(sizes[i]) if i == tamper else plains[i]
         assert _host(dsts[i]) == want, i
+
+
+@pytest.mark.parametrize("per_level,nlevels,reps", [(1, 2, 40), (3, 4, 20), (60, 4, 3), (2, 8, 10)])
+def test_fused_levels_chain(ctx_for, torch_cuda, per_level, nlevels, reps):
+    """sp_crypt_levels: a chain of dependent levels in ONE launch — level 0
+    seals plaintexts, every odd level opens what the level before sealed,
+    every later even level re-seals that plaintext at a new counter (the
+    flush shape of a KV swap-in: stage seal -> receiver open).  Every seal
+    matches the oracle bit for bit, every open returns the plaintext, an
+    open at the wrong counter fails and is zeroed; repeated launches on one
+    stream reuse the in-kernel level counters."""
+    import ctypes
+
+    from paper_2411_03357_b200 import _native
+
+    torch = torch_cuda
+    rng = random.Random(per_level * 100 + nlevels)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    lib = _native.load_spgcm()
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    sizes = [rng.choice([1, 17, 2048, 229_376, rng.randrange(1, MIB)]) for _ in range(per_level)]
+    plains = [rng.randbytes(s) for s in sizes]
+    n = per_level * nlevels
+    bufs = [[_dev(torch, p)] for p in plains]  # bufs[i][l] = output of level l-1 for chain i
+    for i in range(per_level):
+        for _ in range(nlevels):
+            bufs[i].append(torch.full_like(bufs[i][0], 0xAB))
+    tags = torch.zeros((nlevels, per_level, 16), dtype=torch.uint8, device="cuda")
+    status = torch.full((n,), 7, dtype=torch.int32, device="cuda")
+    iv_of = lambda lv, i: 1000 * (lv // 2) + i  # noqa: E731  (seal lv and its open lv+1 share it)
+    bad = (nlevels - 1, per_level - 1) if nlevels % 2 == 0 else None  # last open at a wrong counter
+    descs = (_native.SpDesc * n)()
+    for lv in range(nlevels):
+        for i in range(per_level):
+            d = descs[lv * per_level + i]
+            opening = lv % 2 == 1
+            iv = iv_of(lv, i) + (1 if (lv, i) == bad else 0)
+            d.dir, d.reserved, d.iv, d.len = (lv // 2) & 1, int(opening), iv, sizes[i]
+            d.src, d.dst = bufs[i][lv].data_ptr(), bufs[i][lv + 1].data_ptr()
+            d.tag = tags[lv - 1 if opening else lv, i].data_ptr()
+            d.status = status.data_ptr() + 4 * (lv * per_level + i)
+    starts = (ctypes.c_int * (nlevels + 1))(*[lv * per_level for lv in range(nlevels + 1)])
+    before = _native.launch_count()
+    for _ in range(reps):
+        rc = lib.sp_crypt_levels(ctx._h, descs, n, starts, nlevels, stream)
+        assert rc == 0, _native.last_error()
+    torch.cuda.synchronize()
+    assert _native.launch_count() - before == reps  # one launch per call
+    st = status.cpu().tolist()
+    for lv in range(nlevels):
+        for i in range(per_level):
+            out = _host(bufs[i][lv + 1])
+            if lv % 2 == 0:
+                want = oracle_port.seal(key, (lv // 2) & 1, iv_of(lv, i), plains[i])
+                assert (out, _host(tags[lv, i])) == want, (lv, i)
+            elif (lv, i) == bad:
+                assert st[lv * per_level + i] == 1 and out == bytes(sizes[i])
+            else:
+                assert st[lv * per_level + i] == 0 and out == plains[i], (lv, i)
+
+
+def test_fused_levels_rejects_bad_layout(ctx_for, torch_cuda):
+    import ctypes
+
+    from paper_2411_03357_b200 import _native
+
+    lib = _native.load_spgcm()
+    ctx = ctx_for(bytes(32))
+    descs = (_native.SpDesc * 2)()
+    for starts in ([0, 0, 2], [1, 2], [0, 1]):
+        arr = (ctypes.c_int * len(starts))(*starts)
+        assert lib.sp_crypt_levels(ctx._h, descs, 2, arr, len(starts) - 1, None) == _native.SP_EINVAL
