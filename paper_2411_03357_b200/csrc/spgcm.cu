@@ -243,8 +243,44 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
         // lane-table loads are in flight while the warp covering the
         // message's first row computes E_K(J0) (folded into W: XOR is
         // order-free, so the finisher needs no AES of its own).
-        const uint4 lanes_w =
-            nt_mul_lane(p.nt + (size_t)(kNtLane + (r_end ? 31u : 32u) - (uint32_t)lane) * kNtEntries, y);
+        uint4 lanes_w;
+        if (!TB::kSmall && (p.reserved & kTreeBit)) {
+            // binary tree over lanes in shared memory: level k folds pairs
+            // 2^k apart as left x H^(2^k) + right, so lane 0 ends with
+            // D0 = sum_{l<16} Y_l H^(15-l) and lane 16 with D1 (lanes 16..31);
+            // then W = D0 H^(17|18) + D1 H^(1|2), lane-parallel (two HBM
+            // nibble loads per lane): 128 global loads per warp instead of
+            // 1,024 (the L2 request rate bounded launches of many warps).
+            uint4 v = y;
+#define SP_TREE_LEVEL(K)                                                         \
+    {                                                                            \
+        uint4 r;                                                                 \
+        r.x = __shfl_down_sync(0xffffffffu, v.x, 1 << K);                        \
+        r.y = __shfl_down_sync(0xffffffffu, v.y, 1 << K);                        \
+        r.z = __shfl_down_sync(0xffffffffu, v.z, 1 << K);                        \
+        r.w = __shfl_down_sync(0xffffffffu, v.w, 1 << K);                        \
+        if ((lane & ((2 << K) - 1)) == 0) v = xor4(tree_mul<K>(v), r);           \
+    }
+            SP_TREE_LEVEL(0)
+            SP_TREE_LEVEL(1)
+            SP_TREE_LEVEL(2)
+            SP_TREE_LEVEL(3)
+#undef SP_TREE_LEVEL
+            uint4 d0, d1;
+            d0.x = __shfl_sync(0xffffffffu, v.x, 0);
+            d0.y = __shfl_sync(0xffffffffu, v.y, 0);
+            d0.z = __shfl_sync(0xffffffffu, v.z, 0);
+            d0.w = __shfl_sync(0xffffffffu, v.w, 0);
+            d1.x = __shfl_sync(0xffffffffu, v.x, 16);
+            d1.y = __shfl_sync(0xffffffffu, v.y, 16);
+            d1.z = __shfl_sync(0xffffffffu, v.z, 16);
+            d1.w = __shfl_sync(0xffffffffu, v.w, 16);
+            const uint32_t e = r_end ? 0u : 1u;  // H^(1+e) at kNtLane + e
+            lanes_w = xor4(nt_part(p.nt + (size_t)(kNtLane + 16u + e) * kNtEntries, d0, lane),
+                           nt_part(p.nt + (size_t)(kNtLane + e) * kNtEntries, d1, lane));
+        } else {
+            lanes_w = nt_mul_lane(p.nt + (size_t)(kNtLane + (r_end ? 31u : 32u) - (uint32_t)lane) * kNtEntries, y);
+        }
         uint4 ek = make_uint4(0, 0, 0, 0);
         if (t_a == 0 && lane == 0) ek = aes256_rounds<TB>(p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
         uint4 w = warp_xor(lanes_w);
@@ -301,6 +337,18 @@ __global__ void __launch_bounds__(TB::kSmall ? kThreadsSmall : kThreads, TB::kSm
     asm volatile("griddepcontrol.launch_dependents;");
     if (TB::kSmall) fill_tables_small(sm, p);
     else fill_tables(sm, p);  // per-key constants only: may overlap the previous launch (PDL)
+    if (!TB::kSmall && (p.reserved & kTreeBit)) {
+        // tree tables: H^(2^k) = HBM nibble table kNtLane + 2^k - 1, k = 0..3
+        uint4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t f = threadIdx.x + (uint32_t)j * kThreads, k = f >> 9;
+            v[j] = __ldg(p.nt + (size_t)(kNtLane + (1u << k) - 1u) * kNtEntries + (f & 511u));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            reinterpret_cast<uint4 *>(sm + kSmTree)[threadIdx.x + (uint32_t)j * kThreads] = v[j];
+    }
     __syncthreads();
     // programmatic dependent launch: everything below may read what the
     // previous kernel on this stream wrote (messages, accumulators)
@@ -764,6 +812,20 @@ int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
     return SP_OK;
 }
 
+// Lane combine of a BigTabs launch: with many working warps the 1,024
+// nibble-table loads per warp of nt_mul_lane bound the launch on L2
+// requests; the shared-memory tree (kTreeBit) replaces them with 32 KiB of
+// tables per CTA and 128 loads per warp, at ~0.3-0.5 us more latency per
+// warp (four dependent levels, 32 KiB more fill).  Graph-replayed device
+// time per launch, tree vs nibble tables (profiles/r2_tree_small.txt):
+// 32 x 224 KiB 26.7 vs 32.2 us, 4 x 224 KiB 10.5 vs 11.2, 1 MiB 10.3 vs
+// 10.8; 1 x 224 KiB (224 warps) 7.9 vs 7.6, NOP 5.4 vs 4.9.  So from 256
+// working warps on; SPGCM_TREE_WARPS overrides (0: always, huge: never).
+bool use_tree(uint64_t warps) {
+    static const uint64_t v = env_u64("SPGCM_TREE_WARPS", 256);
+    return warps >= v;
+}
+
 template <uint32_t INL>
 int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t row_end, cudaStream_t s) {
     if (row_end <= row_begin) return SP_OK;
@@ -783,10 +845,12 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
         const char *e = getenv("SPGCM_PDL");
         return !(e && e[0] == '0');
     }();
+    const bool tree = !small && use_tree((uint64_t)grid * p.warps_used);
+    if (tree) p.reserved |= kTreeBit;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(small ? kThreadsSmall : kThreads);
-    cfg.dynamicSmemBytes = small ? kSmallSmem : kSmemBytes;
+    cfg.dynamicSmemBytes = small ? kSmallSmem : (tree ? kSmemBytesTree : kSmemBytes);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -831,10 +895,12 @@ int launch_levels(const sp_ctx *ctx, KParamsT<INL> p, uint32_t nlevels, cudaStre
         const char *e = getenv("SPGCM_PDL");
         return !(e && e[0] == '0');
     }();
+    const bool tree = use_tree((uint64_t)grid * wu);
+    if (tree) p.reserved |= kTreeBit;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = tree ? kSmemBytesTree : kSmemBytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1241,17 +1307,17 @@ int sp_ctx_create(const uint8_t key[SP_KEY_BYTES], sp_ctx **out) {
     SP_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
     if (prop.major != 10) return fail(SP_ENODEV, "libspgcm is built for sm_100a (B200) only");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm)");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineTiny, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm tiny)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm tiny)");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm big)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm big)");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInline, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm levels)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm levels)");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineTiny, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm tiny levels)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm tiny levels)");
     SP_CUDA(cudaFuncSetAttribute(k_gcm<kInlineBig, BigTabs, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes), "cudaFuncSetAttribute(k_gcm big levels)");
+                                 (int)kSmemBytesTree), "cudaFuncSetAttribute(k_gcm big levels)");
     sp_ctx *c = new sp_ctx();
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;

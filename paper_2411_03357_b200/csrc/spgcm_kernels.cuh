@@ -46,6 +46,12 @@ constexpr uint32_t kSmAes0 = 0;
 constexpr uint32_t kSmAes1 = 65536;
 constexpr uint32_t kSmGh = 131072;
 constexpr uint32_t kSmemBytes = 196608;
+// Lane-combine tree (KParamsT.reserved & kTreeBit): nibble tables of H^1,
+// H^2, H^4, H^8 (8 KiB each, same layout as the HBM nibble tables) after
+// the BigTabs tables.
+constexpr uint32_t kSmTree = 196608;
+constexpr uint32_t kSmemBytesTree = kSmemBytes + 4u * 8192u;  // 224 KiB (of 227)
+constexpr uint32_t kTreeBit = 1u;
 
 struct MsgDev {
     const uint8_t *src;
@@ -334,6 +340,21 @@ __device__ __forceinline__ uint4 nt_mul_lane(const uint4 *tab, uint4 v) {
     uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int q = 0; q < 32; ++q) acc = xor4(acc, __ldg(tab + q * 16 + nibble_of(v, q)));
+    return acc;
+}
+
+// v x H^(2^K) with the shared-memory nibble table K of the tree: 32
+// independent LDS.128, no global traffic.
+template <int K>
+__device__ __forceinline__ uint4 tree_mul(uint4 v) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        const uint32_t w = word_of(v, q >> 3);
+        const int sh = 8 * ((q >> 1) & 3) - ((q & 1) ? 4 : 0);  // nibble q of the string, times 16
+        const uint32_t off = (sh >= 0 ? (w >> sh) : (w << (-sh))) & 0xf0u;
+        acc = xor4(acc, lds128_at<kSmTree + (uint32_t)K * 8192u>(off + (uint32_t)q * 256u));
+    }
     return acc;
 }
 
