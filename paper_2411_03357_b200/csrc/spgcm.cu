@@ -820,10 +820,12 @@ int ensure_ws(Workspace *ws, size_t nmsgs, cudaStream_t s) {
 // time per launch, tree vs nibble tables (profiles/r2_tree_small.txt):
 // 32 x 224 KiB 26.7 vs 32.2 us, 4 x 224 KiB 10.5 vs 11.2, 1 MiB 10.3 vs
 // 10.8; 1 x 224 KiB (224 warps) 7.9 vs 7.6, NOP 5.4 vs 4.9.  So from 256
-// working warps on; SPGCM_TREE_WARPS overrides (0: always, huge: never).
-bool use_tree(uint64_t warps) {
+// working warps on, for launches of short runs (<= 16 rows per warp: a big
+// batch combines once per ~500 rows and keeps 192 KiB of shared memory);
+// SPGCM_TREE_WARPS overrides the warp count (0: always, huge: never).
+bool use_tree(uint64_t warps, uint64_t rows) {
     static const uint64_t v = env_u64("SPGCM_TREE_WARPS", 256);
-    return warps >= v;
+    return warps >= v && (v == 0 || rows <= 16 * warps);
 }
 
 template <uint32_t INL>
@@ -845,7 +847,7 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
         const char *e = getenv("SPGCM_PDL");
         return !(e && e[0] == '0');
     }();
-    const bool tree = !small && use_tree((uint64_t)grid * p.warps_used);
+    const bool tree = !small && use_tree((uint64_t)grid * p.warps_used, rows);
     if (tree) p.reserved |= kTreeBit;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -895,7 +897,7 @@ int launch_levels(const sp_ctx *ctx, KParamsT<INL> p, uint32_t nlevels, cudaStre
         const char *e = getenv("SPGCM_PDL");
         return !(e && e[0] == '0');
     }();
-    const bool tree = use_tree((uint64_t)grid * wu);
+    const bool tree = use_tree((uint64_t)grid * wu, p.lvl_row[nlevels] - p.lvl_row[0]);
     if (tree) p.reserved |= kTreeBit;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
