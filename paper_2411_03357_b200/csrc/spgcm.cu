@@ -194,7 +194,18 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
         // epilogue's dependent DRAM round trips with the row loop.  A run
         // that ends at its message's end (r_end = 0) needs neither.
         const uint32_t r_end = md.rows - (uint32_t)t_b;
-        if (r_end) {
+        const bool tree = !TB::kSmall && (p.reserved & kTreeBit);
+        const bool short_tail = r_end < kNumG;
+        if (r_end && short_tail) {
+            const char *gt = reinterpret_cast<const char *>(p.nt + (size_t)(kNtG1 + r_end) * kNtEntries + lane * 16);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gt));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gt + 128));
+            if (tree) {
+                const char *g17 = reinterpret_cast<const char *>(p.nt + (size_t)(kNtG17 + r_end) * kNtEntries + lane * 16);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(g17));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(g17 + 128));
+            }
+        } else if (r_end) {
             const char *ft = reinterpret_cast<const char *>(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries + lane * 16);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ft));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(ft + 128));
@@ -244,7 +255,8 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
         // message's first row computes E_K(J0) (folded into W: XOR is
         // order-free, so the finisher needs no AES of its own).
         uint4 lanes_w;
-        if (!TB::kSmall && (p.reserved & kTreeBit)) {
+        bool scaled = r_end == 0;  // W already carries H^(32 r_end + 1)
+        if (tree) {
             // binary tree over lanes in shared memory: level k folds pairs
             // 2^k apart as left x H^(2^k) + right, so lane 0 ends with
             // D0 = sum_{l<16} Y_l H^(15-l) and lane 16 with D1 (lanes 16..31);
@@ -275,19 +287,34 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
             d1.y = __shfl_sync(0xffffffffu, v.y, 16);
             d1.z = __shfl_sync(0xffffffffu, v.z, 16);
             d1.w = __shfl_sync(0xffffffffu, v.w, 16);
-            const uint32_t e = r_end ? 0u : 1u;  // H^(1+e) at kNtLane + e
-            lanes_w = xor4(nt_part(p.nt + (size_t)(kNtLane + 16u + e) * kNtEntries, d0, lane),
-                           nt_part(p.nt + (size_t)(kNtLane + e) * kNtEntries, d1, lane));
+            uint32_t t0, t1;  // tables scaling D0 and D1
+            if (r_end == 0) {
+                t0 = kNtLane + 17u;  // H^18
+                t1 = kNtLane + 1u;   // H^2
+            } else if (short_tail) {
+                t0 = kNtG17 + r_end;  // H^(32 r_end + 17)
+                t1 = kNtG1 + r_end;   // H^(32 r_end + 1)
+                scaled = true;
+            } else {
+                t0 = kNtLane + 16u;  // H^17
+                t1 = kNtLane;        // H^1
+            }
+            lanes_w = xor4(nt_part(p.nt + (size_t)t0 * kNtEntries, d0, lane),
+                           nt_part(p.nt + (size_t)t1 * kNtEntries, d1, lane));
         } else {
             lanes_w = nt_mul_lane(p.nt + (size_t)(kNtLane + (r_end ? 31u : 32u) - (uint32_t)lane) * kNtEntries, y);
         }
         uint4 ek = make_uint4(0, 0, 0, 0);
         if (t_a == 0 && lane == 0) ek = aes256_rounds<TB>(p.rk, lct, x0, x1, x2, bswap32(1u) ^ p.rk[3]);
         uint4 w = warp_xor(lanes_w);
-        if (r_end) {  // scale by H^(32 r_end + 1) = F[r_end / 16] x H^(32 (r_end mod 16))
-            w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
-            if (r_end & 15u)
-                w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+        if (!scaled) {  // scale by H^(32 r_end + 1)
+            if (short_tail) {
+                w = warp_xor(nt_part(p.nt + (size_t)(kNtG1 + r_end) * kNtEntries, w, lane));
+            } else {  // = F[r_end / 16] x H^(32 (r_end mod 16))
+                w = warp_xor(nt_part(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries, w, lane));
+                if (r_end & 15u)
+                    w = warp_xor(nt_part(p.nt + (size_t)(kNtP32 + (r_end & 15u) - 1u) * kNtEntries, w, lane));
+            }
         }
         if (t_a == 0) {
             ek.x = __shfl_sync(0xffffffffu, ek.x, 0);
@@ -503,7 +530,9 @@ __global__ void k_setup_powers(const uint4 *hptr, uint4 *powers) {
     uint64_t e;
     if (idx < kNtF) e = idx + 1;                                   // H^1..H^33
     else if (idx < kNtP32) e = 512ull * (idx - kNtF) + 1;          // F_a
-    else if (idx < kNumNt) e = 32ull * (idx - kNtP32 + 1);         // H^(32b)
+    else if (idx < kNtG1) e = 32ull * (idx - kNtP32 + 1);          // H^(32b)
+    else if (idx < kNtG17) e = 32ull * (idx - kNtG1) + 1;          // short tails
+    else if (idx < kNumNt) e = 32ull * (idx - kNtG17) + 17;
     else e = 32;                                                    // G
     powers[idx] = g_to_words(g_pow(h, e));
 }

@@ -39,7 +39,13 @@ constexpr uint32_t kNumF = (kMaxRows + 15) / 16;                     // 4096
 constexpr uint32_t kNtLane = 0;          // H^e, e = 1..33 -> index e-1 (H^(33-l): runs ending at their message's end)
 constexpr uint32_t kNtF = 33;            // F_a = H^(512a+1), a < kNumF
 constexpr uint32_t kNtP32 = kNtF + kNumF;  // H^(32b), b = 1..15 -> kNtP32 + b - 1
-constexpr uint32_t kNumNt = kNtP32 + 15;
+// Short tails: a run ending r_end < kNumG rows before its message's end
+// scales by H^(32 r_end + 1) in ONE lookup (instead of F then H^(32b)), and
+// the tree's last step folds that scaling in: D0 x H^(32 r_end + 17).
+constexpr uint32_t kNumG = 512;
+constexpr uint32_t kNtG1 = kNtP32 + 15;        // H^(32r + 1),  r < kNumG
+constexpr uint32_t kNtG17 = kNtG1 + kNumG;     // H^(32r + 17), r < kNumG
+constexpr uint32_t kNumNt = kNtG17 + kNumG;
 constexpr uint32_t kNtEntries = 32 * 16;
 
 constexpr uint32_t kSmAes0 = 0;
