@@ -197,13 +197,13 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
         const bool tree = !TB::kSmall && (p.reserved & kTreeBit);
         const bool short_tail = r_end < kNumG;
         if (r_end && short_tail) {
-            const char *gt = reinterpret_cast<const char *>(p.nt + (size_t)(kNtG1 + r_end) * kNtEntries + lane * 16);
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(gt));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(gt + 128));
+            const char *ga = reinterpret_cast<const char *>(p.nt + (size_t)((tree ? kNtG2 : kNtG1) + r_end) * kNtEntries + lane * 16);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ga));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ga + 128));
             if (tree) {
-                const char *g17 = reinterpret_cast<const char *>(p.nt + (size_t)(kNtG17 + r_end) * kNtEntries + lane * 16);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(g17));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(g17 + 128));
+                const char *gb = reinterpret_cast<const char *>(p.nt + (size_t)(kNtG18 + r_end) * kNtEntries + lane * 16);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(gb));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + 128));
             }
         } else if (r_end) {
             const char *ft = reinterpret_cast<const char *>(p.nt + (size_t)(kNtF + (r_end >> 4)) * kNtEntries + lane * 16);
@@ -292,8 +292,8 @@ __device__ __forceinline__ void gcm_rows(const KParamsT<INL> &p, uint64_t g, con
                 t0 = kNtLane + 17u;  // H^18
                 t1 = kNtLane + 1u;   // H^2
             } else if (short_tail) {
-                t0 = kNtG17 + r_end;  // H^(32 r_end + 17)
-                t1 = kNtG1 + r_end;   // H^(32 r_end + 1)
+                t0 = kNtG18 + r_end;  // H^(32 r_end + 18)
+                t1 = kNtG2 + r_end;   // H^(32 r_end + 2)
                 scaled = true;
             } else {
                 t0 = kNtLane + 16u;  // H^17
@@ -531,8 +531,9 @@ __global__ void k_setup_powers(const uint4 *hptr, uint4 *powers) {
     if (idx < kNtF) e = idx + 1;                                   // H^1..H^33
     else if (idx < kNtP32) e = 512ull * (idx - kNtF) + 1;          // F_a
     else if (idx < kNtG1) e = 32ull * (idx - kNtP32 + 1);          // H^(32b)
-    else if (idx < kNtG17) e = 32ull * (idx - kNtG1) + 1;          // short tails
-    else if (idx < kNumNt) e = 32ull * (idx - kNtG17) + 17;
+    else if (idx < kNtG2) e = 32ull * (idx - kNtG1) + 1;           // short tails
+    else if (idx < kNtG18) e = 32ull * (idx - kNtG2) + 2;
+    else if (idx < kNumNt) e = 32ull * (idx - kNtG18) + 18;
     else e = 32;                                                    // G
     powers[idx] = g_to_words(g_pow(h, e));
 }

@@ -41,11 +41,13 @@ constexpr uint32_t kNtF = 33;            // F_a = H^(512a+1), a < kNumF
 constexpr uint32_t kNtP32 = kNtF + kNumF;  // H^(32b), b = 1..15 -> kNtP32 + b - 1
 // Short tails: a run ending r_end < kNumG rows before its message's end
 // scales by H^(32 r_end + 1) in ONE lookup (instead of F then H^(32b)), and
-// the tree's last step folds that scaling in: D0 x H^(32 r_end + 17).
+// the tree's last step folds that scaling in: W = D0 H^17 + D1 H, so
+// W x H^(32 r_end + 1) = D0 x H^(32 r_end + 18) + D1 x H^(32 r_end + 2).
 constexpr uint32_t kNumG = 512;
 constexpr uint32_t kNtG1 = kNtP32 + 15;        // H^(32r + 1),  r < kNumG
-constexpr uint32_t kNtG17 = kNtG1 + kNumG;     // H^(32r + 17), r < kNumG
-constexpr uint32_t kNumNt = kNtG17 + kNumG;
+constexpr uint32_t kNtG2 = kNtG1 + kNumG;      // H^(32r + 2)
+constexpr uint32_t kNtG18 = kNtG2 + kNumG;     // H^(32r + 18)
+constexpr uint32_t kNumNt = kNtG18 + kNumG;
 constexpr uint32_t kNtEntries = 32 * 16;
 
 constexpr uint32_t kSmAes0 = 0;
