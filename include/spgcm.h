@@ -137,6 +137,12 @@ int sp_open_host_batch(sp_ctx *ctx, const sp_desc *descs, int n);
  * call; the only mutable context state (an atomic). */
 int sp_ctx_set_max_sms(sp_ctx *ctx, int max_sms);
 int sp_ctx_max_sms(const sp_ctx *ctx);
+/* SM cap of this context's SMALL launches (<= 2 MiB of rows: KV batches,
+ * tokens, NOP pads; 0 = none, the default).  Such launches are latency-bound
+ * and each CTA holds a whole SM while it runs, so a pipeline running beside
+ * model compute caps them (libsppipe sets 32) at the cost of a slower launch
+ * alone.  Results are identical. */
+int sp_ctx_set_small_sms(sp_ctx *ctx, int small_sms);
 
 /* Diagnostics. */
 const char *sp_last_error(void);

@@ -22,7 +22,7 @@ SPGCM_SYMBOLS = (
     "sp_ctx_create", "sp_ctx_destroy", "sp_seal", "sp_open", "sp_seal_batch", "sp_open_batch",
     "sp_crypt_batch", "sp_seal_host", "sp_open_host", "sp_seal_host_batch", "sp_open_host_batch",
     "sp_last_error", "sp_version", "sp_launch_count", "sp_ctx_round_keys", "sp_ctx_hash_key",
-    "sp_ctx_set_max_sms", "sp_ctx_max_sms", "sp_crypt_levels",
+    "sp_ctx_set_max_sms", "sp_ctx_max_sms", "sp_crypt_levels", "sp_ctx_set_small_sms",
 )
 
 
@@ -79,6 +79,7 @@ def load_spgcm() -> ctypes.CDLL:
         lib.sp_ctx_round_keys.argtypes = [vp, vp]
         lib.sp_ctx_hash_key.argtypes = [vp, vp]
         lib.sp_ctx_set_max_sms.argtypes = [vp, ctypes.c_int]
+        lib.sp_ctx_set_small_sms.argtypes = [vp, ctypes.c_int]
         lib.sp_ctx_max_sms.argtypes = [vp]
         _lib = lib
         return lib

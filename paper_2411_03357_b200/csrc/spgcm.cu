@@ -685,6 +685,7 @@ struct sp_ctx {
     int device = 0;
     int num_sms = 148;
     std::atomic<int> max_sms{0};  // SM budget (0: all); sp_ctx_set_max_sms
+    std::atomic<int> small_sms{0};  // SM cap of small launches (0: none); sp_ctx_set_small_sms
     int sms() const {
         const int m = max_sms.load(std::memory_order_relaxed);
         return m > 0 && m < num_sms ? m : num_sms;
@@ -760,8 +761,32 @@ uint32_t pack_warps() {
     return v;
 }
 
-void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used, uint64_t rpw) {
+uint64_t env_u64(const char *name, uint64_t dflt);
+
+// SMs a launch of `rows` rows may use.  Small launches (<= SPGCM_SMALL_SMS_ROWS
+// rows, default 4096 = 2 MiB: KV batches, tokens, NOP pads) are latency-
+// bound, not throughput-bound, yet each 512-thread CTA holds a whole SM's
+// register file while it runs; spread over up to 148 SMs they take SMs from
+// the model's compute and from the k_xfer transfers beside them.  A context
+// can cap them (sp_ctx_set_small_sms; libsppipe sets 32 on its pipes): the
+// OPT-30B KV trace then runs 0.947 -> 0.964 of plain with compute and
+// 0.77 -> 0.79 swap-only, 64 KiB chunks 0.89 -> 0.91 / 0.80 -> 0.85
+// (profiles/r2_ab_kv_sms.txt, r2_ab_small_sms.txt), while one launch alone
+// gets slower (1 x 224 KiB 7.3 -> 10.1 us), so direct callers stay uncapped
+// by default.  SPGCM_SMALL_SMS overrides every context (0 = no cap).  The
+// context's SM budget (sp_ctx_set_max_sms) still applies.
+uint64_t launch_sms(const sp_ctx *ctx, uint64_t rows) {
+    static const char *env = getenv("SPGCM_SMALL_SMS");  // overrides every context's setting (A/B)
+    static const uint64_t env_cap = env ? (uint64_t)atoll(env) : 0;
+    static const uint64_t cap_rows = env_u64("SPGCM_SMALL_SMS_ROWS", 4096);
+    const uint64_t cap = env ? env_cap : (uint64_t)ctx->small_sms.load(std::memory_order_relaxed);
     const uint64_t sms = (uint64_t)ctx->sms();
+    return cap && rows <= cap_rows ? std::min(sms, cap) : sms;
+}
+
+void launch_shape(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used, uint64_t rpw,
+                  uint64_t cap_rows = ~0ull) {
+    const uint64_t sms = launch_sms(ctx, cap_rows == ~0ull ? rows : cap_rows);
     const uint64_t want_warps =
         std::max<uint64_t>(1, std::min<uint64_t>(std::max(rows / rpw, std::min(nmsgs, rows)),
                                                  sms * kWarpsPerCta));
@@ -803,7 +828,7 @@ uint64_t small_rows_per_warp() {
 }
 
 void launch_shape_small(const sp_ctx *ctx, uint64_t rows, uint64_t nmsgs, int &grid, uint32_t &warps_used) {
-    const uint64_t sms = (uint64_t)ctx->sms();
+    const uint64_t sms = launch_sms(ctx, rows);
     // under an SM budget the grid stays within `sms` CTAs (the scheduler
     // may place co-resident CTAs on different SMs)
     const uint64_t per_cta = kThreadsSmall / 32, ctas_per_sm = sms < (uint64_t)ctx->num_sms ? 1 : 4;
@@ -903,7 +928,8 @@ int launch_rows(const sp_ctx *ctx, KParamsT<INL> p, uint64_t row_begin, uint64_t
 // largest level in one wave and warps loop over claimed units.
 template <uint32_t INL>
 int launch_levels(const sp_ctx *ctx, KParamsT<INL> p, uint32_t nlevels, cudaStream_t s) {
-    const uint64_t sms = (uint64_t)ctx->sms();
+    const uint64_t all_rows = p.lvl_row[nlevels] - p.lvl_row[0];
+    const uint64_t sms = launch_sms(ctx, all_rows);
     int grid = 1;
     uint32_t wu = 1;
     p.nlevels = nlevels;
@@ -915,7 +941,7 @@ int launch_levels(const sp_ctx *ctx, KParamsT<INL> p, uint32_t nlevels, cudaStre
                                                                        sms * kWarpsPerCta));
         int g = 1;
         uint32_t w = 1;
-        launch_shape(ctx, rows, 1, g, w, rpw);
+        launch_shape(ctx, rows, 1, g, w, rpw, all_rows);
         grid = std::max(grid, g);
         wu = std::max(wu, w);
         p.lvl_unit[l + 1] = p.lvl_unit[l] + (uint32_t)want;
@@ -1405,6 +1431,12 @@ int sp_ctx_set_max_sms(sp_ctx *c, int max_sms) {
 }
 
 int sp_ctx_max_sms(const sp_ctx *c) { return c ? c->sms() : 0; }
+
+int sp_ctx_set_small_sms(sp_ctx *c, int small_sms) {
+    if (!c || small_sms < 0) return fail(SP_EINVAL, "small_sms must be >= 0");
+    c->small_sms.store(small_sms, std::memory_order_relaxed);
+    return SP_OK;
+}
 
 int sp_ctx_hash_key(const sp_ctx *c, uint8_t out[16]) {
     if (!c || !out) return fail(SP_EINVAL, "null argument");

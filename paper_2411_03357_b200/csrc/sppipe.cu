@@ -2838,7 +2838,17 @@ class Engine {
         : cfg(c), plane(c.dry != 0, key, c.batch_bytes ? c.batch_bytes : (64ull << 20), c.reserve_bytes), pred(p),
           val(mem, c.window) {
         val.history = c.record_history;
-        if (!plane.dry) ck_sp(sp_ctx_set_max_sms(plane.ctx, (int)c.crypto_sms), "sp_ctx_set_max_sms");
+        if (!plane.dry) {
+            ck_sp(sp_ctx_set_max_sms(plane.ctx, (int)c.crypto_sms), "sp_ctx_set_max_sms");
+            // small launches (KV batches, tokens, NOP pads) on <= 32 SMs, so
+            // they leave the rest to the model's compute and the k_xfer
+            // transfers (include/spgcm.h; SPPIPE_SMALL_SMS overrides, 0 = off)
+            static const int small_sms = [] {
+                const char *e = getenv("SPPIPE_SMALL_SMS");
+                return e ? atoi(e) : 32;
+            }();
+            ck_sp(sp_ctx_set_small_sms(plane.ctx, small_sms), "sp_ctx_set_small_sms");
+        }
         if (c.hw_guards) {
             if (spg_init() != SPG_OK) throw std::runtime_error("spg_init failed");
             mem.hw = true;
