@@ -150,6 +150,10 @@ class GcmContext:
     def max_sms(self) -> int:
         return int(self._lib.sp_ctx_max_sms(self._h))
 
+    def set_small_sms(self, small_sms: int) -> None:
+        """SM cap of this context's small (<= 2 MiB) launches (0: none)."""
+        _check(self._lib.sp_ctx_set_small_sms(self._h, int(small_sms)), "sp_ctx_set_small_sms")
+
     def seal_batch(self, items: Sequence[tuple], stream=None) -> None:
         """items: (dir, iv, src, dst, tag) with device tensors (or int
         pointers + explicit len via a 6th element)."""

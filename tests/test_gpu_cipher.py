@@ -505,3 +505,24 @@ def test_fused_levels_rejects_bad_layout(ctx_for, torch_cuda):
     for starts in ([0, 0, 2], [1, 2], [0, 1]):
         arr = (ctypes.c_int * len(starts))(*starts)
         assert lib.sp_crypt_levels(ctx._h, descs, 2, arr, len(starts) - 1, None) == _native.SP_EINVAL
+
+
+def test_small_sms_cap_same_bytes(ctx_for, torch_cuda):
+    """sp_ctx_set_small_sms changes only where small launches run: a KV-sized
+    batch sealed capped at 8 SMs is bit-identical to the oracle."""
+    torch = torch_cuda
+    from paper_2411_03357_b200.gcm import GcmContext
+
+    rng = random.Random(11)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = GcmContext(key)
+    ctx.set_small_sms(8)
+    plains = [rng.randbytes(229_376) for _ in range(4)] + [rng.randbytes(2048), b"\x00"]
+    srcs = [_dev(torch, p) for p in plains]
+    dsts = [torch.empty_like(s) for s in srcs]
+    tags = torch.zeros((len(plains), 16), dtype=torch.uint8, device="cuda")
+    ctx.seal_batch([(0, 50 + i, srcs[i], dsts[i], tags[i]) for i in range(len(plains))])
+    torch.cuda.synchronize()
+    for i, p in enumerate(plains):
+        assert (_host(dsts[i]), _host(tags[i])) == oracle_port.seal(key, 0, 50 + i, p), i
+    ctx.set_small_sms(0)
