@@ -628,6 +628,7 @@ class Validator {
 // ---- data plane -----------------------------------------------------------------------
 struct Streams {
     cudaStream_t comp, spec, h2d, d2h, land, host, out;  // host: ordered app writes; out: swap-out seals
+    cudaStream_t spec_h2d;  // encrypt-ahead staging copies (SPPIPE_SPEC_H2D=0: they use h2d)
     cudaStream_t comp2;  // consecutive flushes alternate between comp and comp2
     cudaStream_t app;    // the model's compute (trace ComputeEvents)
 };
@@ -702,7 +703,7 @@ Streams streams_for(int dev) {
     int lo = 0, hi = 0;
     ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
     const int plane_prio = (mode == 0 || mode == 3) ? hi : lo, app_prio = mode == 1 ? hi : lo;
-    cudaStream_t *all[8] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2};
+    cudaStream_t *all[9] = {&s.comp, &s.spec, &s.h2d, &s.d2h, &s.land, &s.host, &s.out, &s.comp2, &s.spec_h2d};
     for (auto p : all)
         ck(cudaStreamCreateWithPriority(p, cudaStreamNonBlocking, (mode == 3 && p == &s.spec) ? lo : plane_prio),
            "cudaStreamCreate");
@@ -762,6 +763,7 @@ struct CopyBatch {
     std::vector<BufP> keep;     // staging buffers, alive until issued
     std::vector<FenceP> waits;  // host blocks' landings that must precede the reads
     FenceP fence;
+    cudaStream_t stream = nullptr;  // copy stream (null: the plane's h2d stream)
     bool empty() const { return n.empty(); }
 };
 
@@ -1878,18 +1880,19 @@ class Plane {
     // Issue a gathered batch of H2D staging copies on the copy stream.
     void issue(CopyBatch &cb) {
         if (cb.empty()) return;
+        const cudaStream_t st = cb.stream ? cb.stream : s.h2d;
         std::unordered_set<Fence *> seen;
         for (auto &f : cb.waits)
-            if (f && seen.insert(f.get()).second) wait(s.h2d, f);
-        copy_batch(s.h2d, true, cb.n.size(), [&](size_t i, void *&dst, void *&src, size_t &n) {
+            if (f && seen.insert(f.get()).second) wait(st, f);
+        copy_batch(st, true, cb.n.size(), [&](size_t i, void *&dst, void *&src, size_t &n) {
             dst = cb.dst[i];
             src = cb.src[i];
             n = cb.n[i];
         });
-        record(cb.fence, s.h2d, "rec_copy");
-        if (dbg_times()) dbg_log.push_back({"h2d-copy", s.h2d, cb.fence, dbg_computes});
+        record(cb.fence, st, "rec_copy");
+        if (dbg_times()) dbg_log.push_back({"h2d-copy", st, cb.fence, dbg_computes});
         ++tick;
-        for (auto &b : cb.keep) b->use(s.h2d, cb.fence, tick);
+        for (auto &b : cb.keep) b->use(st, cb.fence, tick);
         cb.dst.clear();
         cb.src.clear();
         cb.n.clear();
@@ -2078,7 +2081,7 @@ class Plane {
         uint64_t first = spans[0].first;
         auto it = host_ready.find(b.id);
         if (it != host_ready.end() && it->second) cb.waits.push_back(it->second);
-        BufP buf = alloc(round16(total) + kTag * spans.size(), s.h2d);
+        BufP buf = alloc(round16(total) + kTag * spans.size(), cb.stream ? cb.stream : s.h2d);
         if (!cb.fence) cb.fence = new_fence();
         cb.dst.push_back(buf->ptr);
         cb.src.push_back(b.host + inner + first);
@@ -2184,6 +2187,20 @@ class Plane {
         CopyBatch copies;
         explicit SpecBatch(Plane *pl) : p(pl) {
             if (!p->dry) ready = p->new_fence();
+            if (spec_h2d_enabled()) copies.stream = p->s.spec_h2d;
+        }
+        // Encrypt-ahead staging copies run on their own copy stream, so the
+        // demand (on-the-fly) copies on h2d never queue behind them and the
+        // two streams' small-copy k_xfer launches overlap: KV trace swap-only
+        // 0.80 -> 0.82 of plain in three alternating A/B pairs, unchanged
+        // with compute and within noise on the 32 MiB-chunk traces
+        // (profiles/r2_ab_spec_h2d.txt).  SPPIPE_SPEC_H2D=0 restores h2d.
+        static bool spec_h2d_enabled() {
+            static const bool on = [] {
+                const char *e = getenv("SPPIPE_SPEC_H2D");
+                return !(e && e[0] == '0');
+            }();
+            return on;
         }
         ~SpecBatch() {
             if (p->spec_copies == &copies) p->spec_copies = nullptr;
@@ -2517,7 +2534,7 @@ class Plane {
     void finish_streams() {
         flush();
         iss.drain();
-        cudaStream_t all[9] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out, s.comp2, s.app};
+        cudaStream_t all[10] = {s.comp, s.spec, s.land, s.h2d, s.d2h, s.host, s.out, s.comp2, s.app, s.spec_h2d};
         for (auto st : all) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
 
