@@ -2185,16 +2185,18 @@ class Plane {
         FenceP ready;
         FenceP last_copy;
         CopyBatch copies;
+        bool stream_set = false;
         explicit SpecBatch(Plane *pl) : p(pl) {
             if (!p->dry) ready = p->new_fence();
-            if (spec_h2d_enabled()) copies.stream = p->s.spec_h2d;
         }
-        // Encrypt-ahead staging copies run on their own copy stream, so the
-        // demand (on-the-fly) copies on h2d never queue behind them and the
-        // two streams' small-copy k_xfer launches overlap: KV trace swap-only
-        // 0.80 -> 0.82 of plain in three alternating A/B pairs, unchanged
-        // with compute and within noise on the 32 MiB-chunk traces
-        // (profiles/r2_ab_spec_h2d.txt).  SPPIPE_SPEC_H2D=0 restores h2d.
+        // Small encrypt-ahead staging copies (<= 2 MiB, the k_xfer class) run
+        // on their own copy stream, so the demand (on-the-fly) copies on h2d
+        // never queue behind them and the two streams' k_xfer launches
+        // overlap: KV trace swap-only 0.80 -> 0.82 of plain in three
+        // alternating A/B pairs, unchanged with compute
+        // (profiles/r2_ab_spec_h2d.txt).  Big ones stay on h2d: on a second
+        // copy engine they split PCIe with the demand copies (activation
+        // trace, 28 MiB chunks: 0.985 -> 0.954).  SPPIPE_SPEC_H2D=0: all on h2d.
         static bool spec_h2d_enabled() {
             static const bool on = [] {
                 const char *e = getenv("SPPIPE_SPEC_H2D");
@@ -2219,6 +2221,13 @@ class Plane {
             }
             FenceP done;
             p->spec_copies = &copies;  // a flush while this batch is built issues its copies first
+            if (!stream_set) {  // the batch's copy stream, once, by its first chunk's size
+                // (one stream per batch: launch() waits only for the last copy)
+                uint64_t n = 0;
+                for (auto &sp : spans) n += sp.second;
+                copies.stream = spec_h2d_enabled() && n <= p->xfer_max() ? p->s.spec_h2d : nullptr;
+                stream_set = true;
+            }
             BufP buf = p->stage_h2d(b, inner, spans, done, copies);
             last_copy = done;
             uint64_t first = spans[0].first, total = 0;
