@@ -1459,6 +1459,7 @@ int sp_crypt_batch(sp_ctx *ctx, const sp_desc *d, int n, sp_stream_t stream) {
 int sp_crypt_levels(sp_ctx *ctx, const sp_desc *d, int n, const int *level_start, int nlevels,
                     sp_stream_t stream) {
     if (!ctx) return fail(SP_EINVAL, "null context");
+    if (!d || n <= 0) return fail(SP_EINVAL, "null or empty descriptor array");
     if (nlevels < 1 || !level_start) return fail(SP_EINVAL, "need at least one level");
     if (level_start[0] != 0 || level_start[nlevels] != n) return fail(SP_EINVAL, "levels must cover the batch");
     for (int l = 0; l < nlevels; ++l)

@@ -505,6 +505,8 @@ def test_fused_levels_rejects_bad_layout(ctx_for, torch_cuda):
     for starts in ([0, 0, 2], [1, 2], [0, 1]):
         arr = (ctypes.c_int * len(starts))(*starts)
         assert lib.sp_crypt_levels(ctx._h, descs, 2, arr, len(starts) - 1, None) == _native.SP_EINVAL
+    arr = (ctypes.c_int * 2)(0, 0)
+    assert lib.sp_crypt_levels(ctx._h, descs, 0, arr, 1, None) == _native.SP_EINVAL  # empty batch
 
 
 def test_small_sms_cap_same_bytes(ctx_for, torch_cuda):
