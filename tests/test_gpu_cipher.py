@@ -528,3 +528,57 @@ def test_small_sms_cap_same_bytes(ctx_for, torch_cuda):
     for i, p in enumerate(plains):
         assert (_host(dsts[i]), _host(tags[i])) == oracle_port.seal(key, 0, 50 + i, p), i
     ctx.set_small_sms(0)
+
+
+def test_fused_levels_concurrent_streams_under_load(ctx_for, torch_cuda):
+    """sp_crypt_levels on two streams at once while a matmul keeps the SMs
+    busy: every unit of level l waits in-kernel for level l-1, and each
+    stream's control words are its own — all results still match the oracle."""
+    import ctypes
+
+    from paper_2411_03357_b200 import _native
+
+    torch = torch_cuda
+    rng = random.Random(99)
+    key = bytes(rng.randrange(256) for _ in range(32))
+    ctx = ctx_for(key)
+    lib = _native.load_spgcm()
+    per_level, nlevels = 8, 4
+    n = per_level * nlevels
+    setups = []
+    for sidx in range(2):
+        sizes = [rng.choice([17, 2048, 229_376, 65_536]) for _ in range(per_level)]
+        plains = [rng.randbytes(sz) for sz in sizes]
+        bufs = [[_dev(torch, p)] + [torch.full((sz,), 0xAB, dtype=torch.uint8, device="cuda") for _ in range(nlevels)]
+                for p, sz in zip(plains, sizes)]
+        tags = torch.zeros((nlevels, per_level, 16), dtype=torch.uint8, device="cuda")
+        status = torch.full((n,), 7, dtype=torch.int32, device="cuda")
+        descs = (_native.SpDesc * n)()
+        for lv in range(nlevels):
+            for i in range(per_level):
+                d = descs[lv * per_level + i]
+                opening = lv % 2 == 1
+                d.dir, d.reserved, d.iv, d.len = 0, int(opening), 100 * sidx + 10 * (lv // 2) + i, sizes[i]
+                d.src, d.dst = bufs[i][lv].data_ptr(), bufs[i][lv + 1].data_ptr()
+                d.tag = tags[lv - 1 if opening else lv, i].data_ptr()
+                d.status = status.data_ptr() + 4 * (lv * per_level + i)
+        starts = (ctypes.c_int * (nlevels + 1))(*[lv * per_level for lv in range(nlevels + 1)])
+        setups.append((torch.cuda.Stream(), plains, bufs, tags, status, descs, starts, sidx))
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(4):
+        a = a @ a  # keeps SMs busy on the default stream while the fused launches run
+        for st, _, _, _, _, descs, starts, _ in setups:
+            for _ in range(10):
+                rc = lib.sp_crypt_levels(ctx._h, descs, n, starts, nlevels, ctypes.c_void_p(st.cuda_stream))
+                assert rc == 0, _native.last_error()
+    torch.cuda.synchronize()
+    for _, plains, bufs, tags, status, _, _, sidx in setups:
+        assert status.cpu().tolist() == [7] * per_level + [0] * per_level + [7] * per_level + [0] * per_level
+        for lv in range(nlevels):
+            for i, p in enumerate(plains):
+                out = _host(bufs[i][lv + 1])
+                if lv % 2 == 0:
+                    want = oracle_port.seal(key, 0, 100 * sidx + 10 * (lv // 2) + i, p)
+                    assert (out, _host(tags[lv, i])) == want, (sidx, lv, i)
+                else:
+                    assert out == p, (sidx, lv, i)
