@@ -1668,7 +1668,7 @@ class Plane {
                 }
             }
             auto &descs = descs_scratch;
-            if (top >= 1 && top < (int)kFuseLevels && q.size() <= kLaunchMsgs) {
+            if (fuse_levels() && top >= 1 && top < (int)kFuseLevels && q.size() <= kLaunchMsgs) {
                 // the flush's dependent levels in ONE launch (sp_crypt_levels):
                 // level l starts inside the kernel once level l-1 is done, no
                 // launch boundary per level.  Every op's input fence is waited
@@ -2057,6 +2057,21 @@ class Plane {
     }
 
     static constexpr size_t kFuseLevels = 8;
+    // SPPIPE_FUSE_LEVELS=1: multi-level flushes as one sp_crypt_levels launch.
+    // Off by default: one launch per level with programmatic dependent launch
+    // is faster (a KV seal -> open flush: 15.6 vs 18.5 us for one 224 KiB
+    // block, 25.3 vs 31.6 us for eight, profiles/r2_levels_probe.txt; the
+    // traces are neutral, r2_ab_fuse_levels.txt): the next grid's CTAs are
+    // already resident with their tables filled when the level boundary
+    // comes, while the in-kernel hand-off pays a claim, an acquire poll and
+    // an exit round trip per warp.
+    static bool fuse_levels() {
+        static const bool on = [] {
+            const char *e = getenv("SPPIPE_FUSE_LEVELS");
+            return e && e[0] == '1';
+        }();
+        return on;
+    }
     void post_levels(const std::vector<sp_desc> &d, std::vector<int> starts, cudaStream_t st) {
         sp_ctx *c = ctx;
         iss.post([c, st, d = std::vector<sp_desc>(d), starts = std::move(starts)] {
