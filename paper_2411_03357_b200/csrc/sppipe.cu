@@ -1787,6 +1787,18 @@ class Plane {
         }();
         return on;
     }
+    // Smallest message whose landing open follows its seal on the out stream.
+    // Without model compute 4 MiB (small KV opens there queue behind the next
+    // decode step's seals: KV swap-only 0.79 vs 0.76 with every landing on
+    // out).  Once the model's compute shares the GPU, every size: the open
+    // then follows its seal on one stream instead of a cross-stream hop (KV
+    // with compute 0.963 -> 0.970 in four A/B pairs, profiles/r2_ab_land_small.txt).
+    // SPPIPE_LAND_ON_OUT_MIN=<bytes> fixes it either way.
+    uint64_t land_on_out_min() const {
+        static const char *e = getenv("SPPIPE_LAND_ON_OUT_MIN");
+        if (e) return (uint64_t)atoll(e);
+        return app_fence ? 0 : (4ull << 20);
+    }
     void flush_landings() {
         std::vector<Landing> ls;
         ls.swap(landings);
@@ -1803,7 +1815,7 @@ class Plane {
             for (auto &j : l.jobs) {
                 const MsgP &m = std::get<0>(j);
                 total += m->len;
-                if (!m->ready || !m->ready->recorded || m->ready->stream != s.out || m->len < (4ull << 20)) on_out = false;
+                if (!m->ready || !m->ready->recorded || m->ready->stream != s.out || m->len < land_on_out_min()) on_out = false;
             }
         const cudaStream_t ls_st = on_out ? s.out : s.land;
         const uint64_t mk_ready = ++mark_seq;

@@ -365,7 +365,8 @@ def test_random_traces_match_reference_gpu():
 @pytest.mark.parametrize("switch", ["SPPIPE_EAGER_OPEN=0", "SPPIPE_SLAB=0", "SPPIPE_OUT_STREAM=1", "SPPIPE_ASYNC_ISSUE=0", "SPPIPE_COMP_STREAMS=1",
                                     "SPPIPE_XFER_MAX=0", "SPPIPE_XFER_MAX=1099511627776", "SPPIPE_FUSE_H2D=1", "SPPIPE_LAND_ON_OUT=0",
                                     "SPPIPE_FUSE_LEVELS=1", "SPGCM_TREE_WARPS=0", "SPGCM_TREE_WARPS=1000000000",
-                                    "SPPIPE_SMALL_SMS=0", "SPPIPE_SPEC_H2D=0"])
+                                    "SPPIPE_SMALL_SMS=0", "SPPIPE_SPEC_H2D=0",
+                                    "SPPIPE_LAND_ON_OUT_MIN=0"])
 def test_native_parity_under_data_plane_switches_gpu(switch):
     """The data-plane switches (drain-time opens, pool-only buffers, own-stream
     swap-out seals, copy-engine-only transfers, SM (k_xfer) transfers of every copy,
